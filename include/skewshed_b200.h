@@ -1,0 +1,206 @@
+/*
+ * skewshed_b200 — C ABI of the B200-native sDEM total-viewshed path.
+ *
+ * This is the drop-in boundary. Every entry point takes plain
+ * pointers and sizes, returns an sks_status, and never lets a C++ exception
+ * cross the ABI; the message of the last failure on the calling thread is in
+ * sks_last_error(). The C++ facade in skewshed_b200.hpp restores the
+ * reference's signatures and exception types on top of this header.
+ *
+ * Citations are to the reference (/root/reference/proj/...) entry point each
+ * function replaces.
+ *
+ * Memory: functions named *_host take host buffers (the library owns all
+ * device memory for the call). Functions taking a `void* stream` and `d_`
+ * pointers work on caller-owned device memory on that CUDA stream.
+ */
+#ifndef SKEWSHED_B200_H
+#define SKEWSHED_B200_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef enum {
+  SKS_OK = 0,
+  SKS_INVALID_ARGUMENT = 1, /* std::invalid_argument in the reference */
+  SKS_OUT_OF_RANGE = 2,     /* std::out_of_range */
+  SKS_CUDA_ERROR = 3,
+  SKS_NCCL_ERROR = 4,
+  SKS_INTERNAL = 5 /* std::runtime_error */
+} sks_status;
+
+enum { SKS_UNITS_M2 = 0, SKS_UNITS_KM2 = 1 };
+enum { SKS_SCAN_FORWARD = 0, SKS_SCAN_BACKWARD = 1 };
+enum { SKS_NO_DISTANCE_CAP = 2147483647 }; /* scan.hpp:15 kNoDistanceCap */
+
+/* RunConfig, dem.hpp:40-46. std::optional<double> max_distance becomes a
+ * double with 0 = off (the CLI's own convention, cli.cpp:82,112); Units
+ * becomes an int; `workers` has no meaning on a GPU and is replaced by the
+ * CUDA device ordinal. */
+typedef struct {
+  int ns;              /* sector count over 2*pi, even >= 2 */
+  double h0;           /* observer height above ground, m, >= 0 */
+  double max_distance; /* visibility cap in m; 0 = off */
+  int units;           /* SKS_UNITS_M2 or SKS_UNITS_KM2 */
+  int device;          /* CUDA device ordinal */
+} sks_run_config;
+
+/* EngineStats, engine.hpp:25-32, plus GPU evidence. Phase seconds are
+ * CUDA-event durations on the library's stream; total_seconds is host wall
+ * time of the call. */
+typedef struct {
+  double skew_seconds;   /* relocation kernels (DEM -> sDEM) */
+  double scan_seconds;   /* line-of-sight scan kernels */
+  double fixup_seconds;  /* exact FP64 re-scan of guard-flagged POV groups */
+  double unskew_seconds; /* unskew + ordered accumulation kernels */
+  double reduce_seconds; /* scaling (+ collective when sharded) */
+  double total_seconds;
+  int sectors;
+  int batches;
+  long long kernel_launches;   /* our kernels launched during the call */
+  long long target_evals;      /* exact sum of scanned targets */
+  long long flagged_groups;    /* POV groups re-run by the exact fixup */
+  long long h2d_bytes;
+  long long d2h_bytes;
+} sks_stats;
+
+/* SectorPlan, skew.hpp:29-41. ops: 0 Transpose, 1 FlipCols, 2 FlipRows. */
+typedef struct {
+  int sector_index;
+  int ns;
+  double sector_deg;
+  double shear_deg;
+  double shear_tan;
+  int n_ops;
+  int ops[3];
+  int rows, cols;         /* grid shape after pre_ops */
+  int src_rows, src_cols; /* DEM shape */
+  int to_source[6];       /* IndexMap ii, ij, ci, ji, jj, cj */
+  int base;               /* sDEM row offset (skew.cpp:16-19) */
+  int skw_rows;           /* base + rows */
+} sks_sector_plan;
+
+/* Message of the last failing call on this thread ("" if none). */
+const char* sks_last_error(void);
+/* Library version string. */
+const char* sks_version(void);
+/* Number of visible CUDA devices (0 on a host without a GPU). */
+int sks_device_count(void);
+
+/* ---- host planning (no GPU needed) ---------------------------------- */
+
+/* plan_sector, skew.cpp:23-95 (also fills base/skw_rows). */
+sks_status sks_plan_sector(int k, int ns, int dimy, int dimx,
+                           sks_sector_plan* out);
+/* shear_params, skew.cpp:97-101. */
+void sks_shear_params(double shear_tan, int j, int* dest, double* frac);
+/* distance_cap_cells, engine.cpp:29-36 (max_distance 0 = off). */
+int sks_distance_cap_cells(double max_distance, double shear_tan,
+                           double cellsize);
+/* area_scale_factor, engine.cpp:103-107. */
+double sks_area_scale_factor(int ns, double cellsize, int units);
+/* row_ranges of build_skw (skew.cpp:185-195) computed from the plan alone
+ * (the weights do not depend on elevations). ranges: 2*skw_rows ints. */
+sks_status sks_row_ranges(int rows, int cols, double shear_tan, int* ranges,
+                          int* skw_rows_out);
+/* Exact number of target evaluations of sector k (sum over skewed rows and
+ * POVs of the forward+backward scan lengths, capped by max_dd). */
+long long sks_sector_target_evals(int k, int ns, int dimy, int dimx,
+                                  double cellsize, double max_distance);
+/* Static sector-to-rank assignment (longest-processing-time first on the
+ * exact per-sector work). owner: ns/2 ints. */
+sks_status sks_partition_sectors(int ns, int dimy, int dimx, double cellsize,
+                                 double max_distance, int world, int* owner);
+/* make_synthetic, dem.cpp:118-173 (kind 0 Flat, 1 Ramp, 2 Cone,
+ * 3 SmoothedNoise) plus kind 4 Fractal (diamond-square). */
+sks_status sks_make_synthetic(int kind, int dimy, int dimx, uint32_t seed,
+                              float* out);
+/* validate(Dem) + has_nodata_cells + validate(RunConfig), dem.cpp:16-87
+ * (engine.cpp:68-81 require_valid). nodata: pointer to the nodata value or
+ * NULL. */
+sks_status sks_validate(const float* dem, int dimy, int dimx, double cellsize,
+                        const float* nodata, const sks_run_config* cfg);
+
+/* ---- end-to-end (host buffers) -------------------------------------- */
+
+/* total_viewshed, engine.cpp:222-233: out_vs (dimy*dimx doubles) receives
+ * the per-cell viewshed area in cfg->units. */
+sks_status sks_total_viewshed(const float* dem, int dimy, int dimx,
+                              double cellsize, const sks_run_config* cfg,
+                              double* out_vs, sks_stats* stats);
+/* total_viewshed_raw, engine.cpp:109-220 (pre-scaling accumulator). */
+sks_status sks_total_viewshed_raw(const float* dem, int dimy, int dimx,
+                                  double cellsize, const sks_run_config* cfg,
+                                  double* out_raw, sks_stats* stats);
+/* sector_sweep, engine.cpp:235-244: one sector's unskewed contribution. */
+sks_status sks_sector_sweep(const float* dem, int dimy, int dimx,
+                            double cellsize, const sks_run_config* cfg, int k,
+                            double* out_contribution);
+
+/* ---- per-phase entry points (host buffers; parity and debugging) ---- */
+
+/* apply_pre_ops + build_skw, skew.cpp:103-196, for sector k of ns:
+ * values ((base+rows) x cols floats, every cell) and ranges (2*skw_rows). */
+sks_status sks_build_sector_sdem(const float* dem, int dimy, int dimx, int k,
+                                 int ns, int device, float* values,
+                                 int* ranges);
+/* build_skw, skew.cpp:144-196, on a grid already in pre_ops space. */
+sks_status sks_build_skw(const float* g, int rows, int cols, double shear_tan,
+                         int device, float* values, int* ranges,
+                         int* base_out);
+/* sector_viewshed, scan.cpp:64-85. out: skw_rows*cols doubles. cv_fwd and
+ * cv_bwd (optional, skw_rows*cols ints) receive the per-direction ring sums.
+ */
+sks_status sks_sector_viewshed(const float* values, const int* ranges,
+                               int skw_rows, int cols, double shear_tan,
+                               double h0, int max_dd, int device, double* out,
+                               int* cv_fwd, int* cv_bwd);
+/* linear_viewshed_row, scan.cpp:8-62, evaluated by the GPU scan kernel for
+ * one POV with absolute observer height h. visible_out (optional) receives
+ * one byte per scanned target. */
+sks_status sks_linear_viewshed_row(const float* row, int n, int first,
+                                   int last, int j0, double h,
+                                   int dir, int max_dd, int device,
+                                   double* cv_out, uint8_t* visible_out,
+                                   int* n_visible);
+/* unskew_accumulate, skew.cpp:204-263: out (dimy*dimx) += unskewed skw_vs. */
+sks_status sks_unskew_accumulate(const double* skw_vs, int skw_rows, int cols,
+                                 int k, int ns, int dimy, int dimx, int device,
+                                 double* out);
+
+/* ---- device-resident context (one per GPU; sector sharding) ---------- */
+
+typedef struct sks_context sks_context;
+
+sks_status sks_context_create(int device, sks_context** out);
+void sks_context_destroy(sks_context* ctx);
+/* Runs sectors[0..n) (any order given; accumulated in ascending k) of the
+ * total viewshed for the device-resident DEM d_dem and ADDS their raw
+ * contributions into the device map d_map (dimy*dimx doubles), all on
+ * `stream` (cudaStream_t). Asynchronous with respect to the host unless
+ * stats is non-NULL (then it synchronises to read the phase events). */
+sks_status sks_context_run_sectors(sks_context* ctx, const float* d_dem,
+                                   int dimy, int dimx, double cellsize,
+                                   const sks_run_config* cfg,
+                                   const int* sectors, int n_sectors,
+                                   double* d_map, void* stream,
+                                   sks_stats* stats);
+/* d_map[i] *= area_scale_factor(ns, cellsize, units) on `stream`. */
+sks_status sks_context_scale(sks_context* ctx, double* d_map, long long n,
+                             int ns, double cellsize, int units,
+                             void* stream);
+/* Total viewshed through the context with host buffers (the e2e path). */
+sks_status sks_context_total_viewshed(sks_context* ctx, const float* dem,
+                                      int dimy, int dimx, double cellsize,
+                                      const sks_run_config* cfg, int raw,
+                                      double* out, sks_stats* stats);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* SKEWSHED_B200_H */

@@ -1,0 +1,344 @@
+// TEST INFRASTRUCTURE ONLY — never linked into the product library.
+//
+// extern "C" shim over the UNMODIFIED reference library (skewshed, built from
+// /root/reference/proj/src by oracle/Makefile into oracle/_ref/). It lets the
+// Python tests, golden-fixture generator and bench.py's CPU baseline call the
+// reference's own public API through ctypes with plain pointers. Every entry
+// point forwards to one reference function; the citation names it.
+//
+// Only tests/, __graft_entry__.smoke() and bench.py's reference/cpu_baseline
+// legs may load this library.
+
+#include <algorithm>
+#include <atomic>
+#include <chrono>
+#include <cmath>
+#include <cstdint>
+#include <cstring>
+#include <exception>
+#include <string>
+#include <thread>
+#include <vector>
+
+#include "skewshed/dem.hpp"
+#include "skewshed/engine.hpp"
+#include "skewshed/oracle.hpp"
+#include "skewshed/scan.hpp"
+#include "skewshed/skew.hpp"
+
+using namespace skewshed;
+
+namespace {
+
+thread_local std::string g_err;
+
+Dem make_dem(const float* v, int dimy, int dimx, double cellsize) {
+  Dem dem;
+  dem.cellsize = cellsize;
+  dem.values.reset(dimy, dimx, 0.0f);
+  std::memcpy(dem.values.data().data(), v,
+              sizeof(float) * static_cast<size_t>(dimy) * dimx);
+  return dem;
+}
+
+RunConfig make_cfg(int ns, double h0, int workers, double max_distance,
+                   int units) {
+  RunConfig cfg;
+  cfg.ns = ns;
+  cfg.h0 = h0;
+  cfg.workers = workers;
+  if (max_distance > 0.0) cfg.max_distance = max_distance;
+  cfg.units = units == 1 ? Units::SquareKilometers : Units::SquareMeters;
+  return cfg;
+}
+
+template <typename Fn>
+int guarded(Fn&& fn) {
+  try {
+    fn();
+    return 0;
+  } catch (const std::invalid_argument& e) {
+    g_err = e.what();
+    return 1;
+  } catch (const std::out_of_range& e) {
+    g_err = e.what();
+    return 2;
+  } catch (const std::exception& e) {
+    g_err = e.what();
+    return 5;
+  }
+}
+
+}  // namespace
+
+extern "C" {
+
+const char* ref_last_error() { return g_err.c_str(); }
+
+// dem.cpp:118-173 make_synthetic
+int ref_make_synthetic(int kind, int dimy, int dimx, double cellsize,
+                       uint32_t seed, float* out) {
+  return guarded([&] {
+    Dem d = make_synthetic(static_cast<SyntheticKind>(kind), dimy, dimx,
+                           cellsize, seed);
+    std::memcpy(out, d.values.data().data(),
+                sizeof(float) * static_cast<size_t>(dimy) * dimx);
+  });
+}
+
+// skew.cpp:23-95 plan_sector. ops_out: up to 3 AxisOp codes
+// (0 Transpose, 1 FlipCols, 2 FlipRows); map_out: ii,ij,ci,ji,jj,cj.
+int ref_plan_sector(int k, int ns, int dimy, int dimx, double* degs_out,
+                    int* shape_out, int* map_out, int* ops_out,
+                    int* n_ops_out) {
+  return guarded([&] {
+    SectorPlan p = plan_sector(k, ns, dimy, dimx);
+    degs_out[0] = p.sector_deg;
+    degs_out[1] = p.shear_deg;
+    degs_out[2] = p.shear_tan;
+    shape_out[0] = p.rows;
+    shape_out[1] = p.cols;
+    const IndexMap& m = p.to_source;
+    int mm[6] = {m.ii, m.ij, m.ci, m.ji, m.jj, m.cj};
+    std::memcpy(map_out, mm, sizeof(mm));
+    *n_ops_out = static_cast<int>(p.pre_ops.size());
+    for (size_t i = 0; i < p.pre_ops.size(); ++i) {
+      ops_out[i] = static_cast<int>(p.pre_ops[i]);
+    }
+  });
+}
+
+// skew.cpp:97-101 shear_params
+void ref_shear_params(double shear_tan, int j, int* dest, double* frac) {
+  ShearParams sp = shear_params(shear_tan, j);
+  *dest = sp.dest;
+  *frac = sp.frac;
+}
+
+// skew.cpp:103-136 apply_pre_ops for sector k's plan
+int ref_apply_pre_ops(const float* dem, int dimy, int dimx, int k, int ns,
+                      float* out) {
+  return guarded([&] {
+    SectorPlan p = plan_sector(k, ns, dimy, dimx);
+    Dem d = make_dem(dem, dimy, dimx, 1.0);
+    Grid<float> pre = apply_pre_ops(d.values, p.pre_ops);
+    std::memcpy(out, pre.data().data(), sizeof(float) * pre.size());
+  });
+}
+
+// skew.cpp:144-196 build_skw. values/weights capacity cap_rows*cols.
+// Returns skw_rows through *skw_rows_out and base through *base_out.
+int ref_build_skw(const float* g, int rows, int cols, double shear_tan,
+                  int cap_rows, float* values, float* weights, int* ranges,
+                  int* skw_rows_out, int* base_out) {
+  return guarded([&] {
+    Dem d = make_dem(g, rows, cols, 1.0);
+    SkwGrid skw = build_skw(d.values, shear_tan);
+    *skw_rows_out = skw.skw_rows();
+    *base_out = skw.base;
+    if (skw.skw_rows() > cap_rows) {
+      throw std::runtime_error("ref_build_skw: capacity too small");
+    }
+    std::memcpy(values, skw.values.data().data(),
+                sizeof(float) * skw.values.size());
+    if (weights) {
+      std::memcpy(weights, skw.weights.data().data(),
+                  sizeof(float) * skw.weights.size());
+    }
+    for (int q = 0; q < skw.skw_rows(); ++q) {
+      ranges[2 * q] = skw.row_ranges[q].first;
+      ranges[2 * q + 1] = skw.row_ranges[q].second;
+    }
+  });
+}
+
+// scan.cpp:8-62 linear_viewshed_row; dir 0 forward, 1 backward.
+// visible_out (optional) receives one flag per scanned target; *n_vis its
+// count.
+double ref_linear_viewshed_row(const float* row, int n, int first, int last,
+                               int j0, double h, int dir, int max_dd,
+                               uint8_t* visible_out, int* n_vis) {
+  std::vector<uint8_t> vis;
+  double cv = linear_viewshed_row(
+      std::span<const float>(row, n), first, last, j0, h,
+      dir == 0 ? ScanDir::Forward : ScanDir::Backward, max_dd,
+      visible_out ? &vis : nullptr);
+  if (visible_out) {
+    std::memcpy(visible_out, vis.data(), vis.size());
+    *n_vis = static_cast<int>(vis.size());
+  }
+  return cv;
+}
+
+// scan.cpp:64-85 sector_viewshed over an sDEM given as values + row ranges.
+int ref_sector_viewshed(const float* values, const int* ranges, int skw_rows,
+                        int cols, int src_rows, int base, double shear_tan,
+                        double h0, int max_dd, double* out) {
+  return guarded([&] {
+    SkwGrid skw;
+    skw.src_rows = src_rows;
+    skw.cols = cols;
+    skw.base = base;
+    skw.shear_tan = shear_tan;
+    skw.values.reset(skw_rows, cols, 0.0f);
+    std::memcpy(skw.values.data().data(), values,
+                sizeof(float) * static_cast<size_t>(skw_rows) * cols);
+    skw.weights.reset(skw_rows, cols, 0.0f);
+    skw.row_ranges.resize(skw_rows);
+    for (int q = 0; q < skw_rows; ++q) {
+      skw.row_ranges[q] = {ranges[2 * q], ranges[2 * q + 1]};
+    }
+    Grid<double> vs;
+    sector_viewshed(skw, h0, max_dd, vs);
+    std::memcpy(out, vs.data().data(), sizeof(double) * vs.size());
+  });
+}
+
+// skew.cpp:204-263 unskew_accumulate (out is read-modify-written).
+int ref_unskew_accumulate(const double* skw_vs, int skw_rows, int cols, int k,
+                          int ns, int dimy, int dimx, double* out) {
+  return guarded([&] {
+    SectorPlan plan = plan_sector(k, ns, dimy, dimx);
+    Grid<double> vs(skw_rows, cols, 0.0);
+    std::memcpy(vs.data().data(), skw_vs, sizeof(double) * vs.size());
+    Grid<double> o(dimy, dimx, 0.0);
+    std::memcpy(o.data().data(), out, sizeof(double) * o.size());
+    unskew_accumulate(vs, plan, o);
+    std::memcpy(out, o.data().data(), sizeof(double) * o.size());
+  });
+}
+
+// engine.cpp:235-244 sector_sweep
+int ref_sector_sweep(const float* dem, int dimy, int dimx, double cellsize,
+                     int ns, double h0, double max_distance, int k,
+                     double* out, double* phase_seconds) {
+  return guarded([&] {
+    Dem d = make_dem(dem, dimy, dimx, cellsize);
+    RunConfig cfg = make_cfg(ns, h0, 1, max_distance, 0);
+    SectorResult r = sector_sweep(d, cfg, k);
+    std::memcpy(out, r.contribution.data().data(),
+                sizeof(double) * r.contribution.size());
+    if (phase_seconds) {
+      phase_seconds[0] = r.skew_seconds;
+      phase_seconds[1] = r.scan_seconds;
+      phase_seconds[2] = r.unskew_seconds;
+      phase_seconds[3] = r.wall_seconds;
+    }
+  });
+}
+
+// engine.cpp:109-220 total_viewshed_raw (raw=1) or engine.cpp:222-233
+// total_viewshed (raw=0). stats_out: skew, scan, unskew, reduce, total secs.
+int ref_total_viewshed(const float* dem, int dimy, int dimx, double cellsize,
+                       int ns, double h0, int workers, double max_distance,
+                       int units, int raw, double* out, double* stats_out) {
+  return guarded([&] {
+    Dem d = make_dem(dem, dimy, dimx, cellsize);
+    RunConfig cfg = make_cfg(ns, h0, workers, max_distance, units);
+    EngineStats st;
+    if (raw) {
+      Grid<double> g = total_viewshed_raw(d, cfg, &st);
+      std::memcpy(out, g.data().data(), sizeof(double) * g.size());
+    } else {
+      VsGrid g = total_viewshed(d, cfg, &st);
+      std::memcpy(out, g.values.data().data(),
+                  sizeof(double) * g.values.size());
+    }
+    if (stats_out) {
+      stats_out[0] = st.skew_seconds;
+      stats_out[1] = st.scan_seconds;
+      stats_out[2] = st.unskew_seconds;
+      stats_out[3] = st.reduce_seconds;
+      stats_out[4] = st.total_seconds;
+    }
+  });
+}
+
+// engine.cpp:103-107 area_scale_factor
+double ref_area_scale_factor(int ns, double cellsize, int units) {
+  RunConfig cfg = make_cfg(ns, 1.5, 1, 0.0, units);
+  return area_scale_factor(cfg, cellsize);
+}
+
+// oracle.cpp:143-194 total_viewshed_reference (rotational sweep, secondary
+// sanity oracle).
+int ref_rotational_total_viewshed(const float* dem, int dimy, int dimx,
+                                  double cellsize, int ns, double h0,
+                                  double max_distance, double* out) {
+  return guarded([&] {
+    Dem d = make_dem(dem, dimy, dimx, cellsize);
+    RunConfig cfg = make_cfg(ns, h0, 1, max_distance, 0);
+    cfg.workers = std::max(1u, std::thread::hardware_concurrency());
+    VsGrid g = oracle::total_viewshed_reference(d, cfg, true);
+    std::memcpy(out, g.values.data().data(), sizeof(double) * g.values.size());
+  });
+}
+
+// CPU baseline sampler. Runs the reference's own per-sector pipeline
+// (plan_sector -> apply_pre_ops -> build_skw -> linear_viewshed_row for every
+// POV of the sampled skewed rows, both directions) on `threads` host threads
+// and returns the target evaluations done and the wall seconds. Rows are
+// sampled with a stride so the sample is stratified over row lengths; the
+// caller extrapolates with the exact work count of the full workload.
+int ref_sample_scan(const float* dem, int dimy, int dimx, int ns, double h0,
+                    int max_dd, const int* sectors, int n_sectors,
+                    int row_stride, int row_offset, int threads,
+                    double* target_evals_out, double* seconds_out) {
+  return guarded([&] {
+    Dem d = make_dem(dem, dimy, dimx, 10.0);
+    struct Item {
+      int s;
+      int q;
+    };
+    // Relocation is done up front (outside the timed region) because the
+    // scan is >99% of the reference's worker time.
+    std::vector<SkwGrid> skws(n_sectors);
+    std::vector<Item> items;
+    for (int s = 0; s < n_sectors; ++s) {
+      SectorPlan p = plan_sector(sectors[s], ns, dimy, dimx);
+      Grid<float> pre = apply_pre_ops(d.values, p.pre_ops);
+      skws[s] = build_skw(pre, p.shear_tan);
+      for (int q = row_offset; q < skws[s].skw_rows(); q += row_stride) {
+        auto [f, l] = skws[s].row_ranges[q];
+        if (l > f) items.push_back({s, q});
+      }
+    }
+    std::atomic<size_t> next{0};
+    std::atomic<long long> evals{0};
+    std::atomic<long long> sink{0};
+    auto worker = [&] {
+      long long local = 0;
+      double acc = 0.0;
+      for (;;) {
+        size_t it = next.fetch_add(1);
+        if (it >= items.size()) break;
+        const SkwGrid& skw = skws[items[it].s];
+        int q = items[it].q;
+        auto [first, last] = skw.row_ranges[q];
+        std::span<const float> row(skw.values.row(q), skw.cols);
+        for (int j0 = first; j0 < last; ++j0) {
+          double h = row[j0] + h0;
+          acc += linear_viewshed_row(row, first, last, j0, h,
+                                     ScanDir::Forward, max_dd);
+          acc += linear_viewshed_row(row, first, last, j0, h,
+                                     ScanDir::Backward, max_dd);
+          long long fw = std::min<long long>(last - 1 - j0, max_dd);
+          long long bw = std::min<long long>(j0 - first, max_dd);
+          local += fw + bw;
+        }
+      }
+      evals += local;
+      sink += static_cast<long long>(acc) & 1;
+    };
+    auto t0 = std::chrono::steady_clock::now();
+    std::vector<std::thread> pool;
+    for (int t = 0; t < std::max(1, threads); ++t) pool.emplace_back(worker);
+    for (auto& t : pool) t.join();
+    *seconds_out = std::chrono::duration<double>(
+                       std::chrono::steady_clock::now() - t0)
+                       .count();
+    *target_evals_out = static_cast<double>(evals.load());
+  });
+}
+
+}  // extern "C"

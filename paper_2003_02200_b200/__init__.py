@@ -1,0 +1,24 @@
+"""skewshed-b200: B200-native sDEM total viewshed (arXiv 2003.02200).
+
+The hot path (relocation -> line-of-sight scan -> unskew/accumulate) runs in
+hand-written sm_100a kernels inside libskewshed_b200.so, reached through its C
+ABI (include/skewshed_b200.h). This package is the host-side mirror of the
+reference's C++ API (proj/include/skewshed/*.hpp) plus the multi-GPU sharding.
+"""
+from .engine import (AxisOp, Context, Dem, EngineStats, RunConfig, ScanDir, SectorPlan, SectorResult,
+                     SkwGrid, SyntheticKind, Units, VsGrid, accumulate_into, area_scale, area_scale_factor,
+                     build_sector_sdem, build_skw, convert_units, device_count, distance_cap_cells,
+                     kNoDistanceCap, linear_viewshed_row, make_synthetic, partition_sectors, plan_sector,
+                     reduce_ordered, row_ranges, sector_sweep, sector_target_evals, sector_viewshed,
+                     shear_params, total_target_evals, total_viewshed, total_viewshed_raw,
+                     unskew_accumulate, validate)
+
+__all__ = [
+    "AxisOp", "Context", "Dem", "EngineStats", "RunConfig", "ScanDir", "SectorPlan", "SectorResult",
+    "SkwGrid", "SyntheticKind", "Units", "VsGrid", "accumulate_into", "area_scale", "area_scale_factor",
+    "build_sector_sdem", "build_skw", "convert_units", "device_count", "distance_cap_cells",
+    "kNoDistanceCap", "linear_viewshed_row", "make_synthetic", "partition_sectors", "plan_sector",
+    "reduce_ordered", "row_ranges", "sector_sweep", "sector_target_evals", "sector_viewshed",
+    "shear_params", "total_target_evals", "total_viewshed", "total_viewshed_raw", "unskew_accumulate",
+    "validate",
+]

@@ -1,0 +1,899 @@
+// Engine and C ABI of the B200 sDEM total-viewshed path.
+//
+// Replaces the reference engine (engine.cpp:29-244): instead of a pool of
+// std::threads each running relocation -> scan -> unskew on one sector, a
+// per-GPU context runs whole BATCHES of sectors with one launch per phase:
+//   relocate (all sectors of the batch) -> scan (one persistent launch over
+//   every skewed row of the batch, longest first) -> exact fixup of flagged
+//   POV groups -> unskew + accumulate (ascending k, into the FP64 map).
+// Sector plans (pure geometry) and the batch metadata are cached per
+// context, so repeated runs on DEMs of the same shape only move elevations.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <chrono>
+#include <cmath>
+#include <cstring>
+#include <map>
+#include <memory>
+#include <mutex>
+#include <numeric>
+#include <sstream>
+#include <stdexcept>
+#include <string>
+#include <tuple>
+#include <vector>
+
+#include "../../include/skewshed_b200.h"
+#include "sks_device.cuh"
+#include "sks_plan.hpp"
+
+namespace sks {
+
+namespace {
+
+thread_local std::string g_error;
+
+struct CudaError : std::runtime_error {
+  using std::runtime_error::runtime_error;
+};
+
+void cuda_check(cudaError_t e, const char* what) {
+  if (e != cudaSuccess) {
+    std::ostringstream os;
+    os << what << ": " << cudaGetErrorString(e);
+    throw CudaError(os.str());
+  }
+}
+void cuda_check(int e, const char* what) { cuda_check(static_cast<cudaError_t>(e), what); }
+
+template <typename Fn>
+sks_status guarded(Fn&& fn) {
+  try {
+    fn();
+    g_error.clear();
+    return SKS_OK;
+  } catch (const std::invalid_argument& e) {
+    g_error = e.what();
+    return SKS_INVALID_ARGUMENT;
+  } catch (const std::out_of_range& e) {
+    g_error = e.what();
+    return SKS_OUT_OF_RANGE;
+  } catch (const CudaError& e) {
+    g_error = e.what();
+    return SKS_CUDA_ERROR;
+  } catch (const std::exception& e) {
+    g_error = e.what();
+    return SKS_INTERNAL;
+  }
+}
+
+// Device buffer that only grows.
+struct DevBuf {
+  void* p = nullptr;
+  size_t bytes = 0;
+  int device = -1;
+  void ensure(size_t n, int dev) {
+    if (n <= bytes && p) return;
+    release();
+    cuda_check(cudaMalloc(&p, std::max<size_t>(n, 256)), "cudaMalloc");
+    bytes = std::max<size_t>(n, 256);
+    device = dev;
+  }
+  void release() {
+    if (p) cudaFree(p);
+    p = nullptr;
+    bytes = 0;
+  }
+  ~DevBuf() { release(); }
+  template <typename T>
+  T* as() const {
+    return static_cast<T*>(p);
+  }
+};
+
+int round_up(int x, int m) { return (x + m - 1) / m * m; }
+
+// One batch of sectors, fully prepared on the host and mirrored on device.
+struct Batch {
+  std::vector<int> slots;  // indices into Plans::plans, ascending k
+  std::vector<SectorDev> sdev;
+  std::vector<int> dest;
+  std::vector<float> fracf;
+  std::vector<double> fracd;
+  std::vector<int2> ranges;
+  std::vector<ScanItem> items;
+  long long pool_elems = 0;  // sdem / cv pool elements
+  int lmax = 0;
+  unsigned fix_cap = 0;
+  int tiles_x = 0, tiles_total = 0;
+  long long target_evals = 0;
+  // device copies
+  DevBuf d_sectors, d_dest, d_fracf, d_fracd, d_ranges, d_items;
+};
+
+struct Plans {
+  std::vector<SectorPlanH> plans;  // ascending k
+  std::vector<std::unique_ptr<Batch>> batches;
+};
+
+long long batch_budget_bytes() {
+  if (const char* s = std::getenv("SKS_BATCH_GB")) {
+    double gb = std::atof(s);
+    if (gb > 0) return static_cast<long long>(gb * (1LL << 30));
+  }
+  return 24LL << 30;
+}
+
+std::unique_ptr<Batch> make_batch(const std::vector<SectorPlanH>& plans,
+                                  const std::vector<int>& slots, int device) {
+  auto b = std::make_unique<Batch>();
+  b->slots = slots;
+  long long off = 0;
+  int col_off = 0, row_off = 0;
+  int max_cols = 0, max_rows = 0;
+  for (size_t s = 0; s < slots.size(); ++s) {
+    const SectorPlanH& p = plans[slots[s]];
+    SectorDev d{};
+    d.k = p.k;
+    d.rows = p.rows;
+    d.cols = p.cols;
+    d.src_rows = p.src_rows;
+    d.src_cols = p.src_cols;
+    d.base = p.base;
+    d.skw_rows = p.skw_rows;
+    d.pitch = round_up(p.cols, 32);
+    d.max_dd = p.max_dd;
+    d.col_off = col_off;
+    d.row_off = row_off;
+    std::copy(p.map, p.map + 6, d.map);
+    std::copy(p.inv, p.inv + 6, d.inv);
+    d.correction = p.correction;
+    d.sdem_off = off;
+    off += static_cast<long long>(p.skw_rows) * d.pitch;
+    col_off += p.cols;
+    row_off += p.skw_rows;
+    b->dest.insert(b->dest.end(), p.dest.begin(), p.dest.end());
+    b->fracf.insert(b->fracf.end(), p.fracf.begin(), p.fracf.end());
+    b->fracd.insert(b->fracd.end(), p.fracd.begin(), p.fracd.end());
+    for (int q = 0; q < p.skw_rows; ++q) {
+      const RowRange& r = p.ranges[q];
+      b->ranges.push_back(make_int2(r.first, r.last));
+      const int L = r.last - r.first;
+      if (L >= 2 && p.max_dd > 0) {
+        b->items.push_back(ScanItem{static_cast<int>(s), q});
+        b->lmax = std::max(b->lmax, L);
+        b->fix_cap += 2u * static_cast<unsigned>((L + 3) / 4);
+      }
+    }
+    b->target_evals += p.target_evals;
+    max_cols = std::max(max_cols, p.cols);
+    max_rows = std::max(max_rows, p.skw_rows);
+    b->sdev.push_back(d);
+  }
+  b->pool_elems = off;
+  // longest rows first (load balance of the persistent scan)
+  std::stable_sort(b->items.begin(), b->items.end(), [&](const ScanItem& x, const ScanItem& y) {
+    const int2 rx = b->ranges[b->sdev[x.s].row_off + x.q];
+    const int2 ry = b->ranges[b->sdev[y.s].row_off + y.q];
+    return (rx.y - rx.x) > (ry.y - ry.x);
+  });
+  b->tiles_x = (max_cols + relocate_tile_cols() - 1) / relocate_tile_cols();
+  b->tiles_total = b->tiles_x * ((max_rows + relocate_tile_rows() - 1) / relocate_tile_rows());
+  if (b->fix_cap == 0) b->fix_cap = 1;
+  // upload metadata once
+  auto up = [&](DevBuf& buf, const void* src, size_t bytes) {
+    buf.ensure(bytes, device);
+    if (bytes) cuda_check(cudaMemcpy(buf.p, src, bytes, cudaMemcpyHostToDevice), "upload metadata");
+  };
+  up(b->d_sectors, b->sdev.data(), b->sdev.size() * sizeof(SectorDev));
+  up(b->d_dest, b->dest.data(), b->dest.size() * sizeof(int));
+  up(b->d_fracf, b->fracf.data(), b->fracf.size() * sizeof(float));
+  up(b->d_fracd, b->fracd.data(), b->fracd.size() * sizeof(double));
+  up(b->d_ranges, b->ranges.data(), b->ranges.size() * sizeof(int2));
+  up(b->d_items, b->items.data(), b->items.size() * sizeof(ScanItem));
+  return b;
+}
+
+// Split plans (ascending k) into batches under the memory budget.
+void make_batches(Plans& P, int device) {
+  const long long budget = batch_budget_bytes();
+  std::vector<int> cur;
+  long long cur_bytes = 0;
+  for (int s = 0; s < static_cast<int>(P.plans.size()); ++s) {
+    const SectorPlanH& p = P.plans[s];
+    // sdem f32 + cv i32 + fixup queue (<= 2 entries of 8 B per 4 POVs)
+    long long bytes = static_cast<long long>(p.skw_rows) * round_up(p.cols, 32) * 8LL +
+                      static_cast<long long>(p.rows) * p.cols * 4LL + 64LL * p.skw_rows;
+    if (!cur.empty() && cur_bytes + bytes > budget) {
+      P.batches.push_back(make_batch(P.plans, cur, device));
+      cur.clear();
+      cur_bytes = 0;
+    }
+    cur.push_back(s);
+    cur_bytes += bytes;
+  }
+  if (!cur.empty()) P.batches.push_back(make_batch(P.plans, cur, device));
+}
+
+}  // namespace
+
+}  // namespace sks
+
+using namespace sks;
+
+struct sks_context {
+  int device = 0;
+  cudaStream_t own_stream = nullptr;
+  int sms = 0;
+  std::mutex mu;
+  // plan cache
+  std::map<std::tuple<int, int, int, double, double, std::vector<int>>, std::unique_ptr<Plans>>
+      cache;
+  // work buffers
+  DevBuf sdem, cv, cvb, queue, counters, dem, map, vis;
+  cudaEvent_t ev[8] = {};
+  long long launches = 0;
+
+  void activate() const { cuda_check(cudaSetDevice(device), "cudaSetDevice"); }
+
+  Plans& plans_for(int dimy, int dimx, int ns, double cellsize, double max_distance,
+                   const std::vector<int>& sectors) {
+    auto key = std::make_tuple(dimy, dimx, ns, cellsize, max_distance, sectors);
+    auto it = cache.find(key);
+    if (it != cache.end()) return *it->second;
+    if (cache.size() > 16) cache.clear();
+    auto P = std::make_unique<Plans>();
+    for (int k : sectors) P->plans.push_back(plan_sector(k, ns, dimy, dimx, cellsize, max_distance));
+    make_batches(*P, device);
+    Plans& ref = *P;
+    cache.emplace(key, std::move(P));
+    return ref;
+  }
+
+  BatchDev batch_dev(const Batch& b, bool split_bwd) {
+    BatchDev d{};
+    d.sectors = b.d_sectors.as<SectorDev>();
+    d.n_sectors = static_cast<int>(b.sdev.size());
+    d.dest = b.d_dest.as<int>();
+    d.fracf = b.d_fracf.as<float>();
+    d.fracd = b.d_fracd.as<double>();
+    d.ranges = b.d_ranges.as<int2>();
+    d.sdem = sdem.as<float>();
+    d.cv = cv.as<int>();
+    d.cv_bwd = split_bwd ? cvb.as<int>() : nullptr;
+    return d;
+  }
+
+  void ensure_pools(const Batch& b, bool split_bwd) {
+    sdem.ensure(static_cast<size_t>(b.pool_elems) * sizeof(float), device);
+    cv.ensure(static_cast<size_t>(b.pool_elems) * sizeof(int), device);
+    if (split_bwd) cvb.ensure(static_cast<size_t>(b.pool_elems) * sizeof(int), device);
+    queue.ensure(static_cast<size_t>(b.fix_cap) * sizeof(unsigned long long), device);
+    counters.ensure(64, device);
+  }
+
+  ScanArgs scan_args(const Batch& b, const BatchDev& bd, double h0) {
+    ScanArgs a{};
+    a.b = bd;
+    a.items = b.d_items.as<ScanItem>();
+    a.n_items = static_cast<int>(b.items.size());
+    a.lmax = std::max(b.lmax, 4);
+    a.item_counter = counters.as<unsigned>();
+    a.fix_queue = queue.as<unsigned long long>();
+    a.fix_count = counters.as<unsigned>() + 1;
+    a.fix_cap = b.fix_cap;
+    a.h0 = h0;
+    a.dbg_j0 = -1;
+    a.dbg_h = 0.0;
+    a.dbg_vis_fwd = nullptr;
+    a.dbg_vis_bwd = nullptr;
+    a.force_exact = 0;
+    return a;
+  }
+
+  // scan + fixup of one batch whose sDEM is already in the pool
+  void scan_batch(const Batch& b, const ScanArgs& a, cudaStream_t st, bool split_bwd) {
+    cuda_check(cudaMemsetAsync(cv.p, 0, static_cast<size_t>(b.pool_elems) * sizeof(int), st),
+               "memset cv");
+    if (split_bwd) {
+      cuda_check(cudaMemsetAsync(cvb.p, 0, static_cast<size_t>(b.pool_elems) * sizeof(int), st),
+                 "memset cvb");
+    }
+    cuda_check(cudaMemsetAsync(counters.p, 0, 64, st), "memset counters");
+    if (a.n_items > 0) {
+      int grid = 0;
+      cuda_check(scan_occupancy(a.lmax, &grid), "scan occupancy");
+      grid = std::min(grid, std::max(1, a.n_items));
+      cuda_check(launch_scan(a, grid, st), "launch scan");
+      ++launches;
+    }
+  }
+
+  void fixup_batch(const ScanArgs& a, cudaStream_t st) {
+    if (a.n_items == 0) return;
+    cuda_check(launch_fixup(a, sms * 8, st), "launch fixup");
+    ++launches;
+  }
+
+  ~sks_context() {
+    for (cudaEvent_t& e : ev) {
+      if (e) cudaEventDestroy(e);
+    }
+    if (own_stream) cudaStreamDestroy(own_stream);
+  }
+};
+
+namespace {
+
+std::mutex g_ctx_mu;
+std::map<int, std::unique_ptr<sks_context>> g_default;
+
+sks_context* default_context(int device) {
+  std::lock_guard<std::mutex> lk(g_ctx_mu);
+  auto it = g_default.find(device);
+  if (it != g_default.end()) return it->second.get();
+  auto ctx = std::make_unique<sks_context>();
+  ctx->device = device;
+  ctx->activate();
+  cuda_check(cudaStreamCreateWithFlags(&ctx->own_stream, cudaStreamNonBlocking), "stream");
+  cuda_check(cudaDeviceGetAttribute(&ctx->sms, cudaDevAttrMultiProcessorCount, device), "attr");
+  for (cudaEvent_t& e : ctx->ev) cuda_check(cudaEventCreate(&e), "event");
+  sks_context* raw = ctx.get();
+  g_default.emplace(device, std::move(ctx));
+  return raw;
+}
+
+void require_valid(const float* dem, int dimy, int dimx, double cellsize,
+                   const sks_run_config* cfg) {
+  if (!cfg) throw std::invalid_argument("null run config");
+  if (!dem) throw std::invalid_argument("null DEM");
+  std::string err =
+      validate_inputs(dem, dimy, dimx, cellsize, nullptr, cfg->ns, cfg->h0, cfg->max_distance);
+  if (!err.empty()) throw std::invalid_argument(err);
+}
+
+// Elevation magnitudes the FP32 filter's proof covers: every
+// nonzero |e| and h0 in [2^-40, 2^40]. Outside, the whole run uses the exact
+// FP64 path.
+bool filter_preconditions_hold(const float* dem, size_t n, double h0) {
+  const double lo = std::ldexp(1.0, -40), hi = std::ldexp(1.0, 40);
+  if (h0 != 0.0 && (h0 < lo || h0 > hi)) return false;
+  for (size_t i = 0; i < n; ++i) {
+    const double a = std::fabs(static_cast<double>(dem[i]));
+    if (a != 0.0 && (a < lo || a > hi)) return false;
+  }
+  return true;
+}
+
+double elapsed(cudaEvent_t a, cudaEvent_t b) {
+  float ms = 0.f;
+  cuda_check(cudaEventElapsedTime(&ms, a, b), "event time");
+  return ms * 1e-3;
+}
+
+// Core: run the given sectors on device data. Accumulates into d_map.
+void run_sectors(sks_context* ctx, const float* d_dem, int dimy, int dimx, double cellsize,
+                 const sks_run_config* cfg, std::vector<int> sectors, double* d_map,
+                 cudaStream_t st, sks_stats* stats, bool force_exact) {
+  std::sort(sectors.begin(), sectors.end());
+  sectors.erase(std::unique(sectors.begin(), sectors.end()), sectors.end());
+  for (int k : sectors) {
+    if (k < 0 || k >= cfg->ns / 2) throw std::out_of_range("sector index out of range");
+  }
+  Plans& P = ctx->plans_for(dimy, dimx, cfg->ns, cellsize, cfg->max_distance, sectors);
+  const long long launches0 = ctx->launches;
+  double t_skew = 0, t_scan = 0, t_fix = 0, t_unskew = 0;
+  long long flagged = 0, evals = 0;
+  for (auto& bp : P.batches) {
+    Batch& b = *bp;
+    ctx->ensure_pools(b, false);
+    BatchDev bd = ctx->batch_dev(b, false);
+    ScanArgs a = ctx->scan_args(b, bd, cfg->h0);
+    a.force_exact = force_exact ? 1 : 0;
+    if (stats) cuda_check(cudaEventRecord(ctx->ev[0], st), "event");
+    cuda_check(launch_relocate_grid(d_dem, bd, b.tiles_x, b.tiles_total, st), "launch relocate");
+    ++ctx->launches;
+    if (stats) cuda_check(cudaEventRecord(ctx->ev[1], st), "event");
+    ctx->scan_batch(b, a, st, false);
+    if (stats) cuda_check(cudaEventRecord(ctx->ev[2], st), "event");
+    ctx->fixup_batch(a, st);
+    if (stats) cuda_check(cudaEventRecord(ctx->ev[3], st), "event");
+    cuda_check(launch_unskew(bd, nullptr, d_map, dimy, dimx, st), "launch unskew");
+    ++ctx->launches;
+    if (stats) {
+      cuda_check(cudaEventRecord(ctx->ev[4], st), "event");
+      cuda_check(cudaEventSynchronize(ctx->ev[4]), "sync");
+      t_skew += elapsed(ctx->ev[0], ctx->ev[1]);
+      t_scan += elapsed(ctx->ev[1], ctx->ev[2]);
+      t_fix += elapsed(ctx->ev[2], ctx->ev[3]);
+      t_unskew += elapsed(ctx->ev[3], ctx->ev[4]);
+      unsigned cnt[2] = {0, 0};
+      cuda_check(cudaMemcpy(cnt, ctx->counters.p, sizeof(cnt), cudaMemcpyDeviceToHost), "counters");
+      flagged += cnt[1];
+    }
+    evals += b.target_evals;
+  }
+  if (stats) {
+    stats->skew_seconds += t_skew;
+    stats->scan_seconds += t_scan;
+    stats->fixup_seconds += t_fix;
+    stats->unskew_seconds += t_unskew;
+    stats->sectors += static_cast<int>(sectors.size());
+    stats->batches += static_cast<int>(P.batches.size());
+    stats->kernel_launches += ctx->launches - launches0;
+    stats->target_evals += evals;
+    stats->flagged_groups += flagged;
+  }
+}
+
+void total_host(sks_context* ctx, const float* dem, int dimy, int dimx, double cellsize,
+                const sks_run_config* cfg, int raw, double* out, sks_stats* stats) {
+  auto t0 = std::chrono::steady_clock::now();
+  require_valid(dem, dimy, dimx, cellsize, cfg);
+  if (!out) throw std::invalid_argument("null output");
+  ctx->activate();
+  std::lock_guard<std::mutex> lk(ctx->mu);
+  const size_t n = static_cast<size_t>(dimy) * dimx;
+  const bool exact = !filter_preconditions_hold(dem, n, cfg->h0);
+  cudaStream_t st = ctx->own_stream;
+  ctx->dem.ensure(n * sizeof(float), ctx->device);
+  ctx->map.ensure(n * sizeof(double), ctx->device);
+  cuda_check(cudaMemcpyAsync(ctx->dem.p, dem, n * sizeof(float), cudaMemcpyHostToDevice, st), "H2D dem");
+  cuda_check(cudaMemsetAsync(ctx->map.p, 0, n * sizeof(double), st), "memset map");
+  std::vector<int> all(cfg->ns / 2);
+  std::iota(all.begin(), all.end(), 0);
+  sks_stats local{};
+  run_sectors(ctx, ctx->dem.as<float>(), dimy, dimx, cellsize, cfg, all, ctx->map.as<double>(), st,
+              stats ? &local : nullptr, exact);
+  if (!raw) {
+    cuda_check(launch_scale(ctx->map.as<double>(), static_cast<long long>(n),
+                            area_scale_factor(cfg->ns, cellsize, cfg->units), st),
+               "launch scale");
+    ++ctx->launches;
+    local.kernel_launches += 1;
+  }
+  cuda_check(cudaMemcpyAsync(out, ctx->map.p, n * sizeof(double), cudaMemcpyDeviceToHost, st), "D2H map");
+  cuda_check(cudaStreamSynchronize(st), "sync");
+  if (stats) {
+    local.h2d_bytes = static_cast<long long>(n * sizeof(float));
+    local.d2h_bytes = static_cast<long long>(n * sizeof(double));
+    local.total_seconds = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
+    *stats = local;
+  }
+}
+
+// Single-sector debug batch from a custom plan; the sDEM is produced by the
+// relocation kernel from `grid` (pre_ops applied through the plan's map).
+struct DebugBatch {
+  std::vector<SectorPlanH> plans;
+  std::unique_ptr<Batch> batch;
+};
+
+DebugBatch debug_batch(SectorPlanH plan, int device) {
+  DebugBatch d;
+  d.plans.push_back(std::move(plan));
+  d.batch = make_batch(d.plans, {0}, device);
+  return d;
+}
+
+}  // namespace
+
+extern "C" {
+
+const char* sks_last_error(void) { return g_error.c_str(); }
+
+const char* sks_version(void) { return "skewshed_b200 0.1.0 (sm_100a)"; }
+
+int sks_device_count(void) {
+  int n = 0;
+  if (cudaGetDeviceCount(&n) != cudaSuccess) {
+    cudaGetLastError();
+    return 0;
+  }
+  return n;
+}
+
+sks_status sks_plan_sector(int k, int ns, int dimy, int dimx, sks_sector_plan* out) {
+  return guarded([&] {
+    if (!out) throw std::invalid_argument("null output");
+    SectorPlanH p = plan_sector(k, ns, dimy, dimx, 1.0, 0.0);
+    out->sector_index = p.k;
+    out->ns = p.ns;
+    out->sector_deg = p.sector_deg;
+    out->shear_deg = p.shear_deg;
+    out->shear_tan = p.shear_tan;
+    out->n_ops = p.n_ops;
+    std::copy(p.ops, p.ops + 3, out->ops);
+    out->rows = p.rows;
+    out->cols = p.cols;
+    out->src_rows = p.src_rows;
+    out->src_cols = p.src_cols;
+    std::copy(p.map, p.map + 6, out->to_source);
+    out->base = p.base;
+    out->skw_rows = p.skw_rows;
+  });
+}
+
+void sks_shear_params(double shear_tan, int j, int* dest, double* frac) {
+  shear_params(shear_tan, j, dest, frac);
+}
+
+int sks_distance_cap_cells(double max_distance, double shear_tan, double cellsize) {
+  return distance_cap_cells(max_distance, shear_tan, cellsize);
+}
+
+double sks_area_scale_factor(int ns, double cellsize, int units) {
+  return area_scale_factor(ns, cellsize, units);
+}
+
+sks_status sks_row_ranges(int rows, int cols, double shear_tan, int* ranges, int* skw_rows_out) {
+  return guarded([&] {
+    SectorPlanH p = plan_custom(rows, cols, shear_tan);
+    if (skw_rows_out) *skw_rows_out = p.skw_rows;
+    if (ranges) {
+      for (int q = 0; q < p.skw_rows; ++q) {
+        ranges[2 * q] = p.ranges[q].first;
+        ranges[2 * q + 1] = p.ranges[q].last;
+      }
+    }
+  });
+}
+
+long long sks_sector_target_evals(int k, int ns, int dimy, int dimx, double cellsize,
+                                  double max_distance) {
+  long long r = -1;
+  guarded([&] { r = plan_sector(k, ns, dimy, dimx, cellsize, max_distance).target_evals; });
+  return r;
+}
+
+sks_status sks_partition_sectors(int ns, int dimy, int dimx, double cellsize, double max_distance,
+                                 int world, int* owner) {
+  return guarded([&] {
+    if (world < 1 || !owner) throw std::invalid_argument("world must be >= 1");
+    if (ns < 2 || ns % 2) throw std::invalid_argument("ns must be an even integer >= 2");
+    std::vector<long long> work(ns / 2);
+    for (int k = 0; k < ns / 2; ++k) {
+      work[k] = plan_sector(k, ns, dimy, dimx, cellsize, max_distance).target_evals;
+    }
+    std::vector<int> o = partition_lpt(work, world);
+    std::copy(o.begin(), o.end(), owner);
+  });
+}
+
+sks_status sks_make_synthetic(int kind, int dimy, int dimx, uint32_t seed, float* out) {
+  return guarded([&] {
+    if (!out) throw std::invalid_argument("null output");
+    make_synthetic(kind, dimy, dimx, seed, out);
+  });
+}
+
+sks_status sks_validate(const float* dem, int dimy, int dimx, double cellsize, const float* nodata,
+                        const sks_run_config* cfg) {
+  return guarded([&] {
+    if (!cfg || !dem) throw std::invalid_argument("null argument");
+    std::string err =
+        validate_inputs(dem, dimy, dimx, cellsize, nodata, cfg->ns, cfg->h0, cfg->max_distance);
+    if (!err.empty()) throw std::invalid_argument(err);
+  });
+}
+
+sks_status sks_context_create(int device, sks_context** out) {
+  return guarded([&] {
+    if (!out) throw std::invalid_argument("null output");
+    auto ctx = std::make_unique<sks_context>();
+    ctx->device = device;
+    ctx->activate();
+    cuda_check(cudaStreamCreateWithFlags(&ctx->own_stream, cudaStreamNonBlocking), "stream");
+    cuda_check(cudaDeviceGetAttribute(&ctx->sms, cudaDevAttrMultiProcessorCount, device), "attr");
+    for (cudaEvent_t& e : ctx->ev) cuda_check(cudaEventCreate(&e), "event");
+    *out = ctx.release();
+  });
+}
+
+void sks_context_destroy(sks_context* ctx) { delete ctx; }
+
+sks_status sks_context_run_sectors(sks_context* ctx, const float* d_dem, int dimy, int dimx,
+                                   double cellsize, const sks_run_config* cfg, const int* sectors,
+                                   int n_sectors, double* d_map, void* stream, sks_stats* stats) {
+  return guarded([&] {
+    if (!ctx || !cfg || !d_dem || !d_map) throw std::invalid_argument("null argument");
+    if (cfg->ns < 2 || cfg->ns % 2) throw std::invalid_argument("ns must be an even integer >= 2");
+    if (dimy < 2 || dimx < 2) throw std::invalid_argument("grid must be at least 2x2");
+    ctx->activate();
+    std::lock_guard<std::mutex> lk(ctx->mu);
+    std::vector<int> ks(sectors, sectors + n_sectors);
+    sks_stats local{};
+    run_sectors(ctx, d_dem, dimy, dimx, cellsize, cfg, ks, d_map, static_cast<cudaStream_t>(stream),
+                stats ? &local : nullptr, false);
+    if (stats) *stats = local;
+  });
+}
+
+sks_status sks_context_scale(sks_context* ctx, double* d_map, long long n, int ns, double cellsize,
+                             int units, void* stream) {
+  return guarded([&] {
+    if (!ctx || !d_map) throw std::invalid_argument("null argument");
+    ctx->activate();
+    cuda_check(launch_scale(d_map, n, area_scale_factor(ns, cellsize, units),
+                            static_cast<cudaStream_t>(stream)),
+               "launch scale");
+    ++ctx->launches;
+  });
+}
+
+sks_status sks_context_total_viewshed(sks_context* ctx, const float* dem, int dimy, int dimx,
+                                      double cellsize, const sks_run_config* cfg, int raw,
+                                      double* out, sks_stats* stats) {
+  return guarded([&] {
+    if (!ctx) throw std::invalid_argument("null context");
+    total_host(ctx, dem, dimy, dimx, cellsize, cfg, raw, out, stats);
+  });
+}
+
+sks_status sks_total_viewshed(const float* dem, int dimy, int dimx, double cellsize,
+                              const sks_run_config* cfg, double* out_vs, sks_stats* stats) {
+  return guarded([&] {
+    if (!cfg) throw std::invalid_argument("null run config");
+    total_host(default_context(cfg->device), dem, dimy, dimx, cellsize, cfg, 0, out_vs, stats);
+  });
+}
+
+sks_status sks_total_viewshed_raw(const float* dem, int dimy, int dimx, double cellsize,
+                                  const sks_run_config* cfg, double* out_raw, sks_stats* stats) {
+  return guarded([&] {
+    if (!cfg) throw std::invalid_argument("null run config");
+    total_host(default_context(cfg->device), dem, dimy, dimx, cellsize, cfg, 1, out_raw, stats);
+  });
+}
+
+sks_status sks_sector_sweep(const float* dem, int dimy, int dimx, double cellsize,
+                            const sks_run_config* cfg, int k, double* out) {
+  return guarded([&] {
+    require_valid(dem, dimy, dimx, cellsize, cfg);
+    if (k < 0 || k >= cfg->ns / 2) throw std::out_of_range("sector index out of range");
+    if (!out) throw std::invalid_argument("null output");
+    sks_context* ctx = default_context(cfg->device);
+    ctx->activate();
+    std::lock_guard<std::mutex> lk(ctx->mu);
+    const size_t n = static_cast<size_t>(dimy) * dimx;
+    cudaStream_t st = ctx->own_stream;
+    ctx->dem.ensure(n * sizeof(float), ctx->device);
+    ctx->map.ensure(n * sizeof(double), ctx->device);
+    cuda_check(cudaMemcpyAsync(ctx->dem.p, dem, n * sizeof(float), cudaMemcpyHostToDevice, st), "H2D");
+    cuda_check(cudaMemsetAsync(ctx->map.p, 0, n * sizeof(double), st), "memset");
+    run_sectors(ctx, ctx->dem.as<float>(), dimy, dimx, cellsize, cfg, {k}, ctx->map.as<double>(), st,
+                nullptr, !filter_preconditions_hold(dem, n, cfg->h0));
+    cuda_check(cudaMemcpyAsync(out, ctx->map.p, n * sizeof(double), cudaMemcpyDeviceToHost, st), "D2H");
+    cuda_check(cudaStreamSynchronize(st), "sync");
+  });
+}
+
+namespace {
+
+// Relocation of one debug batch from a host grid; values copied back with
+// every cell (the pool is zeroed first so empty tiles read as +0).
+void debug_relocate(sks_context* ctx, Batch& b, const float* grid, size_t grid_elems,
+                    float* values) {
+  cudaStream_t st = ctx->own_stream;
+  ctx->ensure_pools(b, false);
+  ctx->dem.ensure(grid_elems * sizeof(float), ctx->device);
+  cuda_check(cudaMemcpyAsync(ctx->dem.p, grid, grid_elems * sizeof(float), cudaMemcpyHostToDevice, st),
+             "H2D grid");
+  cuda_check(cudaMemsetAsync(ctx->sdem.p, 0, static_cast<size_t>(b.pool_elems) * sizeof(float), st),
+             "memset sdem");
+  BatchDev bd = ctx->batch_dev(b, false);
+  cuda_check(launch_relocate_grid(ctx->dem.as<float>(), bd, b.tiles_x, b.tiles_total, st),
+             "launch relocate");
+  const SectorDev& sd = b.sdev[0];
+  cuda_check(cudaMemcpy2DAsync(values, sizeof(float) * sd.cols, ctx->sdem.p, sizeof(float) * sd.pitch,
+                               sizeof(float) * sd.cols, sd.skw_rows, cudaMemcpyDeviceToHost, st),
+             "D2H sdem");
+  cuda_check(cudaStreamSynchronize(st), "sync");
+}
+
+}  // namespace
+
+sks_status sks_build_sector_sdem(const float* dem, int dimy, int dimx, int k, int ns, int device,
+                                 float* values, int* ranges) {
+  return guarded([&] {
+    if (!dem || !values) throw std::invalid_argument("null argument");
+    SectorPlanH p = plan_sector(k, ns, dimy, dimx, 1.0, 0.0);
+    sks_context* ctx = default_context(device);
+    ctx->activate();
+    std::lock_guard<std::mutex> lk(ctx->mu);
+    DebugBatch d = debug_batch(p, device);
+    debug_relocate(ctx, *d.batch, dem, static_cast<size_t>(dimy) * dimx, values);
+    if (ranges) {
+      for (int q = 0; q < p.skw_rows; ++q) {
+        ranges[2 * q] = p.ranges[q].first;
+        ranges[2 * q + 1] = p.ranges[q].last;
+      }
+    }
+  });
+}
+
+sks_status sks_build_skw(const float* g, int rows, int cols, double shear_tan, int device,
+                         float* values, int* ranges, int* base_out) {
+  return guarded([&] {
+    if (!g || !values) throw std::invalid_argument("null argument");
+    SectorPlanH p = plan_custom(rows, cols, shear_tan);
+    sks_context* ctx = default_context(device);
+    ctx->activate();
+    std::lock_guard<std::mutex> lk(ctx->mu);
+    DebugBatch d = debug_batch(p, device);
+    debug_relocate(ctx, *d.batch, g, static_cast<size_t>(rows) * cols, values);
+    if (ranges) {
+      for (int q = 0; q < p.skw_rows; ++q) {
+        ranges[2 * q] = p.ranges[q].first;
+        ranges[2 * q + 1] = p.ranges[q].last;
+      }
+    }
+    if (base_out) *base_out = p.base;
+  });
+}
+
+namespace {
+
+// Scan of a caller-provided sDEM (values + ranges) with split fwd/bwd output.
+void debug_scan(sks_context* ctx, const float* values, const int* ranges, int skw_rows, int cols,
+                double shear_tan, double h0, int max_dd, int dbg_j0, double dbg_h,
+                uint8_t* vis_fwd_host, uint8_t* vis_bwd_host, int vis_len, std::vector<int>& cvf,
+                std::vector<int>& cvb) {
+  cudaStream_t st = ctx->own_stream;
+  // A one-sector batch with the caller's geometry.
+  SectorPlanH p;
+  p.rows = p.src_rows = skw_rows;
+  p.cols = p.src_cols = cols;
+  p.base = 0;
+  p.skw_rows = skw_rows;
+  p.shear_tan = shear_tan;
+  p.correction = 1.0 + shear_tan * shear_tan;
+  p.max_dd = max_dd;
+  p.dest.assign(cols, 0);
+  p.fracf.assign(cols, 0.f);
+  p.fracd.assign(cols, 0.0);
+  p.ranges.resize(skw_rows);
+  for (int q = 0; q < skw_rows; ++q) p.ranges[q] = RowRange{ranges[2 * q], ranges[2 * q + 1]};
+  std::vector<SectorPlanH> plans{p};
+  auto b = make_batch(plans, {0}, ctx->device);
+  ctx->ensure_pools(*b, true);
+  const SectorDev& sd = b->sdev[0];
+  cuda_check(cudaMemcpy2DAsync(ctx->sdem.p, sizeof(float) * sd.pitch, values, sizeof(float) * cols,
+                               sizeof(float) * cols, skw_rows, cudaMemcpyHostToDevice, st),
+             "H2D sdem");
+  BatchDev bd = ctx->batch_dev(*b, true);
+  ScanArgs a = ctx->scan_args(*b, bd, h0);
+  uint8_t* dvis = nullptr;
+  if (dbg_j0 >= 0) {
+    a.dbg_j0 = dbg_j0;
+    a.dbg_h = dbg_h;
+    if (vis_fwd_host || vis_bwd_host) {
+      ctx->vis.ensure(2 * static_cast<size_t>(std::max(vis_len, 1)), ctx->device);
+      dvis = ctx->vis.as<uint8_t>();
+      cuda_check(cudaMemsetAsync(dvis, 0xff, 2 * static_cast<size_t>(std::max(vis_len, 1)), st), "memset vis");
+      a.dbg_vis_fwd = dvis;
+      a.dbg_vis_bwd = dvis + std::max(vis_len, 1);
+    }
+  }
+  ctx->scan_batch(*b, a, st, true);
+  ctx->fixup_batch(a, st);
+  cvf.assign(static_cast<size_t>(skw_rows) * cols, 0);
+  cvb.assign(static_cast<size_t>(skw_rows) * cols, 0);
+  cuda_check(cudaMemcpy2DAsync(cvf.data(), sizeof(int) * cols, ctx->cv.p, sizeof(int) * sd.pitch,
+                               sizeof(int) * cols, skw_rows, cudaMemcpyDeviceToHost, st),
+             "D2H cvf");
+  cuda_check(cudaMemcpy2DAsync(cvb.data(), sizeof(int) * cols, ctx->cvb.p, sizeof(int) * sd.pitch,
+                               sizeof(int) * cols, skw_rows, cudaMemcpyDeviceToHost, st),
+             "D2H cvb");
+  if (dvis) {
+    if (vis_fwd_host) cuda_check(cudaMemcpyAsync(vis_fwd_host, dvis, vis_len, cudaMemcpyDeviceToHost, st), "D2H vis");
+    if (vis_bwd_host) cuda_check(cudaMemcpyAsync(vis_bwd_host, dvis + std::max(vis_len, 1), vis_len, cudaMemcpyDeviceToHost, st), "D2H vis");
+  }
+  cuda_check(cudaStreamSynchronize(st), "sync");
+}
+
+}  // namespace
+
+sks_status sks_sector_viewshed(const float* values, const int* ranges, int skw_rows, int cols,
+                               double shear_tan, double h0, int max_dd, int device, double* out,
+                               int* cv_fwd, int* cv_bwd) {
+  return guarded([&] {
+    if (!values || !ranges || !out) throw std::invalid_argument("null argument");
+    if (skw_rows < 1 || cols < 1) throw std::invalid_argument("empty sDEM");
+    if (max_dd < 0) throw std::invalid_argument("max_dd must be >= 0");
+    sks_context* ctx = default_context(device);
+    ctx->activate();
+    std::lock_guard<std::mutex> lk(ctx->mu);
+    std::vector<int> cvf, cvb;
+    debug_scan(ctx, values, ranges, skw_rows, cols, shear_tan, h0, max_dd, -1, 0.0, nullptr, nullptr,
+               0, cvf, cvb);
+    // skwVS = (fwd + bwd) * (1 + tan^2) on device (scan.cpp:67-82)
+    const size_t n = static_cast<size_t>(skw_rows) * cols;
+    DevBuf df, db, dout;
+    df.ensure(n * sizeof(int), device);
+    db.ensure(n * sizeof(int), device);
+    dout.ensure(n * sizeof(double), device);
+    cudaStream_t st = ctx->own_stream;
+    cuda_check(cudaMemcpyAsync(df.p, cvf.data(), n * sizeof(int), cudaMemcpyHostToDevice, st), "H2D");
+    cuda_check(cudaMemcpyAsync(db.p, cvb.data(), n * sizeof(int), cudaMemcpyHostToDevice, st), "H2D");
+    cuda_check(launch_cv_to_vs(df.as<int>(), db.as<int>(), dout.as<double>(), static_cast<long long>(n),
+                               1.0 + shear_tan * shear_tan, st),
+               "launch cv_to_vs");
+    cuda_check(cudaMemcpyAsync(out, dout.p, n * sizeof(double), cudaMemcpyDeviceToHost, st), "D2H");
+    cuda_check(cudaStreamSynchronize(st), "sync");
+    if (cv_fwd) std::copy(cvf.begin(), cvf.end(), cv_fwd);
+    if (cv_bwd) std::copy(cvb.begin(), cvb.end(), cv_bwd);
+  });
+}
+
+sks_status sks_linear_viewshed_row(const float* row, int n, int first, int last, int j0, double h,
+                                   int dir, int max_dd, int device, double* cv_out,
+                                   uint8_t* visible_out, int* n_visible) {
+  return guarded([&] {
+    if (!row || !cv_out) throw std::invalid_argument("null argument");
+    if (!(0 <= first && first <= j0 && j0 < last && last <= n)) {
+      throw std::invalid_argument("require 0 <= first <= j0 < last <= n");
+    }
+    if (max_dd < 0) throw std::invalid_argument("max_dd must be >= 0");
+    const int D = std::min(max_dd, dir == 0 ? last - 1 - j0 : j0 - first);
+    if (n_visible) *n_visible = D;
+    if (D <= 0) {
+      *cv_out = 0.0;
+      return;
+    }
+    sks_context* ctx = default_context(device);
+    ctx->activate();
+    std::lock_guard<std::mutex> lk(ctx->mu);
+    int rr[2] = {first, last};
+    std::vector<int> cvf, cvb;
+    std::vector<uint8_t> vf(D), vb(D);
+    // both directions of POV j0 are scanned; each capture buffer holds a
+    // whole row so the longer direction cannot overrun the other's bytes
+    vf.assign(n, 0);
+    vb.assign(n, 0);
+    debug_scan(ctx, row, rr, 1, n, 0.0, 0.0, max_dd, j0, h, visible_out ? vf.data() : nullptr,
+               visible_out ? vb.data() : nullptr, n, cvf, cvb);
+    *cv_out = static_cast<double>(dir == 0 ? cvf[j0] : cvb[j0]);
+    if (visible_out) std::copy_n(dir == 0 ? vf.data() : vb.data(), D, visible_out);
+  });
+}
+
+sks_status sks_unskew_accumulate(const double* skw_vs, int skw_rows, int cols, int k, int ns,
+                                 int dimy, int dimx, int device, double* out) {
+  return guarded([&] {
+    if (!skw_vs || !out) throw std::invalid_argument("null argument");
+    SectorPlanH p = plan_sector(k, ns, dimy, dimx, 1.0, 0.0);
+    if (skw_rows != p.skw_rows || cols != p.cols) {
+      std::ostringstream os;
+      os << "skewed grid shape " << skw_rows << "x" << cols << " does not match plan ("
+         << p.skw_rows << "x" << p.cols << ")";
+      throw std::invalid_argument(os.str());
+    }
+    sks_context* ctx = default_context(device);
+    ctx->activate();
+    std::lock_guard<std::mutex> lk(ctx->mu);
+    DebugBatch d = debug_batch(p, device);
+    Batch& b = *d.batch;
+    // skw_vs is read with the batch's cell indexing: give it pitch = cols.
+    b.sdev[0].pitch = cols;
+    b.sdev[0].sdem_off = 0;
+    cuda_check(cudaMemcpy(b.d_sectors.p, b.sdev.data(), sizeof(SectorDev), cudaMemcpyHostToDevice),
+               "upload");
+    const size_t nv = static_cast<size_t>(skw_rows) * cols;
+    const size_t nm = static_cast<size_t>(dimy) * dimx;
+    DevBuf dvs, dmap;
+    dvs.ensure(nv * sizeof(double), device);
+    dmap.ensure(nm * sizeof(double), device);
+    cudaStream_t st = ctx->own_stream;
+    cuda_check(cudaMemcpyAsync(dvs.p, skw_vs, nv * sizeof(double), cudaMemcpyHostToDevice, st), "H2D");
+    cuda_check(cudaMemcpyAsync(dmap.p, out, nm * sizeof(double), cudaMemcpyHostToDevice, st), "H2D");
+    BatchDev bd = ctx->batch_dev(b, false);
+    cuda_check(launch_unskew_from_vs(bd, dvs.as<double>(), dmap.as<double>(), dimy, dimx, st),
+               "launch unskew");
+    cuda_check(cudaMemcpyAsync(out, dmap.p, nm * sizeof(double), cudaMemcpyDeviceToHost, st), "D2H");
+    cuda_check(cudaStreamSynchronize(st), "sync");
+  });
+}
+
+}  // extern "C"

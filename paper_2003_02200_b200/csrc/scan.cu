@@ -1,0 +1,547 @@
+// Line-of-sight scan kernels for the sDEM pipeline (sm_100a).
+//
+// Replaces sector_viewshed / linear_viewshed_row (reference scan.cpp:8-85).
+//
+// Algorithm. For observer (POV) j0 with absolute height h = row[j0] + h0
+// (double, scan.cpp:76) the reference visits targets k = j0 +- dd, computes
+// theta = (row[k] - h) / dd in FP64 and calls a target visible when theta
+// strictly exceeds the running maximum (scan.cpp:24-34). Its open/close ring
+// bookkeeping telescopes to cv = sum over visible targets of (2*dd + 1)
+// (SURVEY §7 hard part 2), which is what we accumulate.
+//
+// FP32 certified filter. Per target the kernel evaluates
+//     t = ((e - hf) - hl) * fl(1/dd)           (h = hf + hl exactly)
+// in FP32 (packed FADD2/FMUL2). |t - theta| <= 4.01u|theta| (u = 2^-24;
+// DESIGN.md "Certified filter" gives the derivation and the preconditions,
+// which the kernel checks per POV). The state is a band [lo, hi] around the
+// last record r, lo/hi = t_r -+ 10u|t_r|. A target is certainly visible if
+// t > hi and certainly hidden if t < lo; anything in between (near ties,
+// exact ties, collinear terrain) sets a per-lane flag. A flagged POV group
+// (4 POVs x one direction) is not trusted: its cv is discarded and the
+// group is queued for the fixup kernel, which re-runs the reference
+// recurrence in IEEE FP64 (division included) — so every decision that
+// reaches the output is bit-identical to the reference's.
+//
+// Mapping. A CTA owns one skewed row at a time. The row is prefetched with a
+// TMA bulk copy (cp.async.bulk + mbarrier) while the previous row is being
+// scanned, then laid out four times in shared memory: S (forward), S1 (S
+// shifted by one), R (reversed, so the backward scan is a forward scan) and
+// R1, each followed by -inf sentinels so lanes past the row end need no
+// bounds checks. Warps take 128-POV tasks (chunk, direction) longest first;
+// a lane owns 4 consecutive POVs and walks dd in blocks of 4: per block it
+// loads two 16-byte quads (S and S1, which make every packed pair register-
+// aligned) plus one broadcast quad each of 1/dd and 2dd+1. Per target that is
+// 1.5 packed FP32 instructions for t, then 2 FSETP (ALU) and 3 predicated
+// FMA-pipe ops (band update and the ring add), i.e. ~6.6 issue slots for the
+// 4 algorithmic FP32 ops the roofline counts.
+#include <cuda_runtime.h>
+
+#include <cfloat>
+#include <cstdint>
+
+#include "sks_device.cuh"
+
+namespace sks {
+
+namespace {
+
+constexpr int kChunk = 128;  // POVs per warp task
+constexpr int kPad = 144;    // -inf sentinels after each row copy
+constexpr float kBand = 5.9604644775390625e-07f;  // 10 * 2^-24
+
+__host__ __device__ inline int round4(int x) { return (x + 3) & ~3; }
+
+struct SmemLayout {
+  int lp;   // round4(lmax)
+  int lb;   // row buffer length (floats)
+  int lt;   // dd table length (floats)
+  int staging, s, s1, r, r1, inv, xt, total;  // float offsets / total floats
+  __host__ __device__ SmemLayout(int lmax, bool shifted) {
+    lp = round4(lmax);
+    lb = lp + kPad;
+    lt = round4(lmax + 16);
+    staging = 8;  // first 32 bytes: mbarrier + control words
+    s = staging + lp + 8;
+    s1 = s + lb;
+    r = s1 + (shifted ? lb : 0);
+    r1 = r + lb;
+    inv = r1 + (shifted ? lb : 0);
+    xt = inv + lt;
+    total = xt + lt;
+  }
+};
+
+// ---- PTX helpers: mbarrier + TMA bulk copy --------------------------------
+__device__ __forceinline__ unsigned smem_u32(const void* p) {
+  return static_cast<unsigned>(__cvta_generic_to_shared(p));
+}
+__device__ __forceinline__ void mbar_init(uint64_t* bar, unsigned count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count));
+  asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+}
+__device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, unsigned bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)),
+               "r"(bytes)
+               : "memory");
+}
+__device__ __forceinline__ void tma_bulk_g2s(void* dst, const void* src, unsigned bytes,
+                                             uint64_t* bar) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+          smem_u32(dst)),
+      "l"(src), "r"(bytes), "r"(smem_u32(bar))
+      : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, unsigned parity) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n\tWAIT_%=:\n\t"
+      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n\t"
+      "@!p bra WAIT_%=;\n\t}" ::"r"(smem_u32(bar)),
+      "r"(parity)
+      : "memory");
+}
+__device__ __forceinline__ void fence_proxy_async() {
+  asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+}
+
+// ---- the certified per-target step ----------------------------------------
+// Reference semantics of one target (scan.cpp:24-34) under the FP32 filter.
+// Returns the decision; sets flag when the decision is not certified.
+__device__ __forceinline__ bool step1(float t, float X, float& hi, float& lo, float& cv,
+                                      unsigned& flag) {
+  const bool above = t > hi;
+  if (above) {
+    const float at = fabsf(t);
+    hi = __fmaf_rn(at, kBand, t);
+    lo = __fmaf_rn(at, -kBand, t);
+    cv = __fadd_rn(cv, X);
+  } else if (t >= lo) {
+    flag = 1u;
+  }
+  return above;
+}
+
+// Same decisions as 16 x step1 (4 dd steps x 4 POVs). Per target: two
+// FSETP (t > hi: record; t >= lo: not certainly hidden) and four predicated
+// FMA-pipe ops (band update, ring add, and `cvg`, the ring add over every
+// target with t >= lo). cvg == sum(cv) over a flush window iff no target fell
+// inside the uncertainty band (every band target adds 2dd+1 >= 3 to cvg
+// only); both sums are exact integers below 2^24 between flushes.
+__device__ __forceinline__ void block16(const float (&t)[4][4], const float4 X, float (&hi)[4],
+                                        float (&lo)[4], float (&cv)[4], float& cvg) {
+  asm volatile(
+      "{\n\t.reg .pred pg, pa;\n\t.reg .f32 at;\n\t"
+#define ONE(TI, HI, LO, CV, X)                               \
+  "setp.ge.f32 pg, %" #TI ", %" #LO ";\n\t"                  \
+  "setp.gt.f32 pa, %" #TI ", %" #HI ";\n\t"                  \
+  "abs.f32 at, %" #TI ";\n\t"                                \
+  "@pa fma.rn.f32 %" #HI ", at, 0f35200000, %" #TI ";\n\t"   \
+  "@pa fma.rn.f32 %" #LO ", at, 0fB5200000, %" #TI ";\n\t"   \
+  "@pa add.rn.f32 %" #CV ", %" #CV ", %" #X ";\n\t"          \
+  "@pg add.rn.f32 %12, %12, %" #X ";\n\t"
+      // operands: 0-3 hi, 4-7 lo, 8-11 cv, 12 cvg, 13-28 t[i][p] (13 + 4i + p),
+      // 29-32 X
+      ONE(13, 0, 4, 8, 29) ONE(14, 1, 5, 9, 29) ONE(15, 2, 6, 10, 29) ONE(16, 3, 7, 11, 29)
+      ONE(17, 0, 4, 8, 30) ONE(18, 1, 5, 9, 30) ONE(19, 2, 6, 10, 30) ONE(20, 3, 7, 11, 30)
+      ONE(21, 0, 4, 8, 31) ONE(22, 1, 5, 9, 31) ONE(23, 2, 6, 10, 31) ONE(24, 3, 7, 11, 31)
+      ONE(25, 0, 4, 8, 32) ONE(26, 1, 5, 9, 32) ONE(27, 2, 6, 10, 32) ONE(28, 3, 7, 11, 32)
+#undef ONE
+      "}"
+      : "+f"(hi[0]), "+f"(hi[1]), "+f"(hi[2]), "+f"(hi[3]), "+f"(lo[0]), "+f"(lo[1]),
+        "+f"(lo[2]), "+f"(lo[3]), "+f"(cv[0]), "+f"(cv[1]), "+f"(cv[2]), "+f"(cv[3]),
+        "+f"(cvg)
+      : "f"(t[0][0]), "f"(t[0][1]), "f"(t[0][2]), "f"(t[0][3]), "f"(t[1][0]), "f"(t[1][1]),
+        "f"(t[1][2]), "f"(t[1][3]), "f"(t[2][0]), "f"(t[2][1]), "f"(t[2][2]), "f"(t[2][3]),
+        "f"(t[3][0]), "f"(t[3][1]), "f"(t[3][2]), "f"(t[3][3]), "f"(X.x), "f"(X.y), "f"(X.z),
+        "f"(X.w));
+}
+
+__device__ __forceinline__ float2 f2(float a, float b) { return make_float2(a, b); }
+
+// t for the two POV pairs of one dd step: e01/e23 are the (register-aligned)
+// target pairs, nhf/nhl the negated splits of h, inv = fl(1/dd).
+__device__ __forceinline__ void tpair(float2 e01, float2 e23, float2 nhf01, float2 nhf23,
+                                      float2 nhl01, float2 nhl23, float inv, float (&t)[4]) {
+  const float2 iv = f2(inv, inv);
+  const float2 a = __fmul2_rn(__fadd2_rn(__fadd2_rn(e01, nhf01), nhl01), iv);
+  const float2 b = __fmul2_rn(__fadd2_rn(__fadd2_rn(e23, nhf23), nhl23), iv);
+  t[0] = a.x;
+  t[1] = a.y;
+  t[2] = b.x;
+  t[3] = b.y;
+}
+
+// One 128-POV task: POVs y0..y0+3 per lane in buffer B (row copy, forward
+// direction in B's own coordinates), dd = 1..Dw. Returns per-POV cv and the
+// lane flag. kVis: debug path recording decisions of one POV.
+template <bool kShifted, bool kVis>
+__device__ __forceinline__ void scan_task(const float* __restrict__ B,
+                                          const float* __restrict__ B1,
+                                          const float4* __restrict__ INV4,
+                                          const float4* __restrict__ X4, int y0, int L, int Dw,
+                                          const float (&hf)[4], const float (&hl)[4],
+                                          float (&hi)[4], float (&lo)[4], int (&cvi)[4],
+                                          unsigned& flag, int vis_p, uint8_t* vis) {
+  float cv[4] = {0.f, 0.f, 0.f, 0.f};
+  float cvg = 0.f;
+  const float2 nhf01 = f2(-hf[0], -hf[1]), nhf23 = f2(-hf[2], -hf[3]);
+  const float2 nhl01 = f2(-hl[0], -hl[1]), nhl23 = f2(-hl[2], -hl[3]);
+  const float* INV = reinterpret_cast<const float*>(INV4);
+  const float* XT = reinterpret_cast<const float*>(X4);
+
+  if (kVis || !kShifted) {
+    // Straight per-dd loop (debug / no shifted copies); same arithmetic.
+    for (int dd = 1; dd <= Dw; ++dd) {
+      const float inv = INV[dd];
+      const float X = XT[dd];
+      float t[4];
+      const float* e = B + y0 + dd;
+      tpair(f2(e[0], e[1]), f2(e[2], e[3]), nhf01, nhf23, nhl01, nhl23, inv, t);
+#pragma unroll
+      for (int p = 0; p < 4; ++p) {
+        const bool a = step1(t[p], X, hi[p], lo[p], cv[p], flag);
+        if (kVis && p == vis_p) vis[dd - 1] = a ? 1 : 0;
+      }
+      if ((dd & 255) == 0) {
+#pragma unroll
+        for (int p = 0; p < 4; ++p) {
+          cvi[p] += __float2int_rn(cv[p]);
+          cv[p] = 0.f;
+        }
+      }
+    }
+  } else {
+    const float4* Q = reinterpret_cast<const float4*>(B) + (y0 >> 2);
+    const float4* Q1 = reinterpret_cast<const float4*>(B1) + (y0 >> 2);
+    float4 qa = Q[0], qa1 = Q1[0];
+    // partial block: steps i in [i0, i1] of block b (window qa/qb)
+    auto partial = [&](int b, int i0, int i1, float4 qb, float4 qb1) {
+      const float4 iv = INV4[b];
+      const float4 xx = X4[b];
+      const float ivs[4] = {iv.x, iv.y, iv.z, iv.w};
+      const float xs[4] = {xx.x, xx.y, xx.z, xx.w};
+      const float w[8] = {qa.x, qa.y, qa.z, qa.w, qb.x, qb.y, qb.z, qb.w};
+#pragma unroll
+      for (int i = 0; i < 4; ++i) {
+        if (i < i0 || i > i1) continue;
+        float t[4];
+        tpair(f2(w[i], w[i + 1]), f2(w[i + 2], w[i + 3]), nhf01, nhf23, nhl01, nhl23, ivs[i],
+              t);
+#pragma unroll
+        for (int p = 0; p < 4; ++p) step1(t[p], xs[i], hi[p], lo[p], cv[p], flag);
+      }
+    };
+    {
+      const float4 qb = Q[1], qb1 = Q1[1];
+      partial(0, 1, min(3, Dw), qb, qb1);
+      qa = qb;
+      qa1 = qb1;
+#pragma unroll
+      for (int p = 0; p < 4; ++p) {  // windows of the band check start clean
+        cvi[p] += __float2int_rn(cv[p]);
+        cv[p] = 0.f;
+      }
+    }
+    const int blast = (Dw - 3) >> 2;  // last full block (4b+3 <= Dw)
+    int b = 1;
+    while (b <= blast) {
+      const int bend = min(blast, b + 31);  // cvg, cv < 2^24 between flushes
+#pragma unroll 2
+      for (; b <= bend; ++b) {
+        const float4 qb = Q[b + 1];
+        const float4 qb1 = Q1[b + 1];
+        const float4 iv = INV4[b];
+        const float4 xx = X4[b];
+        float t[4][4];
+        tpair(f2(qa.x, qa.y), f2(qa.z, qa.w), nhf01, nhf23, nhl01, nhl23, iv.x, t[0]);
+        tpair(f2(qa1.x, qa1.y), f2(qa1.z, qa1.w), nhf01, nhf23, nhl01, nhl23, iv.y, t[1]);
+        tpair(f2(qa.z, qa.w), f2(qb.x, qb.y), nhf01, nhf23, nhl01, nhl23, iv.z, t[2]);
+        tpair(f2(qa1.z, qa1.w), f2(qb1.x, qb1.y), nhf01, nhf23, nhl01, nhl23, iv.w, t[3]);
+        block16(t, xx, hi, lo, cv, cvg);
+        qa = qb;
+        qa1 = qb1;
+      }
+      // band check for the window, then flush the exact float sums
+      if (cvg != __fadd_rn(__fadd_rn(cv[0], cv[1]), __fadd_rn(cv[2], cv[3]))) flag = 1u;
+      cvg = 0.f;
+#pragma unroll
+      for (int p = 0; p < 4; ++p) {
+        cvi[p] += __float2int_rn(cv[p]);
+        cv[p] = 0.f;
+      }
+    }
+    const int bt = max(1, blast + 1);
+    if (4 * bt <= Dw) {
+      const float4 qb = Q[bt + 1], qb1 = Q1[bt + 1];
+      partial(bt, 0, Dw - 4 * bt, qb, qb1);
+    }
+  }
+#pragma unroll
+  for (int p = 0; p < 4; ++p) cvi[p] += __float2int_rn(cv[p]);
+}
+
+template <bool kShifted, bool kVis>
+__global__ void __launch_bounds__(512, 2) scan_kernel(ScanArgs a) {
+  extern __shared__ __align__(16) float smem[];
+  const SmemLayout lay(a.lmax, kShifted);
+  uint64_t* bar = reinterpret_cast<uint64_t*>(smem);
+  int* ctrl = reinterpret_cast<int*>(smem + 2);  // [0] next item, [1] task counter
+  float* staging = smem + lay.staging;
+  float* S = smem + lay.s;
+  float* S1 = smem + lay.s1;
+  float* R = smem + lay.r;
+  float* R1 = smem + lay.r1;
+  float* INV = smem + lay.inv;
+  float* XT = smem + lay.xt;
+  const int tid = threadIdx.x;
+  const int lane = tid & 31;
+  const int warp = tid >> 5;
+  const int nthreads = blockDim.x;
+
+  auto issue = [&](int it) {
+    const ScanItem item = a.items[it];
+    const SectorDev& sd = a.b.sectors[item.s];
+    const int2 rg = a.b.ranges[sd.row_off + item.q];
+    const int fa = rg.x & ~3;
+    const int la = round4(rg.y);
+    const float* src = a.b.sdem + sd.sdem_off + static_cast<long long>(item.q) * sd.pitch + fa;
+    const unsigned bytes = static_cast<unsigned>(la - fa) * 4u;
+    mbar_expect_tx(bar, bytes);
+    tma_bulk_g2s(staging, src, bytes, bar);
+  };
+
+  if (tid == 0) {
+    mbar_init(bar, 1);
+    const int it = static_cast<int>(atomicAdd(a.item_counter, 1u));
+    ctrl[0] = it;
+    if (it < a.n_items) issue(it);
+  }
+  for (int d = tid; d < lay.lt; d += nthreads) {
+    INV[d] = d == 0 ? 0.0f : __frcp_rn(static_cast<float>(d));
+    XT[d] = static_cast<float>(2 * d + 1);
+  }
+  __syncthreads();
+
+  unsigned phase = 0;
+  for (;;) {
+    const int cur = ctrl[0];
+    if (cur >= a.n_items) break;
+    const ScanItem item = a.items[cur];
+    const SectorDev sd = a.b.sectors[item.s];
+    const int2 rg = a.b.ranges[sd.row_off + item.q];
+    const int first = rg.x;
+    const int L = rg.y - rg.x;
+    const int off = first & 3;
+    mbar_wait(bar, phase);
+    phase ^= 1u;
+    const float ninf = -INFINITY;
+    for (int x = tid; x < lay.lb; x += nthreads) {
+      S[x] = x < L ? staging[off + x] : ninf;
+      R[x] = x < L ? staging[off + L - 1 - x] : ninf;
+      if (kShifted) {
+        S1[x] = x + 1 < L ? staging[off + x + 1] : ninf;
+        R1[x] = x + 1 < L ? staging[off + L - 2 - x] : ninf;
+      }
+    }
+    if (tid == 0) ctrl[1] = 0;
+    __syncthreads();
+    if (tid == 0) {
+      fence_proxy_async();
+      const int it = static_cast<int>(atomicAdd(a.item_counter, 1u));
+      ctrl[0] = it;
+      if (it < a.n_items) issue(it);
+    }
+    const int nchunks = (L + kChunk - 1) / kChunk;
+    const int ntasks = 2 * nchunks;
+    const int max_dd = sd.max_dd;
+    int* cvrow = a.b.cv + sd.sdem_off + static_cast<long long>(item.q) * sd.pitch;
+    int* cvrow_b =
+        (a.b.cv_bwd ? a.b.cv_bwd : a.b.cv) + sd.sdem_off + static_cast<long long>(item.q) * sd.pitch;
+    // Warps claim tasks (chunk, direction) longest first; the CTA barrier
+    // after the loop closes the row.
+    for (;;) {
+      int task = 0;
+      if (lane == 0) task = atomicAdd(&ctrl[1], 1);
+      const int tsk = __shfl_sync(0xffffffffu, task, 0);
+      if (tsk >= ntasks) break;
+      const int dir = tsk & 1;
+      const int chunk = tsk >> 1;
+      const int Dw = min(max_dd, L - 1 - chunk * kChunk);
+      if (Dw <= 0) continue;
+      const float* B = dir ? R : S;
+      const float* B1 = dir ? R1 : S1;
+      const int y0 = chunk * kChunk + lane * 4;
+      float hf[4], hl[4], hi[4], lo[4];
+      int cvi[4] = {0, 0, 0, 0};
+      unsigned flag = a.force_exact ? 1u : 0u;
+      bool any_valid = false;
+      int vis_p = -1;
+#pragma unroll
+      for (int p = 0; p < 4; ++p) {
+        const int y = y0 + p;
+        if (y < L) {
+          any_valid = true;
+          const int x = dir ? (L - 1 - y) : y;
+          double h;
+          if (a.dbg_j0 >= 0 && item.s == 0 && item.q == 0 && first + x == a.dbg_j0) {
+            h = a.dbg_h;
+            vis_p = p;
+          } else {
+            h = __dadd_rn(static_cast<double>(B[y]), a.h0);
+          }
+          const float hff = __double2float_rn(h);
+          const double hld = __dsub_rn(h, static_cast<double>(hff));
+          const float hlf = __double2float_rn(hld);
+          // preconditions of the certified filter: h splits
+          // exactly into two floats and stays far from overflow.
+          if (static_cast<double>(hlf) != hld || !(fabsf(hff) < 1e30f)) flag = 1u;
+          hf[p] = hff;
+          hl[p] = hlf;
+          hi[p] = -INFINITY;
+          lo[p] = -FLT_MAX;
+        } else {
+          hf[p] = 0.f;
+          hl[p] = 0.f;
+          hi[p] = INFINITY;
+          lo[p] = INFINITY;
+        }
+      }
+      uint8_t* vis = nullptr;
+      if (kVis && vis_p >= 0) vis = dir ? a.dbg_vis_bwd : a.dbg_vis_fwd;
+      scan_task<kShifted, kVis>(B, B1, reinterpret_cast<const float4*>(INV),
+                                reinterpret_cast<const float4*>(XT), y0, L, Dw, hf, hl, hi, lo,
+                                cvi, flag, vis ? vis_p : -1, vis);
+      if (!any_valid) continue;
+      if (flag) {
+        const unsigned slot = atomicAdd(a.fix_count, 1u);
+        if (slot < a.fix_cap) {
+          a.fix_queue[slot] = pack_fix(static_cast<unsigned>(item.s),
+                                       static_cast<unsigned>(item.q),
+                                       static_cast<unsigned>(dir),
+                                       static_cast<unsigned>(y0 >> 2));
+        }
+      } else {
+        int* dst = dir ? cvrow_b : cvrow;
+#pragma unroll
+        for (int p = 0; p < 4; ++p) {
+          const int y = y0 + p;
+          if (y < L && cvi[p] != 0) {
+            const int x = dir ? (L - 1 - y) : y;
+            atomicAdd(dst + first + x, cvi[p]);
+          }
+        }
+      }
+    }
+    __syncthreads();
+  }
+}
+
+// Exact FP64 re-scan of flagged POV groups: one warp per queue entry. Each
+// POV's targets are split across lanes 32 at a time; theta is computed with
+// the reference's IEEE operations ((double)row[k] - h) / dd, the running
+// maximum before each target is an exclusive warp prefix max (max is exact,
+// so association order is irrelevant), and visible targets add 2dd+1.
+__global__ void __launch_bounds__(256) fixup_kernel(ScanArgs a) {
+  const unsigned n = min(*a.fix_count, a.fix_cap);
+  const int lane = threadIdx.x & 31;
+  const unsigned gw = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const unsigned nw = (gridDim.x * blockDim.x) >> 5;
+  for (unsigned e = gw; e < n; e += nw) {
+    const unsigned long long v = a.fix_queue[e];
+    const int s = static_cast<int>(v >> 45);
+    const int q = static_cast<int>((v >> 23) & 0x3fffffu);
+    const int dir = static_cast<int>((v >> 22) & 1u);
+    const int g = static_cast<int>(v & 0x3fffffu);
+    const SectorDev sd = a.b.sectors[s];
+    const int2 rg = a.b.ranges[sd.row_off + q];
+    const int first = rg.x;
+    const int L = rg.y - rg.x;
+    const float* rowp = a.b.sdem + sd.sdem_off + static_cast<long long>(q) * sd.pitch;
+    int* dst = ((dir && a.b.cv_bwd) ? a.b.cv_bwd : a.b.cv) + sd.sdem_off +
+               static_cast<long long>(q) * sd.pitch;
+    for (int p = 0; p < 4; ++p) {
+      const int y = 4 * g + p;
+      if (y >= L) break;
+      const int x = dir ? (L - 1 - y) : y;
+      const int j0 = first + x;
+      const bool dbg = a.dbg_j0 >= 0 && s == 0 && q == 0 && j0 == a.dbg_j0;
+      const double h = dbg ? a.dbg_h : __dadd_rn(static_cast<double>(rowp[j0]), a.h0);
+      const int D = min(sd.max_dd, dir ? x : (L - 1 - x));
+      uint8_t* vis = dbg ? (dir ? a.dbg_vis_bwd : a.dbg_vis_fwd) : nullptr;
+      long long cv = 0;
+      double carry = -INFINITY;
+      for (int base = 0; base < D; base += 32) {
+        const int dd = base + lane + 1;
+        const bool valid = dd <= D;
+        double th = -INFINITY;
+        if (valid) {
+          const int k = dir ? (j0 - dd) : (j0 + dd);
+          th = __ddiv_rn(__dsub_rn(static_cast<double>(rowp[k]), h), static_cast<double>(dd));
+        }
+        double incl = th;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+          const double u = __shfl_up_sync(0xffffffffu, incl, o);
+          if (lane >= o) incl = fmax(incl, u);
+        }
+        double excl = __shfl_up_sync(0xffffffffu, incl, 1);
+        if (lane == 0) excl = -INFINITY;
+        excl = fmax(excl, carry);
+        const bool above = valid && th > excl;
+        if (above) cv += 2LL * dd + 1;
+        if (vis && valid) vis[dd - 1] = above ? 1 : 0;
+        carry = fmax(carry, __shfl_sync(0xffffffffu, incl, 31));
+      }
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) cv += __shfl_xor_sync(0xffffffffu, cv, o);
+      if (lane == 0 && cv != 0) atomicAdd(dst + j0, static_cast<int>(cv));
+    }
+  }
+}
+
+}  // namespace
+
+size_t scan_smem_bytes(int lmax, bool shifted) {
+  return static_cast<size_t>(SmemLayout(lmax, shifted).total) * sizeof(float);
+}
+
+static bool use_shifted(int lmax) { return scan_smem_bytes(lmax, true) <= 220 * 1024 && lmax <= 16000; }
+
+int scan_block_threads(int lmax) { return use_shifted(lmax) ? 512 : 512; }
+
+int scan_occupancy(int lmax, int* grid_out) {
+  int dev = 0;
+  cudaGetDevice(&dev);
+  int sms = 0;
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  const bool sh = use_shifted(lmax);
+  const size_t smem = scan_smem_bytes(lmax, sh);
+  auto fn = sh ? scan_kernel<true, false> : scan_kernel<false, false>;
+  cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                       static_cast<int>(smem));
+  if (e != cudaSuccess) return static_cast<int>(e);
+  int per_sm = 0;
+  e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fn, scan_block_threads(lmax), smem);
+  if (e != cudaSuccess) return static_cast<int>(e);
+  *grid_out = sms * (per_sm > 0 ? per_sm : 1);
+  return 0;
+}
+
+int launch_scan(const ScanArgs& a, int grid, void* stream) {
+  const bool vis = a.dbg_vis_fwd != nullptr || a.dbg_vis_bwd != nullptr;
+  const bool sh = use_shifted(a.lmax) && !vis;
+  const size_t smem = scan_smem_bytes(a.lmax, sh);
+  auto fn = vis ? scan_kernel<false, true> : (sh ? scan_kernel<true, false> : scan_kernel<false, false>);
+  cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                       static_cast<int>(smem));
+  if (e != cudaSuccess) return static_cast<int>(e);
+  fn<<<grid, scan_block_threads(a.lmax), smem, static_cast<cudaStream_t>(stream)>>>(a);
+  return static_cast<int>(cudaGetLastError());
+}
+
+int launch_fixup(const ScanArgs& a, int grid, void* stream) {
+  fixup_kernel<<<grid, 256, 0, static_cast<cudaStream_t>(stream)>>>(a);
+  return static_cast<int>(cudaGetLastError());
+}
+
+}  // namespace sks

@@ -1,0 +1,102 @@
+// Device-side data layout shared by the sm_100a kernels and the engine.
+//
+// HBM layout for one batch of sectors:
+//   * dem      : dimy x dimx float32, row-major (the caller's DEM, resident).
+//   * sdem pool: for each sector slot s, skw_rows_s x pitch_s float32
+//                (pitch a multiple of 32 floats = 128 B), at sdem_off_s.
+//   * cv pool  : same geometry as the sdem pool, int32 per skewed cell: the
+//                exact integer ring sum cv = sum over visible targets of
+//                (2*dd+1), forward + backward (SURVEY §7 hard part 2).
+//   * column tables (per sector, at col_off): dest int32, fracf float32,
+//                fracd float64 (skew.cpp:155-158, 222-227).
+//   * row ranges (per sector, at row_off): int2 [first, last).
+//   * map      : dimy x dimx float64, the raw total-viewshed accumulator.
+#pragma once
+
+#include <cstdint>
+
+namespace sks {
+
+struct SectorDev {
+  int k;
+  int rows, cols;          // pre_ops space
+  int src_rows, src_cols;  // DEM space
+  int base, skw_rows, pitch;
+  int max_dd;
+  int col_off;   // into dest / fracf / fracd
+  int row_off;   // into ranges
+  int pad0;
+  int map[6];    // pre (i, j) -> DEM (si, sj)
+  int inv[6];    // DEM (si, sj) -> pre (i, j)
+  double correction;  // 1 + tan^2
+  long long sdem_off;  // element offset of this sector in the sdem / cv pools
+};
+
+// One unit of scan work: skewed row q of sector slot s (L >= 2).
+struct ScanItem {
+  int s;
+  int q;
+};
+
+struct BatchDev {
+  const SectorDev* sectors;
+  int n_sectors;
+  const int* dest;
+  const float* fracf;
+  const double* fracd;
+  const int2* ranges;
+  float* sdem;
+  int* cv;
+  int* cv_bwd;  // debug: backward scan results kept apart (nullptr = cv)
+};
+
+struct ScanArgs {
+  BatchDev b;
+  const ScanItem* items;
+  int n_items;
+  int lmax;               // longest row length in the batch
+  unsigned* item_counter; // zero before launch
+  unsigned long long* fix_queue;
+  unsigned* fix_count;    // zero before launch
+  unsigned fix_cap;
+  double h0;
+  // debug single-POV mode (sks_linear_viewshed_row): POV j0 of row 0 of
+  // sector slot 0 uses the absolute height h_abs; its per-target decisions
+  // are written to vis (one byte per target, forward or backward).
+  int dbg_j0;
+  double dbg_h;
+  uint8_t* dbg_vis_fwd;
+  uint8_t* dbg_vis_bwd;
+  int force_exact;        // every POV group goes through the FP64 fixup
+};
+
+// Packed fixup entry: sector slot (10 b) | q (22 b) | dir (1 b) | group (22 b)
+__host__ __device__ inline unsigned long long pack_fix(unsigned s, unsigned q,
+                                                       unsigned dir,
+                                                       unsigned g) {
+  return (static_cast<unsigned long long>(s) << 45) |
+         (static_cast<unsigned long long>(q) << 23) |
+         (static_cast<unsigned long long>(dir) << 22) |
+         static_cast<unsigned long long>(g);
+}
+
+// Kernel entry points (launch wrappers). All return the launch error.
+// grid: (tiles_total, n_sectors); tile t -> (t / tiles_x, t % tiles_x)
+int launch_relocate_grid(const float* dem, const BatchDev& b, int tiles_x,
+                         int tiles_total, void* stream);
+int relocate_tile_rows();
+int relocate_tile_cols();
+size_t scan_smem_bytes(int lmax, bool shifted);
+int scan_block_threads(int lmax);
+int launch_scan(const ScanArgs& a, int grid, void* stream);
+int scan_occupancy(int lmax, int* grid_out);
+int launch_fixup(const ScanArgs& a, int grid, void* stream);
+int launch_unskew(const BatchDev& b, const float* unused, double* map,
+                  int dimy, int dimx, void* stream);
+int launch_unskew_from_vs(const BatchDev& b, const double* skw_vs,
+                          double* map, int dimy, int dimx, void* stream);
+int launch_scale(double* map, long long n, double factor, void* stream);
+int launch_cv_to_vs(const int* cvf, const int* cvb, double* out,
+                    long long n, double correction, void* stream);
+
+}  // namespace sks

@@ -1,0 +1,69 @@
+"""Sector sharding over GPUs with one reduce of the viewshed maps.
+
+Replaces the reference's single-process sector pool (engine.cpp:115-176) and
+the paper's host-side multi-GPU reduction (Alg. 10): one process per
+GPU (torch.distributed, NCCL over NVLink), sectors assigned statically by
+longest-processing-time on their exact scan work (sks_partition_sectors),
+each rank accumulating its sectors in ascending k into a private FP64 map on
+its GPU, then a single ``reduce(SUM)`` of the maps to rank 0. That reduce is
+the path's only exchange step; the DEM itself is copied host->device on every
+rank (it is the caller's input).
+
+``compute`` lets CPU tests (gloo, world_size 2) exercise exactly this
+sharding/reduce logic with the oracle standing in for the GPU pipeline; the
+product path (compute=None) always runs the CUDA kernels.
+"""
+from __future__ import annotations
+
+from typing import Callable, Optional, Sequence
+
+import numpy as np
+
+from .engine import RunConfig, Units, area_scale_factor, partition_sectors
+
+
+def my_sectors(ns: int, dimy: int, dimx: int, world: int, rank: int, cellsize: float = 1.0,
+               max_distance: Optional[float] = None) -> list:
+    owner = partition_sectors(ns, dimy, dimx, world, cellsize, max_distance)
+    return [k for k in range(ns // 2) if int(owner[k]) == rank]
+
+
+def total_viewshed_distributed(dem: np.ndarray, cellsize: float, cfg: RunConfig, raw: bool = False,
+                               compute: Optional[Callable[[Sequence[int]], np.ndarray]] = None,
+                               context=None, stream=None, stats: Optional[dict] = None):
+    """Total viewshed of ``dem`` sharded over the default process group.
+
+    Returns the (scaled unless ``raw``) map on rank 0 and None elsewhere.
+    """
+    import torch
+    import torch.distributed as dist
+
+    rank, world = dist.get_rank(), dist.get_world_size()
+    dimy, dimx = dem.shape
+    mine = my_sectors(cfg.ns, dimy, dimx, world, rank, cellsize, cfg.max_distance)
+    factor = area_scale_factor(cfg, cellsize)
+    if compute is not None:
+        part = torch.from_numpy(np.ascontiguousarray(compute(mine), dtype=np.float64))
+        dist.reduce(part, dst=0, op=dist.ReduceOp.SUM)
+        if rank != 0:
+            return None
+        out = part.numpy()
+        return out if raw else out * factor
+
+    from .engine import Context
+    dev = torch.device("cuda", torch.cuda.current_device())
+    ctx = context or Context(dev.index)
+    st = stream or torch.cuda.current_stream(dev)
+    d_dem = torch.from_numpy(np.ascontiguousarray(dem, np.float32)).to(dev, non_blocking=True)
+    d_map = torch.zeros((dimy, dimx), dtype=torch.float64, device=dev)
+    es = ctx.run_sectors(d_dem.data_ptr(), dimy, dimx, cellsize, cfg, mine, d_map.data_ptr(),
+                         stream=st.cuda_stream, want_stats=stats is not None)
+    if stats is not None:
+        stats["rank_stats"] = es
+        stats["sectors"] = mine
+    dist.reduce(d_map, dst=0, op=dist.ReduceOp.SUM)
+    if rank != 0:
+        return None
+    if not raw:
+        ctx.scale(d_map.data_ptr(), dimy * dimx, cfg.ns, cellsize, int(cfg.units), st.cuda_stream)
+    return d_map.cpu().numpy()

@@ -1,0 +1,349 @@
+"""GPU parity tests: the CUDA path (through the C ABI) against the oracle.
+
+The oracle is the reference itself (oracle/_ref/libskewshed_ref.so, compiled
+from the unmodified reference sources) when present, else the C
+restatement (oracle/liboracle.so), which tests/test_oracle.py pins to the
+reference bit-for-bit. Bars:
+  * relocation: sDEM values and row ranges bit-exact (P1)
+  * scan: per-POV cv and skwVS bit-exact; per-target visibility bit-exact (P2)
+  * unskew: bit-exact (P3)
+  * end to end on one GPU: bit-exact to total_viewshed_raw (P4, stronger
+    than the 1e-5 relative bar)
+"""
+import numpy as np
+import pytest
+
+import paper_2003_02200_b200 as sk
+from _oracle import NO_CAP, Orc, Ref, have_ref
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module")
+def ora():
+    return Ref() if have_ref() else Orc()
+
+
+def b32(a):
+    return np.ascontiguousarray(a).view(np.uint32)
+
+
+def b64(a):
+    return np.ascontiguousarray(a).view(np.uint64)
+
+
+# ---- P1 relocation ---------------------------------------------------------
+
+@pytest.mark.parametrize("shape,kind,ns", [
+    ((64, 64), sk.SyntheticKind.SmoothedNoise, 180),
+    ((24, 40), sk.SyntheticKind.SmoothedNoise, 36),
+    ((40, 24), sk.SyntheticKind.Fractal, 36),
+    ((33, 33), sk.SyntheticKind.Cone, 360),
+    ((2, 2), sk.SyntheticKind.Ramp, 8),
+    ((130, 70), sk.SyntheticKind.Fractal, 24),
+])
+def test_relocation_bitexact_every_sector(ora, shape, kind, ns):
+    dem = sk.make_synthetic(kind, *shape, 10.0, 7).values
+    for k in range(ns // 2):
+        p = sk.plan_sector(k, ns, *shape)
+        pre = ora.apply_pre_ops(dem, k, ns)
+        v, _w, rr, base = ora.build_skw(pre, p.shear_tan)
+        g = sk.build_sector_sdem(dem, k, ns)
+        assert g.base == base
+        assert np.array_equal(g.row_ranges, rr), k
+        assert np.array_equal(b32(g.values), b32(v)), k
+
+
+def test_build_skw_arbitrary_shears(ora):
+    rng = np.random.default_rng(99)
+    g = (rng.standard_normal((37, 53)) * 100).astype(np.float32)
+    g[3, 4] = -0.0
+    g[5, :] = -2.5
+    for t in [0.0, 1.0, 1e-7, 1 - 1e-7, 0.5, *rng.random(8)]:
+        ours = sk.build_skw(g, float(t))
+        v, _w, rr, base = ora.build_skw(g, float(t))
+        assert ours.base == base
+        assert np.array_equal(ours.row_ranges, rr)
+        assert np.array_equal(b32(ours.values), b32(v))
+
+
+def test_relocation_2000_sampled_sectors(ora):
+    dem = sk.make_synthetic(sk.SyntheticKind.Fractal, 2000, 2000, 10.0, 7).values
+    for k in [0, 1, 22, 44, 45, 46, 67, 89]:
+        p = sk.plan_sector(k, 180, 2000, 2000)
+        pre = ora.apply_pre_ops(dem, k, 180)
+        v, _w, rr, base = ora.build_skw(pre, p.shear_tan)
+        g = sk.build_sector_sdem(dem, k, 180)
+        assert np.array_equal(g.row_ranges, rr), k
+        assert np.array_equal(b32(g.values), b32(v)), k
+
+
+# ---- P2 scan -----------------------------------------------------------------
+
+def _ref_sdem(ora, dem, k, ns):
+    p = sk.plan_sector(k, ns, *dem.shape)
+    pre = ora.apply_pre_ops(dem, k, ns)
+    v, _w, rr, base = ora.build_skw(pre, p.shear_tan)
+    return p, v, rr, base
+
+
+@pytest.mark.parametrize("kind", [sk.SyntheticKind.SmoothedNoise, sk.SyntheticKind.Fractal,
+                                  sk.SyntheticKind.Cone, sk.SyntheticKind.Ramp, sk.SyntheticKind.Flat])
+@pytest.mark.parametrize("max_dd", [NO_CAP, 0, 1, 7])
+def test_sector_viewshed_bitexact(ora, kind, max_dd):
+    dem = sk.make_synthetic(kind, 48, 40, 10.0, 11).values
+    for k in range(0, 18):
+        p, v, rr, base = _ref_sdem(ora, dem, k, 36)
+        ref = ora.sector_viewshed(v, rr, p.rows, base, p.shear_tan, 1.5, max_dd)
+        skw = sk.SkwGrid(v, rr, base, p.rows, p.shear_tan)
+        ours = sk.sector_viewshed(skw, 1.5, max_dd)
+        assert np.array_equal(b64(ours), b64(ref)), (kind, max_dd, k)
+
+
+@pytest.mark.parametrize("h0", [0.0, 1.5, 1.7, 30.0])
+def test_sector_viewshed_observer_heights(ora, h0):
+    # h0 = 0 on a ramp makes collinear targets exact ties (not visible,
+    # scan.cpp:25); 1.7 is not a float, so the filter's exact-split check
+    # routes those POVs to the FP64 fixup.
+    for kind in (sk.SyntheticKind.Ramp, sk.SyntheticKind.Fractal, sk.SyntheticKind.Cone):
+        dem = sk.make_synthetic(kind, 40, 40, 10.0, 3).values
+        for k in (0, 5, 9, 13):
+            p, v, rr, base = _ref_sdem(ora, dem, k, 36)
+            ref = ora.sector_viewshed(v, rr, p.rows, base, p.shear_tan, h0)
+            ours = sk.sector_viewshed(sk.SkwGrid(v, rr, base, p.rows, p.shear_tan), h0)
+            assert np.array_equal(b64(ours), b64(ref)), (kind, k, h0)
+
+
+def test_scan_long_rows_sampled_pov_parity(ora):
+    """2000^2 fractal: full GPU sector scan vs the reference's own
+    linear_viewshed_row on sampled POVs (both directions)."""
+    dem = sk.make_synthetic(sk.SyntheticKind.Fractal, 2000, 2000, 10.0, 7).values
+    rng = np.random.default_rng(5)
+    for k in (0, 17, 45, 71):
+        p, v, rr, base = _ref_sdem(ora, dem, k, 180)
+        _out, cvf, cvb = sk.sector_viewshed(sk.SkwGrid(v, rr, base, p.rows, p.shear_tan), 1.5,
+                                            return_cv=True)
+        rows = np.nonzero(rr[:, 1] - rr[:, 0] >= 2)[0]
+        for q in rng.choice(rows, 40, replace=False):
+            first, last = rr[q]
+            for j0 in rng.integers(first, last, 12):
+                h = float(v[q, j0]) + 1.5
+                f = ora.linear_viewshed_row(v[q], first, last, j0, h, 0)
+                b = ora.linear_viewshed_row(v[q], first, last, j0, h, 1)
+                assert cvf[q, j0] == f and cvb[q, j0] == b, (k, q, j0)
+
+
+def test_visibility_vectors(ora):
+    rng = np.random.default_rng(7)
+    for trial in range(60):
+        n = int(rng.integers(2, 300))
+        kind = trial % 3
+        if kind == 0:
+            row = (rng.random(n) * 50).astype(np.float32)
+        elif kind == 1:
+            row = np.cumsum(rng.standard_normal(n)).astype(np.float32) + 500
+        else:
+            row = np.linspace(0, 1, n, dtype=np.float32)  # ramp: near ties
+        first = int(rng.integers(0, n - 1))
+        last = int(rng.integers(first + 1, n + 1))
+        j0 = int(rng.integers(first, last))
+        h = float(row[j0]) + [0.0, 1.5, 0.3][trial % 3]
+        for d in (0, 1):
+            for cap in (NO_CAP, int(rng.integers(0, 20))):
+                cv, vis = sk.linear_viewshed_row(row, first, last, j0, h, d, cap, want_visible=True)
+                rcv, rvis = ora.linear_viewshed_row(row, first, last, j0, h, d, cap, want_visible=True)
+                assert cv == rcv
+                assert np.array_equal(vis, rvis)
+
+
+# ---- KATs from the reference's scan tests (test_scan.cpp) -------------------
+
+def test_kat_flat_row():  # test_scan.cpp:48-53
+    assert sk.linear_viewshed_row(np.zeros(5, np.float32), 0, 5, 0, 1.5, sk.ScanDir.Forward) == 24.0
+
+
+def test_kat_single_target():  # :55-59
+    assert sk.linear_viewshed_row(np.array([3, 17], np.float32), 0, 2, 0, 5.0, sk.ScanDir.Forward) == 3.0
+
+
+def test_kat_near_wall():  # :61-67
+    row = np.array([0, 5, 0, 0, 10, 0], np.float32)
+    assert sk.linear_viewshed_row(row, 0, 6, 0, 1.0, sk.ScanDir.Forward) == 3.0
+
+
+def test_kat_empty_range():  # :69-73
+    row = np.zeros(3, np.float32)
+    assert sk.linear_viewshed_row(row, 0, 1, 0, 1.5, sk.ScanDir.Forward) == 0.0
+    assert sk.linear_viewshed_row(row, 2, 3, 2, 1.5, sk.ScanDir.Backward) == 0.0
+
+
+def test_kat_reversal_symmetry():  # :75-90
+    rng = np.random.default_rng(21)
+    for _ in range(50):
+        n = int(2 + rng.integers(0, 30))
+        row = (rng.integers(0, 1000, n) / 10.0).astype(np.float32)
+        j0 = int(rng.integers(0, n))
+        h = float(row[j0]) + 1.5
+        fwd = sk.linear_viewshed_row(row, 0, n, j0, h, sk.ScanDir.Forward)
+        bwd = sk.linear_viewshed_row(row[::-1].copy(), 0, n, n - 1 - j0, h, sk.ScanDir.Backward)
+        assert fwd == bwd
+
+
+def test_kat_descending_all_visible():  # :92-102
+    for L in (1, 4, 9):
+        row = np.array([100.0 - 2.0 * k for k in range(L + 1)], np.float32)
+        cv, vis = sk.linear_viewshed_row(row, 0, L + 1, 0, float(row[0]) + 1.5, sk.ScanDir.Forward,
+                                         want_visible=True)
+        assert cv == (L + 1) ** 2 - 1.0
+        assert vis.tolist() == [1] * L
+
+
+def test_kat_distance_cap():  # :145-150
+    assert sk.linear_viewshed_row(np.zeros(11, np.float32), 0, 11, 0, 1.5, sk.ScanDir.Forward, 3) == 15.0
+
+
+def test_kat_flat_zero_shear_formula():  # :152-164
+    dem = sk.make_synthetic(sk.SyntheticKind.Flat, 5, 9, 10.0)
+    vs = sk.sector_viewshed(sk.build_skw(dem.values, 0.0), 1.5)
+    for i in range(5):
+        for j0 in range(9):
+            east, west = 9.0 - 1 - j0, j0
+            assert vs[5 + i, j0] == (east + 1) ** 2 - 1 + (west + 1) ** 2 - 1
+
+
+def test_kat_diagonal_factor_two():  # :166-181
+    dem = sk.make_synthetic(sk.SyntheticKind.Flat, 4, 4, 10.0)
+    skw = sk.build_skw(dem.values, 1.0)
+    vs = sk.sector_viewshed(skw, 1.5)
+    for q in range(skw.skw_rows()):
+        first, last = skw.row_ranges[q]
+        for j0 in range(first, last):
+            east, west = last - 1 - j0, j0 - first
+            assert vs[q, j0] == 2.0 * ((east + 1) ** 2 - 1 + (west + 1) ** 2 - 1)
+
+
+def test_kat_outside_ranges_zero():  # :197-213
+    dem = sk.make_synthetic(sk.SyntheticKind.SmoothedNoise, 12, 12, 10.0, 9)
+    t = np.tan(np.deg2rad(20.0))
+    skw = sk.build_skw(dem.values, float(t))
+    vs = sk.sector_viewshed(skw, 1.5)
+    for q in range(skw.skw_rows()):
+        first, last = skw.row_ranges[q]
+        for j in range(skw.cols):
+            if j < first or j >= last:
+                assert vs[q, j] == 0.0
+            else:
+                assert np.isfinite(vs[q, j]) and vs[q, j] >= 0.0
+
+
+def test_acceptance_flat_scan_formula():  # acceptance_main.cpp:218-251 (criterion 4)
+    n, ns = 33, 360
+    dem = np.zeros((n, n), np.float32)
+    scans = 0
+    for k in range(ns // 2):
+        g = sk.build_sector_sdem(dem, k, ns)
+        _out, cvf, _cvb = sk.sector_viewshed(g, 1.5, return_cv=True)
+        for q in range(g.skw_rows()):
+            first, last = g.row_ranges[q]
+            for j0 in range(first, last):
+                L = last - 1 - j0
+                assert cvf[q, j0] == (L + 1) ** 2 - 1
+                scans += 1
+    assert scans == 190388
+
+
+# ---- P3 unskew -----------------------------------------------------------------
+
+@pytest.mark.parametrize("shape,ns", [((48, 40), 36), ((40, 48), 36), ((32, 32), 360), ((2, 2), 8)])
+def test_unskew_bitexact(ora, shape, ns):
+    dem = sk.make_synthetic(sk.SyntheticKind.Fractal, *shape, 10.0, 5).values
+    for k in range(ns // 2):
+        p, v, rr, base = _ref_sdem(ora, dem, k, ns)
+        vs = ora.sector_viewshed(v, rr, p.rows, base, p.shear_tan, 1.5)
+        init = np.random.default_rng(k).random(shape)
+        ref = ora.unskew_accumulate(vs, k, ns, *shape, out=init.copy())
+        ours = init.copy()
+        sk.unskew_accumulate(vs, p, ours)
+        assert np.array_equal(b64(ours), b64(ref)), k
+
+
+def test_round_trip_bitwise_integer_shears():  # test_skew.cpp:286-303
+    dem = sk.make_synthetic(sk.SyntheticKind.SmoothedNoise, 16, 16, 10.0, 5)
+    for k in (0, 45):
+        p = sk.plan_sector(k, 360, 16, 16)
+        g = sk.build_sector_sdem(dem.values, k, 360)
+        out = np.zeros((16, 16))
+        sk.unskew_accumulate(g.values.astype(np.float64), p, out)
+        assert np.array_equal(out, dem.values.astype(np.float64))
+
+
+def test_unskew_rejects_mismatched_shapes():
+    p = sk.plan_sector(0, 360, 6, 6)
+    with pytest.raises(ValueError):
+        sk.unskew_accumulate(np.zeros((11, 6)), p, np.zeros((6, 6)))
+    with pytest.raises(ValueError):
+        sk.unskew_accumulate(np.zeros((12, 6)), p, np.zeros((5, 6)))
+
+
+# ---- P4 end to end -------------------------------------------------------------
+
+@pytest.mark.parametrize("shape,kind,ns,maxd", [
+    ((48, 40), sk.SyntheticKind.SmoothedNoise, 36, None),
+    ((40, 48), sk.SyntheticKind.Fractal, 36, None),
+    ((64, 64), sk.SyntheticKind.Fractal, 180, 150.0),
+    ((32, 32), sk.SyntheticKind.Cone, 90, None),
+    ((24, 40), sk.SyntheticKind.Ramp, 2, None),
+    ((2, 2), sk.SyntheticKind.SmoothedNoise, 8, None),
+])
+def test_total_viewshed_raw_bitexact(ora, shape, kind, ns, maxd):
+    dem = sk.make_synthetic(kind, *shape, 10.0, 13)
+    cfg = sk.RunConfig(ns=ns, h0=1.5, max_distance=maxd, units=sk.Units.SquareMeters)
+    ours = sk.total_viewshed_raw(dem, cfg)
+    ref = ora.total_viewshed(dem.values, 10.0, ns, 1.5, max_distance=maxd or 0.0, raw=True)
+    assert np.array_equal(b64(ours), b64(ref))
+
+
+def test_total_viewshed_units_and_scale(ora):
+    dem = sk.make_synthetic(sk.SyntheticKind.SmoothedNoise, 16, 16, 10.0, 1)
+    for units in (sk.Units.SquareMeters, sk.Units.SquareKilometers):
+        cfg = sk.RunConfig(ns=36, units=units)
+        ours = sk.total_viewshed(dem, cfg)
+        ref = ora.total_viewshed(dem.values, 10.0, 36, 1.5, units=int(units))
+        assert ours.units == units
+        assert np.array_equal(b64(ours.values), b64(ref))
+
+
+def test_sector_sweep_bitexact(ora):
+    dem = sk.make_synthetic(sk.SyntheticKind.Fractal, 40, 40, 10.0, 5)
+    cfg = sk.RunConfig(ns=180)
+    for k in (0, 5, 45, 67, 89):
+        ours = sk.sector_sweep(dem, cfg, k).contribution
+        ref = ora.sector_sweep(dem.values, 10.0, 180, 1.5, 0.0, k)
+        assert np.array_equal(b64(ours), b64(ref))
+
+
+def test_config1_500_fractal_end_to_end(ora):
+    """BASELINE config 1: 500^2 fractal, 180 sectors, h0 1.5, unlimited."""
+    dem = sk.make_synthetic(sk.SyntheticKind.Fractal, 500, 500, 10.0, 7)
+    cfg = sk.RunConfig(ns=180, h0=1.5, units=sk.Units.SquareMeters)
+    stats = sk.EngineStats()
+    ours = sk.total_viewshed(dem, cfg, stats)
+    ref = ora.total_viewshed(dem.values, 10.0, 180, 1.5)
+    assert np.array_equal(b64(ours.values), b64(ref))
+    assert stats.sectors == 90 and stats.kernel_launches > 0
+
+
+def test_rejects_bad_inputs():
+    dem = sk.make_synthetic(sk.SyntheticKind.Flat, 8, 8, 10.0)
+    holed = sk.Dem(dem.values.copy(), 10.0, nodata=-9999.0)
+    holed.values[3, 3] = -9999.0
+    with pytest.raises(ValueError, match="nodata"):
+        sk.total_viewshed(holed, sk.RunConfig())
+    with pytest.raises(ValueError):
+        sk.total_viewshed(dem, sk.RunConfig(ns=7))
+    with pytest.raises(IndexError):
+        sk.sector_sweep(dem, sk.RunConfig(), 180)
+    bad = dem.values.copy()
+    bad[1, 1] = np.nan
+    with pytest.raises(ValueError, match="non-finite"):
+        sk.total_viewshed(sk.Dem(bad, 10.0), sk.RunConfig())
