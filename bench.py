@@ -1,0 +1,401 @@
+#!/usr/bin/env python
+"""Benchmark: sDEM total viewshed, POV-sector evaluations per second.
+
+Workload (BASELINE.json configs[1], "config 2"): synthetic 2000x2000 fractal
+DEM at 10 m (seed 7), 180 sectors, observer height 1.5 m, unlimited radius.
+A step is one full total viewshed: relocation + scan + fixup + unskew of all
+90 sector axes (sharded over ranks, LPT on exact work) + the reduce of the
+maps to rank 0 + area scaling, with the DEM resident in HBM.
+
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+                  [--config 1..5] [--terrain fractal|smooth]
+
+One JSON line on rank 0. See DESIGN.md "Measurement" for every field.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+CONFIGS = {
+    1: dict(n=500, ns=180, max_distance=None),
+    2: dict(n=2000, ns=180, max_distance=None),
+    3: dict(n=2000, ns=360, max_distance=10000.0),
+    4: dict(n=4000, ns=180, max_distance=None),
+    5: dict(n=10000, ns=180, max_distance=None),
+}
+METRIC = "POV-sector evals/sec & total-viewshed time (2000² DEM, 180 sectors) @1/2/4/8 GPU"
+UNIT = "POV-sector/s"
+CELLSIZE = 10.0
+H0 = 1.5
+SEED = 7
+
+
+def workload_name(cfgid, terrain):
+    c = CONFIGS[cfgid]
+    cap = "unlimited radius" if c["max_distance"] is None else f"max radius {c['max_distance'] / 1000:g} km"
+    return (f"config {cfgid}: synthetic {c['n']}x{c['n']} {terrain} DEM at 10 m (seed {SEED}), "
+            f"{c['ns']} sectors, observer height 1.5 m, {cap}")
+
+
+def load_peaks():
+    path = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    if os.path.exists(path):
+        with open(path) as f:
+            p = json.load(f)
+        return p, "measured"
+    return {"hbm_gbs": 6650.0, "sm_max_mhz": 1965.0}, "fallback"
+
+
+class ClockSampler:
+    """nvidia-smi clocks + throttle reasons sampled during the timed region."""
+
+    def __init__(self, index: int):
+        self.index = index
+        self.samples = []
+        self._stop = threading.Event()
+        self._proc = None
+
+    def start(self):
+        q = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+             "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+             "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+        try:
+            self._proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.index), f"--query-gpu={q}", "--format=csv,noheader,nounits",
+                 "-lms", "100"], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+        except Exception:
+            self._proc = None
+            return
+        self._t = threading.Thread(target=self._read, daemon=True)
+        self._t.start()
+
+    def _read(self):
+        for line in self._proc.stdout:
+            parts = [x.strip() for x in line.split(",")]
+            if len(parts) >= 8:
+                self.samples.append(parts)
+
+    def stop(self):
+        if self._proc is not None:
+            self._proc.terminate()
+            try:
+                self._proc.wait(timeout=2)
+            except Exception:
+                self._proc.kill()
+
+    def summary(self):
+        if not self.samples:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unavailable"], "samples": 0}
+        sm = [float(s[0]) for s in self.samples if s[0].replace(".", "").isdigit()]
+        mx = [float(s[1]) for s in self.samples if s[1].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = set()
+        for s in self.samples:
+            for name, v in zip(names, s[4:8]):
+                if v.lower() == "active":
+                    reasons.add(name)
+        loaded = sorted(sm)[len(sm) // 4:] if sm else []
+        med = float(np.median(loaded)) if loaded else None
+        return {"sm_mhz": med, "sm_max_mhz": max(mx) if mx else None, "reasons": sorted(reasons),
+                "samples": len(self.samples)}
+
+
+def dist_setup(n_gpus):
+    import torch
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    if world > 1:
+        import torch.distributed as dist
+        torch.cuda.set_device(local)
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    elif torch.cuda.is_available():
+        torch.cuda.set_device(0)
+    return world, rank, local
+
+
+def barrier(world):
+    if world > 1:
+        import torch.distributed as dist
+        dist.barrier()
+
+
+def max_over_ranks(x, world):
+    if world == 1:
+        return x
+    import torch
+    import torch.distributed as dist
+    t = torch.tensor([x], dtype=torch.float64, device="cuda")
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    return float(t.item())
+
+
+def sum_over_ranks(x, world):
+    if world == 1:
+        return x
+    import torch
+    import torch.distributed as dist
+    t = torch.tensor([x], dtype=torch.float64, device="cuda")
+    dist.all_reduce(t, op=dist.ReduceOp.SUM)
+    return float(t.item())
+
+
+def make_dem(cfgid, terrain):
+    import paper_2003_02200_b200 as sk
+    n = CONFIGS[cfgid]["n"]
+    kind = sk.SyntheticKind.Fractal if terrain == "fractal" else sk.SyntheticKind.SmoothedNoise
+    return sk.make_synthetic(kind, n, n, CELLSIZE, SEED).values
+
+
+# ---- CPU baseline: the reference itself (oracle/_ref) ------------------------------
+
+def cpu_reference_sample(dem, ns, max_distance, budget_s, threads):
+    """Times the reference's own per-sector pipeline (plan_sector ->
+    apply_pre_ops -> build_skw -> linear_viewshed_row both directions for every
+    POV of the sampled rows) on `threads` host threads; returns the projected
+    POV-sector/s of the full workload (exact work model)."""
+    sys.path.insert(0, os.path.join(ROOT, "tests"))
+    from _oracle import Ref, have_ref
+
+    import paper_2003_02200_b200 as sk
+    if not have_ref():
+        raise RuntimeError("oracle/_ref/libskewshed_ref.so missing (build() it where /root/reference exists)")
+    ref = Ref()
+    n = dem.shape[0]
+    total = sk.total_target_evals(ns, n, n, CELLSIZE, max_distance)
+    half = ns // 2
+    sectors = sorted(set(int(round(x)) for x in np.linspace(0, half - 1, min(9, half))))
+    # calibrate the row stride to the time budget
+    stride, offset = 97, 13
+    evals, secs = ref.sample_scan(dem, ns, H0, max_distance, CELLSIZE, sectors, stride, offset, threads)
+    rate = evals / max(secs, 1e-9)
+    want = rate * budget_s
+    per_stride = evals * stride
+    stride = max(1, int(per_stride / max(want, 1.0)))
+    evals, secs = ref.sample_scan(dem, ns, H0, max_distance, CELLSIZE, sectors, stride, 7, threads)
+    rate = evals / max(secs, 1e-9)
+    wall = total / rate
+    value = n * n * half / wall
+    sample = (f"reference scan of every POV (both directions) on every {stride}th skewed row of sectors "
+              f"{sectors} ({evals:.3g} target evals in {secs:.1f} s on {threads} threads); projected to the "
+              f"full workload's {total:.4g} target evals (scan = 99.3% of reference time, SURVEY §6)")
+    return value, wall, rate, sample
+
+
+def run_reference(args, world, rank):
+    if rank != 0:
+        return
+    cfgid = args.config
+    c = CONFIGS[cfgid]
+    dem = make_dem(cfgid, args.terrain)
+    threads = os.cpu_count() or 1
+    budget = max(2.0, min(20.0, 150.0 / (args.steps + args.warmup)))
+    vals = []
+    walls = []
+    sample = ""
+    for i in range(args.warmup + args.steps):
+        v, wall, _rate, sample = cpu_reference_sample(dem, c["ns"], c["max_distance"], budget, threads)
+        if i >= args.warmup:
+            vals.append(v)
+            walls.append(wall)
+    value = float(np.median(vals))
+    line = {
+        "impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": args.gpus,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": float(np.median(walls)) * 1e3,
+        "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
+        "data": "synthetic", "config": {"workload": workload_name(cfgid, args.terrain), "dimy": c["n"],
+                                        "dimx": c["n"], "ns": c["ns"], "h0": H0,
+                                        "max_distance": c["max_distance"], "terrain": args.terrain},
+        "cpu_baseline": {"value": value, "unit": UNIT, "cores": threads, "kind": "reference",
+                         "sample": sample},
+        "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+
+
+# ---- our arm -------------------------------------------------------------------------
+
+def run_ours(args, world, rank, local):
+    import torch
+
+    import paper_2003_02200_b200 as sk
+    from paper_2003_02200_b200.distributed import my_sectors, total_viewshed_distributed
+
+    cfgid = args.config
+    c = CONFIGS[cfgid]
+    n, ns, maxd = c["n"], c["ns"], c["max_distance"]
+    cfg = sk.RunConfig(ns=ns, h0=H0, max_distance=maxd, units=sk.Units.SquareKilometers, device=local)
+    dem = make_dem(cfgid, args.terrain)
+    dev = torch.device("cuda", local)
+    stream = torch.cuda.current_stream(dev)
+    ctx = sk.Context(local)
+    mine = my_sectors(ns, n, n, world, rank, CELLSIZE, maxd)
+    d_dem = torch.from_numpy(dem).to(dev)
+    d_map = torch.zeros((n, n), dtype=torch.float64, device=dev)
+    flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev)
+    factor = sk.area_scale_factor(cfg, CELLSIZE)
+
+    def step(want_stats):
+        d_map.zero_()
+        st = ctx.run_sectors(d_dem.data_ptr(), n, n, CELLSIZE, cfg, mine, d_map.data_ptr(),
+                             stream=stream.cuda_stream, want_stats=want_stats)
+        if world > 1:
+            import torch.distributed as dist
+            dist.reduce(d_map, dst=0, op=dist.ReduceOp.SUM)
+        if rank == 0:
+            ctx.scale(d_map.data_ptr(), n * n, ns, CELLSIZE, int(cfg.units), stream.cuda_stream)
+        return st
+
+    for _ in range(args.warmup):
+        step(False)
+    torch.cuda.synchronize()
+
+    sampler = ClockSampler(local)
+    sampler.start()
+    total_ms = 0.0
+    phases = dict(skew=0.0, scan=0.0, fixup=0.0, unskew=0.0)
+    launches = 0
+    flagged = 0
+    evals = 0
+    for _ in range(args.steps):
+        flush.fill_(1)  # evict L2 (126 MB) between steps, outside the timed region
+        torch.cuda.synchronize()
+        barrier(world)
+        e0 = torch.cuda.Event(enable_timing=True)
+        e1 = torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        st = step(True)
+        e1.record(stream)
+        torch.cuda.synchronize()
+        barrier(world)
+        total_ms += e0.elapsed_time(e1)
+        phases["skew"] += st.skew_seconds
+        phases["scan"] += st.scan_seconds
+        phases["fixup"] += st.fixup_seconds
+        phases["unskew"] += st.unskew_seconds
+        launches += st.kernel_launches + (1 if rank == 0 else 0)
+        flagged += st.flagged_groups
+        evals += st.target_evals
+    sampler.stop()
+    total_ms = max_over_ranks(total_ms, world)
+    scan_s = max_over_ranks(phases["scan"], world)
+    skew_s = max_over_ranks(phases["skew"], world)
+    evals_all = sum_over_ranks(evals, world)
+    launches_all = int(sum_over_ranks(launches, world))
+    flagged_all = int(sum_over_ranks(flagged, world))
+    ms_per_step = total_ms / args.steps
+    povs = n * n * (ns // 2)
+    value = povs / (ms_per_step * 1e-3)
+
+    # e2e through the public API with host buffers (H2D of the DEM and D2H of
+    # the map inside every timed step)
+    pinned_dem = torch.from_numpy(dem).pin_memory()
+    pinned_out = torch.empty((n, n), dtype=torch.float64).pin_memory()
+    e2e_times = []
+    for i in range(args.warmup + args.steps):
+        barrier(world)
+        t0 = time.perf_counter()
+        if world == 1:
+            ctx.total_viewshed(pinned_dem.numpy(), CELLSIZE, cfg, out=pinned_out.numpy())
+        else:
+            total_viewshed_distributed(pinned_dem.numpy(), CELLSIZE, cfg, context=ctx)
+            torch.cuda.synchronize()
+        t1 = time.perf_counter()
+        if i >= args.warmup:
+            e2e_times.append(t1 - t0)
+    e2e_s = max_over_ranks(float(np.mean(e2e_times)), world)
+    e2e_value = povs / e2e_s
+
+    if rank != 0:
+        return
+    peaks, peak_kind = load_peaks()
+    clocks = sampler.summary()
+    props = torch.cuda.get_device_properties(dev)
+    sm_max = float(peaks.get("sm_max_mhz") or clocks.get("sm_max_mhz") or 1965.0)
+    fp32_peak = props.multi_processor_count * 128 * sm_max * 1e6  # lane-ops/s
+    scan_achieved = 4.0 * evals_all / max(scan_s, 1e-12) if world == 1 else 4.0 * evals_all / max(scan_s * world, 1e-12)
+    traffic = None
+    prof = os.path.join(ROOT, "profiles", "ncu_summary.json")
+    if os.path.exists(prof):
+        try:
+            with open(prof) as f:
+                traffic = json.load(f).get("scan_kernel", {}).get("dram_bytes_per_launch")
+        except Exception:
+            traffic = None
+    reloc_bytes = 8.0 * n * n * (ns // 2) * args.steps / world
+    line = {
+        "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": ms_per_step, "higher_is_better": True, "scaling": "strong",
+        "vs_baseline": None, "dtype": "f32 filter + f64 exact fixup/accumulate", "data": "synthetic",
+        "config": {"workload": workload_name(cfgid, args.terrain), "dimy": n, "dimx": n, "ns": ns, "h0": H0,
+                   "max_distance": maxd, "terrain": args.terrain, "cellsize": CELLSIZE,
+                   "l2": "flushed between timed steps (256 MiB device write, untimed)",
+                   "parallelism": f"sector-sharded x{world} (LPT), NCCL reduce of f64 maps"},
+        "roofline": {"kernel": "scan_kernel (FP32-issue bound)", "bound": "fp32",
+                     "achieved": scan_achieved / 1e12, "peak": fp32_peak / 1e12, "unit": "TFLOP/s",
+                     "frac": scan_achieved / fp32_peak, "traffic": traffic,
+                     "note": (f"4 algorithmic FP32 ops per target evaluation (SURVEY 8d) x "
+                              f"{evals_all / args.steps:.4g} evals/step / scan-kernel CUDA-event time; peak = "
+                              f"{props.multi_processor_count} SMs x 128 lanes x {sm_max:g} MHz (sm_max)")},
+        "roofline_relocation": {"kernel": "relocate_kernel", "bound": "hbm",
+                                "achieved": reloc_bytes / max(skew_s, 1e-12) / 1e9,
+                                "peak": float(peaks.get("hbm_gbs", 6650.0)), "unit": "GB/s",
+                                "frac": reloc_bytes / max(skew_s, 1e-12) / 1e9 / float(peaks.get("hbm_gbs", 6650.0)),
+                                "peak_kind": peak_kind, "traffic": None},
+        "phase_ms_per_step": {k: v * 1e3 / args.steps for k, v in phases.items()},
+        "target_evals_per_s": evals_all / args.steps / (ms_per_step * 1e-3),
+        "flagged_groups_per_step": flagged_all / args.steps,
+        "e2e": {"value": e2e_value, "unit": UNIT, "seconds": e2e_s,
+                "h2d_bytes_per_step": int(n * n * 4 * world), "d2h_bytes_per_step": int(n * n * 8)},
+        "gpu_launches": launches_all,
+        "clocks": clocks,
+    }
+    if world == 1 and not args.no_cpu_baseline:
+        try:
+            threads = os.cpu_count() or 1
+            v, wall, rate, sample = cpu_reference_sample(dem, ns, maxd, args.cpu_budget, threads)
+            line["cpu_baseline"] = {"value": v, "unit": UNIT, "cores": threads, "kind": "reference",
+                                    "sample": sample, "projected_wall_s": wall}
+        except Exception as e:  # reported, never fatal
+            line["cpu_baseline"] = {"value": None, "unit": UNIT, "cores": None, "kind": "reference",
+                                    "sample": f"unavailable: {e}"}
+    print(json.dumps(line), flush=True)
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
+    ap.add_argument("--config", type=int, default=2, choices=sorted(CONFIGS))
+    ap.add_argument("--terrain", choices=["fractal", "smooth"], default="fractal")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--cpu-budget", type=float, default=15.0)
+    args = ap.parse_args()
+    args.warmup = max(args.warmup, 3) if args.impl == "ours" else args.warmup
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    if args.impl == "reference":
+        run_reference(args, world, rank)
+        return
+    world, rank, local = dist_setup(args.gpus)
+    run_ours(args, world, rank, local)
+    if world > 1:
+        import torch.distributed as dist
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

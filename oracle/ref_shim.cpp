@@ -281,7 +281,8 @@ int ref_rotational_total_viewshed(const float* dem, int dimy, int dimx,
 // sampled with a stride so the sample is stratified over row lengths; the
 // caller extrapolates with the exact work count of the full workload.
 int ref_sample_scan(const float* dem, int dimy, int dimx, int ns, double h0,
-                    int max_dd, const int* sectors, int n_sectors,
+                    double max_distance, double cellsize, const int* sectors,
+                    int n_sectors,
                     int row_stride, int row_offset, int threads,
                     double* target_evals_out, double* seconds_out) {
   return guarded([&] {
@@ -293,9 +294,17 @@ int ref_sample_scan(const float* dem, int dimy, int dimx, int ns, double h0,
     // Relocation is done up front (outside the timed region) because the
     // scan is >99% of the reference's worker time.
     std::vector<SkwGrid> skws(n_sectors);
+    std::vector<int> caps(n_sectors, kNoDistanceCap);
     std::vector<Item> items;
     for (int s = 0; s < n_sectors; ++s) {
       SectorPlan p = plan_sector(sectors[s], ns, dimy, dimx);
+      if (max_distance > 0.0) {  // engine.cpp:29-36 distance_cap_cells
+        double step = cellsize * std::sqrt(1.0 + p.shear_tan * p.shear_tan);
+        double cap = std::floor(max_distance / step);
+        caps[s] = cap >= static_cast<double>(kNoDistanceCap)
+                      ? kNoDistanceCap
+                      : std::max(0, static_cast<int>(cap));
+      }
       Grid<float> pre = apply_pre_ops(d.values, p.pre_ops);
       skws[s] = build_skw(pre, p.shear_tan);
       for (int q = row_offset; q < skws[s].skw_rows(); q += row_stride) {
@@ -313,6 +322,7 @@ int ref_sample_scan(const float* dem, int dimy, int dimx, int ns, double h0,
         size_t it = next.fetch_add(1);
         if (it >= items.size()) break;
         const SkwGrid& skw = skws[items[it].s];
+        const int max_dd = caps[items[it].s];
         int q = items[it].q;
         auto [first, last] = skw.row_ranges[q];
         std::span<const float> row(skw.values.row(q), skw.cols);

@@ -96,8 +96,9 @@ class Ref:
         lib.ref_area_scale_factor.restype = C.c_double
         lib.ref_rotational_total_viewshed.argtypes = [_f32p, C.c_int, C.c_int, C.c_double, C.c_int, C.c_double,
                                                       C.c_double, _f64p]
-        lib.ref_sample_scan.argtypes = [_f32p, C.c_int, C.c_int, C.c_int, C.c_double, C.c_int, _i32p, C.c_int,
-                                        C.c_int, C.c_int, C.c_int, C.POINTER(C.c_double), C.POINTER(C.c_double)]
+        lib.ref_sample_scan.argtypes = [_f32p, C.c_int, C.c_int, C.c_int, C.c_double, C.c_double, C.c_double,
+                                        _i32p, C.c_int, C.c_int, C.c_int, C.c_int, C.POINTER(C.c_double),
+                                        C.POINTER(C.c_double)]
 
     def _check(self, rc):
         if rc != 0:
@@ -196,12 +197,13 @@ class Ref:
                                                            cellsize, ns, h0, max_distance or 0.0, out))
         return out
 
-    def sample_scan(self, dem, ns, h0, max_dd, sectors, row_stride, row_offset, threads):
+    def sample_scan(self, dem, ns, h0, max_distance, cellsize, sectors, row_stride, row_offset, threads):
         ev = C.c_double()
         sec = C.c_double()
         s = np.ascontiguousarray(sectors, np.int32)
-        self._check(self.lib.ref_sample_scan(np.ascontiguousarray(dem), dem.shape[0], dem.shape[1], ns, h0, max_dd,
-                                             s, len(s), row_stride, row_offset, threads, C.byref(ev), C.byref(sec)))
+        self._check(self.lib.ref_sample_scan(np.ascontiguousarray(dem), dem.shape[0], dem.shape[1], ns, h0,
+                                             max_distance or 0.0, cellsize, s, len(s), row_stride, row_offset,
+                                             threads, C.byref(ev), C.byref(sec)))
         return ev.value, sec.value
 
 
