@@ -122,38 +122,33 @@ __device__ __forceinline__ bool step1(float t, float X, float& hi, float& lo, fl
 }
 
 // Same decisions as 16 x step1 (4 dd steps x 4 POVs). Per target: two
-// FSETP (t > hi: record; t >= lo: not certainly hidden) and four predicated
-// FMA-pipe ops (band update, ring add, and `cvg`, the ring add over every
-// target with t >= lo). cvg == sum(cv) over a flush window iff no target fell
-// inside the uncertainty band (every band target adds 2dd+1 >= 3 to cvg
-// only); both sums are exact integers below 2^24 between flushes.
+// FSETP on the ALU pipe (t > hi: record; t >= lo: not certainly hidden) and
+// four predicated FP32-pipe ops (band update hi and lo, ring add, and `cvg`,
+// the ring add over every target with t >= lo). Over a flush window cvg ==
+// sum(cv) iff no target fell inside the uncertainty band (every band target
+// adds 2dd+1 >= 3 to cvg only); both sums are exact integers below 2^24.
+// (Measured on B200: FADD/FFMA issue 1/clk/SMSP, FADD2/FMUL2 hold the FP32
+// pipe 2 clk. Keeping the flag in a predicate instead (FSETP+FSETP+PLOP3)
+// makes ptxas spill the record predicates to GPR bits.)
 __device__ __forceinline__ void block16(const float (&t)[4][4], const float4 X, float (&hi)[4],
                                         float (&lo)[4], float (&cv)[4], float& cvg) {
-  asm volatile(
-      "{\n\t.reg .pred pg, pa;\n\t.reg .f32 at;\n\t"
-#define ONE(TI, HI, LO, CV, X)                               \
-  "setp.ge.f32 pg, %" #TI ", %" #LO ";\n\t"                  \
-  "setp.gt.f32 pa, %" #TI ", %" #HI ";\n\t"                  \
-  "abs.f32 at, %" #TI ";\n\t"                                \
-  "@pa fma.rn.f32 %" #HI ", at, 0f35200000, %" #TI ";\n\t"   \
-  "@pa fma.rn.f32 %" #LO ", at, 0fB5200000, %" #TI ";\n\t"   \
-  "@pa add.rn.f32 %" #CV ", %" #CV ", %" #X ";\n\t"          \
-  "@pg add.rn.f32 %12, %12, %" #X ";\n\t"
-      // operands: 0-3 hi, 4-7 lo, 8-11 cv, 12 cvg, 13-28 t[i][p] (13 + 4i + p),
-      // 29-32 X
-      ONE(13, 0, 4, 8, 29) ONE(14, 1, 5, 9, 29) ONE(15, 2, 6, 10, 29) ONE(16, 3, 7, 11, 29)
-      ONE(17, 0, 4, 8, 30) ONE(18, 1, 5, 9, 30) ONE(19, 2, 6, 10, 30) ONE(20, 3, 7, 11, 30)
-      ONE(21, 0, 4, 8, 31) ONE(22, 1, 5, 9, 31) ONE(23, 2, 6, 10, 31) ONE(24, 3, 7, 11, 31)
-      ONE(25, 0, 4, 8, 32) ONE(26, 1, 5, 9, 32) ONE(27, 2, 6, 10, 32) ONE(28, 3, 7, 11, 32)
-#undef ONE
-      "}"
-      : "+f"(hi[0]), "+f"(hi[1]), "+f"(hi[2]), "+f"(hi[3]), "+f"(lo[0]), "+f"(lo[1]),
-        "+f"(lo[2]), "+f"(lo[3]), "+f"(cv[0]), "+f"(cv[1]), "+f"(cv[2]), "+f"(cv[3]),
-        "+f"(cvg)
-      : "f"(t[0][0]), "f"(t[0][1]), "f"(t[0][2]), "f"(t[0][3]), "f"(t[1][0]), "f"(t[1][1]),
-        "f"(t[1][2]), "f"(t[1][3]), "f"(t[2][0]), "f"(t[2][1]), "f"(t[2][2]), "f"(t[2][3]),
-        "f"(t[3][0]), "f"(t[3][1]), "f"(t[3][2]), "f"(t[3][3]), "f"(X.x), "f"(X.y), "f"(X.z),
-        "f"(X.w));
+  const float xs[4] = {X.x, X.y, X.z, X.w};
+#pragma unroll
+  for (int i = 0; i < 4; ++i) {
+#pragma unroll
+    for (int p = 0; p < 4; ++p) {
+      const float tt = t[i][p];
+      const bool pg = tt >= lo[p];
+      const bool pa = tt > hi[p];
+      const float at = fabsf(tt);
+      if (pa) {
+        hi[p] = __fmaf_rn(at, kBand, tt);
+        lo[p] = __fmaf_rn(at, -kBand, tt);
+        cv[p] = __fadd_rn(cv[p], xs[i]);
+      }
+      if (pg) cvg = __fadd_rn(cvg, xs[i]);
+    }
+  }
 }
 
 __device__ __forceinline__ float2 f2(float a, float b) { return make_float2(a, b); }
@@ -183,7 +178,6 @@ __device__ __forceinline__ void scan_task(const float* __restrict__ B,
                                           float (&hi)[4], float (&lo)[4], int (&cvi)[4],
                                           unsigned& flag, int vis_p, uint8_t* vis) {
   float cv[4] = {0.f, 0.f, 0.f, 0.f};
-  float cvg = 0.f;
   const float2 nhf01 = f2(-hf[0], -hf[1]), nhf23 = f2(-hf[2], -hf[3]);
   const float2 nhl01 = f2(-hl[0], -hl[1]), nhl23 = f2(-hl[2], -hl[3]);
   const float* INV = reinterpret_cast<const float*>(INV4);
@@ -237,37 +231,69 @@ __device__ __forceinline__ void scan_task(const float* __restrict__ B,
       qa = qb;
       qa1 = qb1;
 #pragma unroll
-      for (int p = 0; p < 4; ++p) {  // windows of the band check start clean
+      for (int p = 0; p < 4; ++p) {  // band-check windows start clean
         cvi[p] += __float2int_rn(cv[p]);
         cv[p] = 0.f;
       }
     }
     const int blast = (Dw - 3) >> 2;  // last full block (4b+3 <= Dw)
-    int b = 1;
-    while (b <= blast) {
-      const int bend = min(blast, b + 31);  // cvg, cv < 2^24 between flushes
-#pragma unroll 2
-      for (; b <= bend; ++b) {
-        const float4 qb = Q[b + 1];
-        const float4 qb1 = Q1[b + 1];
-        const float4 iv = INV4[b];
-        const float4 xx = X4[b];
-        float t[4][4];
-        tpair(f2(qa.x, qa.y), f2(qa.z, qa.w), nhf01, nhf23, nhl01, nhl23, iv.x, t[0]);
-        tpair(f2(qa1.x, qa1.y), f2(qa1.z, qa1.w), nhf01, nhf23, nhl01, nhl23, iv.y, t[1]);
-        tpair(f2(qa.z, qa.w), f2(qb.x, qb.y), nhf01, nhf23, nhl01, nhl23, iv.z, t[2]);
-        tpair(f2(qa1.z, qa1.w), f2(qb1.x, qb1.y), nhf01, nhf23, nhl01, nhl23, iv.w, t[3]);
-        block16(t, xx, hi, lo, cv, cvg);
-        qa = qb;
-        qa1 = qb1;
-      }
-      // band check for the window, then flush the exact float sums
-      if (cvg != __fadd_rn(__fadd_rn(cv[0], cv[1]), __fadd_rn(cv[2], cv[3]))) flag = 1u;
-      cvg = 0.f;
+    if (blast >= 1) {
+      const float4* qp = Q + 2;
+      const float4* qp1 = Q1 + 2;
+      const float4* ivp = INV4 + 1;
+      const float4* xp = X4 + 1;
+      int b = 1;
+      float cvg = 0.f;
+      while (b <= blast) {
+        const int bend = min(blast, b + 31);  // cvg, cv < 2^24 between flushes
+        // two blocks per iteration so the sliding window rotates through
+        // register names instead of moves
+        for (; b + 1 <= bend; b += 2) {
+          const float4 qb = qp[0], qb1 = qp1[0];
+          const float4 qc = qp[1], qc1 = qp1[1];
+          const float4 iv0 = ivp[0], xx0 = xp[0];
+          const float4 iv1 = ivp[1], xx1 = xp[1];
+          qp += 2;
+          qp1 += 2;
+          ivp += 2;
+          xp += 2;
+          float t[4][4];
+          tpair(f2(qa.x, qa.y), f2(qa.z, qa.w), nhf01, nhf23, nhl01, nhl23, iv0.x, t[0]);
+          tpair(f2(qa1.x, qa1.y), f2(qa1.z, qa1.w), nhf01, nhf23, nhl01, nhl23, iv0.y, t[1]);
+          tpair(f2(qa.z, qa.w), f2(qb.x, qb.y), nhf01, nhf23, nhl01, nhl23, iv0.z, t[2]);
+          tpair(f2(qa1.z, qa1.w), f2(qb1.x, qb1.y), nhf01, nhf23, nhl01, nhl23, iv0.w, t[3]);
+          block16(t, xx0, hi, lo, cv, cvg);
+          tpair(f2(qb.x, qb.y), f2(qb.z, qb.w), nhf01, nhf23, nhl01, nhl23, iv1.x, t[0]);
+          tpair(f2(qb1.x, qb1.y), f2(qb1.z, qb1.w), nhf01, nhf23, nhl01, nhl23, iv1.y, t[1]);
+          tpair(f2(qb.z, qb.w), f2(qc.x, qc.y), nhf01, nhf23, nhl01, nhl23, iv1.z, t[2]);
+          tpair(f2(qb1.z, qb1.w), f2(qc1.x, qc1.y), nhf01, nhf23, nhl01, nhl23, iv1.w, t[3]);
+          block16(t, xx1, hi, lo, cv, cvg);
+          qa = qc;
+          qa1 = qc1;
+        }
+        if (b <= bend) {  // odd block count in this window
+          const float4 qb = *qp++;
+          const float4 qb1 = *qp1++;
+          const float4 iv = *ivp++;
+          const float4 xx = *xp++;
+          float t[4][4];
+          tpair(f2(qa.x, qa.y), f2(qa.z, qa.w), nhf01, nhf23, nhl01, nhl23, iv.x, t[0]);
+          tpair(f2(qa1.x, qa1.y), f2(qa1.z, qa1.w), nhf01, nhf23, nhl01, nhl23, iv.y, t[1]);
+          tpair(f2(qa.z, qa.w), f2(qb.x, qb.y), nhf01, nhf23, nhl01, nhl23, iv.z, t[2]);
+          tpair(f2(qa1.z, qa1.w), f2(qb1.x, qb1.y), nhf01, nhf23, nhl01, nhl23, iv.w, t[3]);
+          block16(t, xx, hi, lo, cv, cvg);
+          qa = qb;
+          qa1 = qb1;
+          ++b;
+        }
+        // band check of the window, then flush the exact float sums
+        if (cvg != __fadd_rn(__fadd_rn(cv[0], cv[1]), __fadd_rn(cv[2], cv[3]))) flag = 1u;
+        cvg = 0.f;
 #pragma unroll
-      for (int p = 0; p < 4; ++p) {
-        cvi[p] += __float2int_rn(cv[p]);
-        cv[p] = 0.f;
+        for (int p = 0; p < 4; ++p) {
+          cvi[p] += __float2int_rn(cv[p]);
+          cv[p] = 0.f;
+        }
       }
     }
     const int bt = max(1, blast + 1);
@@ -436,66 +462,87 @@ __global__ void __launch_bounds__(512, 2) scan_kernel(ScanArgs a) {
   }
 }
 
-// Exact FP64 re-scan of flagged POV groups: one warp per queue entry. Each
-// POV's targets are split across lanes 32 at a time; theta is computed with
-// the reference's IEEE operations ((double)row[k] - h) / dd, the running
-// maximum before each target is an exclusive warp prefix max (max is exact,
-// so association order is irrelevant), and visible targets add 2dd+1.
+// Exact resolution of flagged POV groups. One thread per (queue entry, POV):
+// the thread re-runs the same FP32 certified filter as the scan kernel (same
+// operations, so the same certified decisions) and resolves every target
+// that falls inside the uncertainty band exactly: theta_k and the running
+// maximum theta_r (r = index of the last record, tracked here) are computed
+// with the reference's IEEE FP64 operations ((double)row[k] - h) / dd
+// (scan.cpp:24-25) and compared strictly. POVs whose h does not split
+// exactly into two floats run the FP64 recurrence on every target. Either
+// way every decision equals the reference's.
 __global__ void __launch_bounds__(256) fixup_kernel(ScanArgs a) {
   const unsigned n = min(*a.fix_count, a.fix_cap);
-  const int lane = threadIdx.x & 31;
-  const unsigned gw = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
-  const unsigned nw = (gridDim.x * blockDim.x) >> 5;
-  for (unsigned e = gw; e < n; e += nw) {
-    const unsigned long long v = a.fix_queue[e];
+  const unsigned long long total = 4ull * n;
+  const unsigned long long stride = static_cast<unsigned long long>(gridDim.x) * blockDim.x;
+  for (unsigned long long w = static_cast<unsigned long long>(blockIdx.x) * blockDim.x + threadIdx.x;
+       w < total; w += stride) {
+    const unsigned long long v = a.fix_queue[w >> 2];
+    const int p = static_cast<int>(w & 3);
     const int s = static_cast<int>(v >> 45);
     const int q = static_cast<int>((v >> 23) & 0x3fffffu);
     const int dir = static_cast<int>((v >> 22) & 1u);
     const int g = static_cast<int>(v & 0x3fffffu);
-    const SectorDev sd = a.b.sectors[s];
+    const SectorDev& sd = a.b.sectors[s];
     const int2 rg = a.b.ranges[sd.row_off + q];
     const int first = rg.x;
     const int L = rg.y - rg.x;
+    const int y = 4 * g + p;
+    if (y >= L) continue;
     const float* rowp = a.b.sdem + sd.sdem_off + static_cast<long long>(q) * sd.pitch;
     int* dst = ((dir && a.b.cv_bwd) ? a.b.cv_bwd : a.b.cv) + sd.sdem_off +
                static_cast<long long>(q) * sd.pitch;
-    for (int p = 0; p < 4; ++p) {
-      const int y = 4 * g + p;
-      if (y >= L) break;
-      const int x = dir ? (L - 1 - y) : y;
-      const int j0 = first + x;
-      const bool dbg = a.dbg_j0 >= 0 && s == 0 && q == 0 && j0 == a.dbg_j0;
-      const double h = dbg ? a.dbg_h : __dadd_rn(static_cast<double>(rowp[j0]), a.h0);
-      const int D = min(sd.max_dd, dir ? x : (L - 1 - x));
-      uint8_t* vis = dbg ? (dir ? a.dbg_vis_bwd : a.dbg_vis_fwd) : nullptr;
-      long long cv = 0;
-      double carry = -INFINITY;
-      for (int base = 0; base < D; base += 32) {
-        const int dd = base + lane + 1;
-        const bool valid = dd <= D;
-        double th = -INFINITY;
-        if (valid) {
-          const int k = dir ? (j0 - dd) : (j0 + dd);
-          th = __ddiv_rn(__dsub_rn(static_cast<double>(rowp[k]), h), static_cast<double>(dd));
+    const int x = dir ? (L - 1 - y) : y;
+    const int j0 = first + x;
+    const int sg = dir ? -1 : 1;
+    const bool dbg = a.dbg_j0 >= 0 && s == 0 && q == 0 && j0 == a.dbg_j0;
+    const double h = dbg ? a.dbg_h : __dadd_rn(static_cast<double>(rowp[j0]), a.h0);
+    const int D = min(sd.max_dd, dir ? x : (L - 1 - x));
+    uint8_t* vis = dbg ? (dir ? a.dbg_vis_bwd : a.dbg_vis_fwd) : nullptr;
+    const float hf = __double2float_rn(h);
+    const double hld = __dsub_rn(h, static_cast<double>(hf));
+    const float hl = __double2float_rn(hld);
+    const bool exact_all = a.force_exact || static_cast<double>(hl) != hld || !(fabsf(hf) < 1e30f);
+    float hi = -INFINITY, lo = -FLT_MAX;
+    int r = 0;            // last record (0: none yet, max = -inf)
+    double M = -INFINITY; // exact max theta when Mvalid
+    bool Mvalid = true;
+    long long cv = 0;
+    for (int dd = 1; dd <= D; ++dd) {
+      const float e = rowp[j0 + sg * dd];
+      bool above;
+      if (!exact_all) {
+        const float inv = __frcp_rn(static_cast<float>(dd));
+        const float t = __fmul_rn(__fadd_rn(__fsub_rn(e, hf), -hl), inv);
+        if (t > hi) {
+          above = true;
+          Mvalid = false;
+        } else if (t >= lo) {
+          const double th = __ddiv_rn(__dsub_rn(static_cast<double>(e), h), static_cast<double>(dd));
+          if (!Mvalid) {
+            M = __ddiv_rn(__dsub_rn(static_cast<double>(rowp[j0 + sg * r]), h), static_cast<double>(r));
+            Mvalid = true;
+          }
+          above = th > M;
+          if (above) M = th;
+        } else {
+          above = false;
         }
-        double incl = th;
-#pragma unroll
-        for (int o = 1; o < 32; o <<= 1) {
-          const double u = __shfl_up_sync(0xffffffffu, incl, o);
-          if (lane >= o) incl = fmax(incl, u);
+        if (above) {
+          const float at = fabsf(t);
+          hi = __fmaf_rn(at, kBand, t);
+          lo = __fmaf_rn(at, -kBand, t);
+          r = dd;
         }
-        double excl = __shfl_up_sync(0xffffffffu, incl, 1);
-        if (lane == 0) excl = -INFINITY;
-        excl = fmax(excl, carry);
-        const bool above = valid && th > excl;
-        if (above) cv += 2LL * dd + 1;
-        if (vis && valid) vis[dd - 1] = above ? 1 : 0;
-        carry = fmax(carry, __shfl_sync(0xffffffffu, incl, 31));
+      } else {
+        const double th = __ddiv_rn(__dsub_rn(static_cast<double>(e), h), static_cast<double>(dd));
+        above = th > M;
+        if (above) M = th;
       }
-#pragma unroll
-      for (int o = 16; o > 0; o >>= 1) cv += __shfl_xor_sync(0xffffffffu, cv, o);
-      if (lane == 0 && cv != 0) atomicAdd(dst + j0, static_cast<int>(cv));
+      if (above) cv += 2LL * dd + 1;
+      if (vis) vis[dd - 1] = above ? 1 : 0;
     }
+    if (cv != 0) atomicAdd(dst + j0, static_cast<int>(cv));
   }
 }
 
