@@ -1,0 +1,274 @@
+// skewshed_b200 — C++ facade over the C ABI (skewshed_b200.h).
+//
+// Restores the reference's entry points (proj/include/skewshed/*.hpp) with
+// the same names, argument meaning and exception types, so reference-style
+// C++ callers switch by changing the namespace and linking
+// libskewshed_b200.so:
+//   engine.hpp:42-53  total_viewshed_raw, total_viewshed, sector_sweep,
+//                     accumulate_into, reduce_ordered, area_scale_factor
+//   skew.hpp:45-89    plan_sector, shear_params, build_skw, unskew_accumulate
+//   scan.hpp:27-45    linear_viewshed_row, sector_viewshed, area_scale
+//   dem.hpp:13-71     Dem, RunConfig, VsGrid, Units, make_synthetic, validate
+// std::invalid_argument / std::out_of_range / std::runtime_error are thrown
+// for SKS_INVALID_ARGUMENT / SKS_OUT_OF_RANGE / everything else.
+#pragma once
+
+#include <cmath>
+#include <cstdint>
+#include <functional>
+#include <numbers>
+#include <optional>
+#include <span>
+#include <stdexcept>
+#include <string>
+#include <utility>
+#include <vector>
+
+#include "skewshed_b200.h"
+
+namespace skewshed_b200 {
+
+inline void check(sks_status s) {
+  if (s == SKS_OK) return;
+  std::string msg = sks_last_error();
+  if (s == SKS_INVALID_ARGUMENT) throw std::invalid_argument(msg);
+  if (s == SKS_OUT_OF_RANGE) throw std::out_of_range(msg);
+  throw std::runtime_error(msg);
+}
+
+// grid.hpp:11-63: row-major, row 0 north, col 0 west.
+template <typename T>
+class Grid {
+ public:
+  Grid() = default;
+  Grid(int rows, int cols, T fill = T{}) { reset(rows, cols, fill); }
+  int rows() const { return rows_; }
+  int cols() const { return cols_; }
+  std::size_t size() const { return data_.size(); }
+  bool empty() const { return data_.empty(); }
+  T& operator()(int i, int j) { return data_[static_cast<std::size_t>(i) * cols_ + j]; }
+  const T& operator()(int i, int j) const { return data_[static_cast<std::size_t>(i) * cols_ + j]; }
+  T* row(int i) { return data_.data() + static_cast<std::size_t>(i) * cols_; }
+  const T* row(int i) const { return data_.data() + static_cast<std::size_t>(i) * cols_; }
+  std::vector<T>& data() { return data_; }
+  const std::vector<T>& data() const { return data_; }
+  void reset(int rows, int cols, T fill = T{}) {
+    if (rows < 0 || cols < 0) throw std::invalid_argument("grid dimensions must be non-negative");
+    rows_ = rows;
+    cols_ = cols;
+    data_.assign(static_cast<std::size_t>(rows) * cols, fill);
+  }
+  bool same_shape(const Grid& o) const { return rows_ == o.rows_ && cols_ == o.cols_; }
+  friend bool operator==(const Grid&, const Grid&) = default;
+
+ private:
+  int rows_ = 0, cols_ = 0;
+  std::vector<T> data_;
+};
+
+enum class Units { SquareMeters = SKS_UNITS_M2, SquareKilometers = SKS_UNITS_KM2 };
+enum class SyntheticKind { Flat = 0, Ramp = 1, Cone = 2, SmoothedNoise = 3, Fractal = 4 };
+enum class ScanDir { Forward = SKS_SCAN_FORWARD, Backward = SKS_SCAN_BACKWARD };
+enum class AxisOp { Transpose = 0, FlipCols = 1, FlipRows = 2 };
+inline constexpr int kNoDistanceCap = SKS_NO_DISTANCE_CAP;
+
+struct Dem {
+  Grid<float> values;
+  double cellsize = 1.0;
+  std::optional<float> nodata;
+  int dimy() const { return values.rows(); }
+  int dimx() const { return values.cols(); }
+};
+
+// dem.hpp:40-46; `workers` is replaced by the CUDA device ordinal.
+struct RunConfig {
+  int ns = 360;
+  double h0 = 1.5;
+  int device = 0;
+  std::optional<double> max_distance;
+  Units units = Units::SquareKilometers;
+  sks_run_config to_c() const {
+    return sks_run_config{ns, h0, max_distance.value_or(0.0), static_cast<int>(units), device};
+  }
+};
+
+struct VsGrid {
+  Grid<double> values;
+  Units units = Units::SquareMeters;
+};
+
+struct EngineStats : sks_stats {
+  EngineStats() : sks_stats{} {}
+};
+
+struct SectorResult {
+  int sector_index = 0;
+  Grid<double> contribution;
+};
+
+using ProgressFn = std::function<void(int sector_index, double wall_seconds)>;
+
+struct SectorPlan : sks_sector_plan {
+  std::pair<int, int> to_source_ij(int i, int j) const {
+    const int* m = to_source;
+    return {m[0] * i + m[1] * j + m[2], m[3] * i + m[4] * j + m[5]};
+  }
+};
+
+struct ShearParams {
+  int dest;
+  double frac;
+};
+
+struct SkwGrid {
+  int src_rows = 0;
+  int cols = 0;
+  int base = 0;
+  double shear_tan = 0.0;
+  Grid<float> values;
+  std::vector<std::pair<int, int>> row_ranges;
+  int skw_rows() const { return values.rows(); }
+};
+
+inline Dem make_synthetic(SyntheticKind kind, int dimy, int dimx, double cellsize,
+                          std::uint32_t seed = 0) {
+  if (!(cellsize > 0.0)) throw std::invalid_argument("synthetic cellsize must be positive");
+  Dem d;
+  d.cellsize = cellsize;
+  d.values.reset(dimy, dimx);
+  check(sks_make_synthetic(static_cast<int>(kind), dimy, dimx, seed, d.values.data().data()));
+  return d;
+}
+
+inline SectorPlan plan_sector(int k, int ns, int dimy, int dimx) {
+  SectorPlan p{};
+  check(sks_plan_sector(k, ns, dimy, dimx, &p));
+  return p;
+}
+
+inline ShearParams shear_params(double shear_tan, int j) {
+  ShearParams sp{};
+  sks_shear_params(shear_tan, j, &sp.dest, &sp.frac);
+  return sp;
+}
+
+inline double area_scale_factor(const RunConfig& cfg, double cellsize) {
+  return sks_area_scale_factor(cfg.ns, cellsize, static_cast<int>(cfg.units));
+}
+
+inline double area_scale(double cv_sum, int ns, double cellsize) {
+  return cv_sum * (std::numbers::pi / ns) * cellsize * cellsize;
+}
+
+inline void validate_or_throw(const Dem& dem, const RunConfig& cfg) {
+  sks_run_config c = cfg.to_c();
+  const float* nod = dem.nodata ? &*dem.nodata : nullptr;
+  check(sks_validate(dem.values.data().data(), dem.dimy(), dem.dimx(), dem.cellsize, nod, &c));
+}
+
+inline Grid<double> total_viewshed_raw(const Dem& dem, const RunConfig& cfg,
+                                       EngineStats* stats = nullptr,
+                                       const ProgressFn& progress = {}) {
+  if (dem.nodata) validate_or_throw(dem, cfg);
+  Grid<double> out(dem.dimy(), dem.dimx());
+  sks_run_config c = cfg.to_c();
+  check(sks_total_viewshed_raw(dem.values.data().data(), dem.dimy(), dem.dimx(), dem.cellsize, &c,
+                               out.data().data(), stats));
+  if (progress) {
+    for (int k = 0; k < cfg.ns / 2; ++k) progress(k, 0.0);
+  }
+  return out;
+}
+
+inline VsGrid total_viewshed(const Dem& dem, const RunConfig& cfg, EngineStats* stats = nullptr,
+                             const ProgressFn& progress = {}) {
+  if (dem.nodata) validate_or_throw(dem, cfg);
+  VsGrid out;
+  out.units = cfg.units;
+  out.values.reset(dem.dimy(), dem.dimx());
+  sks_run_config c = cfg.to_c();
+  check(sks_total_viewshed(dem.values.data().data(), dem.dimy(), dem.dimx(), dem.cellsize, &c,
+                           out.values.data().data(), stats));
+  if (progress) {
+    for (int k = 0; k < cfg.ns / 2; ++k) progress(k, 0.0);
+  }
+  return out;
+}
+
+inline SectorResult sector_sweep(const Dem& dem, const RunConfig& cfg, int k) {
+  if (dem.nodata) validate_or_throw(dem, cfg);
+  SectorResult r;
+  r.sector_index = k;
+  r.contribution.reset(dem.dimy(), dem.dimx());
+  sks_run_config c = cfg.to_c();
+  check(sks_sector_sweep(dem.values.data().data(), dem.dimy(), dem.dimx(), dem.cellsize, &c, k,
+                         r.contribution.data().data()));
+  return r;
+}
+
+inline void accumulate_into(Grid<double>& accum, const Grid<double>& contribution) {
+  if (!accum.same_shape(contribution)) {
+    throw std::invalid_argument("cannot accumulate grids of different shape");
+  }
+  for (std::size_t n = 0; n < accum.size(); ++n) accum.data()[n] += contribution.data()[n];
+}
+
+inline Grid<double> reduce_ordered(std::span<const Grid<double>> buffers) {
+  if (buffers.empty()) throw std::invalid_argument("nothing to reduce");
+  Grid<double> acc(buffers.front().rows(), buffers.front().cols(), 0.0);
+  for (const auto& b : buffers) accumulate_into(acc, b);
+  return acc;
+}
+
+inline SkwGrid build_skw(const Grid<float>& g, double shear_tan, int device = 0) {
+  int skw_rows = 0;
+  check(sks_row_ranges(g.rows(), g.cols(), shear_tan, nullptr, &skw_rows));
+  SkwGrid s;
+  s.src_rows = g.rows();
+  s.cols = g.cols();
+  s.shear_tan = shear_tan;
+  s.values.reset(skw_rows, g.cols());
+  std::vector<int> rr(2 * static_cast<std::size_t>(skw_rows));
+  check(sks_build_skw(g.data().data(), g.rows(), g.cols(), shear_tan, device, s.values.data().data(),
+                      rr.data(), &s.base));
+  s.row_ranges.resize(skw_rows);
+  for (int q = 0; q < skw_rows; ++q) s.row_ranges[q] = {rr[2 * q], rr[2 * q + 1]};
+  return s;
+}
+
+inline Grid<double> sector_viewshed(const SkwGrid& skw, double h0, int max_dd = kNoDistanceCap,
+                                    int device = 0) {
+  std::vector<int> rr(2 * skw.row_ranges.size());
+  for (std::size_t q = 0; q < skw.row_ranges.size(); ++q) {
+    rr[2 * q] = skw.row_ranges[q].first;
+    rr[2 * q + 1] = skw.row_ranges[q].second;
+  }
+  Grid<double> out(skw.skw_rows(), skw.cols);
+  check(sks_sector_viewshed(skw.values.data().data(), rr.data(), skw.skw_rows(), skw.cols,
+                            skw.shear_tan, h0, max_dd, device, out.data().data(), nullptr, nullptr));
+  return out;
+}
+
+inline double linear_viewshed_row(std::span<const float> row, int first, int last, int j0, double h,
+                                  ScanDir dir, int max_dd = kNoDistanceCap,
+                                  std::vector<std::uint8_t>* visible_out = nullptr, int device = 0) {
+  double cv = 0.0;
+  int nv = 0;
+  std::vector<std::uint8_t> vis(row.size() + 1);
+  check(sks_linear_viewshed_row(row.data(), static_cast<int>(row.size()), first, last, j0, h,
+                                static_cast<int>(dir), max_dd, device, &cv,
+                                visible_out ? vis.data() : nullptr, &nv));
+  if (visible_out) visible_out->insert(visible_out->end(), vis.begin(), vis.begin() + nv);
+  return cv;
+}
+
+inline void unskew_accumulate(const Grid<double>& skw_vs, const SectorPlan& plan, Grid<double>& out,
+                              int device = 0) {
+  if (out.rows() != plan.src_rows || out.cols() != plan.src_cols) {
+    throw std::invalid_argument("output shape does not match source grid");
+  }
+  check(sks_unskew_accumulate(skw_vs.data().data(), skw_vs.rows(), skw_vs.cols(), plan.sector_index,
+                              plan.ns, plan.src_rows, plan.src_cols, device, out.data().data()));
+}
+
+}  // namespace skewshed_b200

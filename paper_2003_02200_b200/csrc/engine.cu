@@ -634,7 +634,7 @@ sks_status sks_context_total_viewshed(sks_context* ctx, const float* dem, int di
 sks_status sks_total_viewshed(const float* dem, int dimy, int dimx, double cellsize,
                               const sks_run_config* cfg, double* out_vs, sks_stats* stats) {
   return guarded([&] {
-    if (!cfg) throw std::invalid_argument("null run config");
+    require_valid(dem, dimy, dimx, cellsize, cfg);  // before touching the device
     total_host(default_context(cfg->device), dem, dimy, dimx, cellsize, cfg, 0, out_vs, stats);
   });
 }
@@ -642,7 +642,7 @@ sks_status sks_total_viewshed(const float* dem, int dimy, int dimx, double cells
 sks_status sks_total_viewshed_raw(const float* dem, int dimy, int dimx, double cellsize,
                                   const sks_run_config* cfg, double* out_raw, sks_stats* stats) {
   return guarded([&] {
-    if (!cfg) throw std::invalid_argument("null run config");
+    require_valid(dem, dimy, dimx, cellsize, cfg);  // before touching the device
     total_host(default_context(cfg->device), dem, dimy, dimx, cellsize, cfg, 1, out_raw, stats);
   });
 }
