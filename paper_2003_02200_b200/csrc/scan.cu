@@ -59,7 +59,7 @@ struct SmemLayout {
   __host__ __device__ SmemLayout(int lmax, bool shifted) {
     lp = round4(lmax);
     lb = lp + kPad;
-    lt = round4(lmax + 16);
+    lt = round4(lmax + 32);
     staging = 8;  // first 32 bytes: mbarrier + control words
     s = staging + lp + 8;
     s1 = s + lb;
@@ -166,6 +166,14 @@ __device__ __forceinline__ void tpair(float2 e01, float2 e23, float2 nhf01, floa
   t[3] = b.y;
 }
 
+__device__ __forceinline__ float4 lds128(unsigned addr) {
+  float4 v;
+  asm("ld.shared.v4.f32 {%0, %1, %2, %3}, [%4];"
+      : "=f"(v.x), "=f"(v.y), "=f"(v.z), "=f"(v.w)
+      : "r"(addr));
+  return v;
+}
+
 // One 128-POV task: POVs y0..y0+3 per lane in buffer B (row copy, forward
 // direction in B's own coordinates), dd = 1..Dw. Returns per-POV cv and the
 // lane flag. kVis: debug path recording decisions of one POV.
@@ -205,87 +213,39 @@ __device__ __forceinline__ void scan_task(const float* __restrict__ B,
       }
     }
   } else {
-    const float4* Q = reinterpret_cast<const float4*>(B) + (y0 >> 2);
-    const float4* Q1 = reinterpret_cast<const float4*>(B1) + (y0 >> 2);
-    float4 qa = Q[0], qa1 = Q1[0];
-    // partial block: steps i in [i0, i1] of block b (window qa/qb)
-    auto partial = [&](int b, int i0, int i1, float4 qb, float4 qb1) {
-      const float4 iv = INV4[b];
-      const float4 xx = X4[b];
-      const float ivs[4] = {iv.x, iv.y, iv.z, iv.w};
-      const float xs[4] = {xx.x, xx.y, xx.z, xx.w};
-      const float w[8] = {qa.x, qa.y, qa.z, qa.w, qb.x, qb.y, qb.z, qb.w};
-#pragma unroll
-      for (int i = 0; i < 4; ++i) {
-        if (i < i0 || i > i1) continue;
-        float t[4];
-        tpair(f2(w[i], w[i + 1]), f2(w[i + 2], w[i + 3]), nhf01, nhf23, nhl01, nhl23, ivs[i],
-              t);
-#pragma unroll
-        for (int p = 0; p < 4; ++p) step1(t[p], xs[i], hi[p], lo[p], cv[p], flag);
-      }
-    };
-    {
-      const float4 qb = Q[1], qb1 = Q1[1];
-      partial(0, 1, min(3, Dw), qb, qb1);
-      qa = qb;
-      qa1 = qb1;
-#pragma unroll
-      for (int p = 0; p < 4; ++p) {  // band-check windows start clean
-        cvi[p] += __float2int_rn(cv[p]);
-        cv[p] = 0.f;
-      }
-    }
-    const int blast = (Dw - 3) >> 2;  // last full block (4b+3 <= Dw)
-    if (blast >= 1) {
-      const float4* qp = Q + 2;
-      const float4* qp1 = Q1 + 2;
-      const float4* ivp = INV4 + 1;
-      const float4* xp = X4 + 1;
-      int b = 1;
-      float cvg = 0.f;
-      while (b <= blast) {
-        const int bend = min(blast, b + 31);  // cvg, cv < 2^24 between flushes
-        // two blocks per iteration so the sliding window rotates through
-        // register names instead of moves
-        for (; b + 1 <= bend; b += 2) {
-          const float4 qb = qp[0], qb1 = qp1[0];
-          const float4 qc = qp[1], qc1 = qp1[1];
-          const float4 iv0 = ivp[0], xx0 = xp[0];
-          const float4 iv1 = ivp[1], xx1 = xp[1];
-          qp += 2;
-          qp1 += 2;
-          ivp += 2;
-          xp += 2;
-          float t[4][4];
-          tpair(f2(qa.x, qa.y), f2(qa.z, qa.w), nhf01, nhf23, nhl01, nhl23, iv0.x, t[0]);
-          tpair(f2(qa1.x, qa1.y), f2(qa1.z, qa1.w), nhf01, nhf23, nhl01, nhl23, iv0.y, t[1]);
-          tpair(f2(qa.z, qa.w), f2(qb.x, qb.y), nhf01, nhf23, nhl01, nhl23, iv0.z, t[2]);
-          tpair(f2(qa1.z, qa1.w), f2(qb1.x, qb1.y), nhf01, nhf23, nhl01, nhl23, iv0.w, t[3]);
-          block16(t, xx0, hi, lo, cv, cvg);
-          tpair(f2(qb.x, qb.y), f2(qb.z, qb.w), nhf01, nhf23, nhl01, nhl23, iv1.x, t[0]);
-          tpair(f2(qb1.x, qb1.y), f2(qb1.z, qb1.w), nhf01, nhf23, nhl01, nhl23, iv1.y, t[1]);
-          tpair(f2(qb.z, qb.w), f2(qc.x, qc.y), nhf01, nhf23, nhl01, nhl23, iv1.z, t[2]);
-          tpair(f2(qb1.z, qb1.w), f2(qc1.x, qc1.y), nhf01, nhf23, nhl01, nhl23, iv1.w, t[3]);
-          block16(t, xx1, hi, lo, cv, cvg);
-          qa = qc;
-          qa1 = qc1;
-        }
-        if (b <= bend) {  // odd block count in this window
-          const float4 qb = *qp++;
-          const float4 qb1 = *qp1++;
-          const float4 iv = *ivp++;
-          const float4 xx = *xp++;
-          float t[4][4];
-          tpair(f2(qa.x, qa.y), f2(qa.z, qa.w), nhf01, nhf23, nhl01, nhl23, iv.x, t[0]);
-          tpair(f2(qa1.x, qa1.y), f2(qa1.z, qa1.w), nhf01, nhf23, nhl01, nhl23, iv.y, t[1]);
-          tpair(f2(qa.z, qa.w), f2(qb.x, qb.y), nhf01, nhf23, nhl01, nhl23, iv.z, t[2]);
-          tpair(f2(qa1.z, qa1.w), f2(qb1.x, qb1.y), nhf01, nhf23, nhl01, nhl23, iv.w, t[3]);
-          block16(t, xx, hi, lo, cv, cvg);
-          qa = qb;
-          qa1 = qb1;
-          ++b;
-        }
+    // Full blocks only: dd = 4b..4b+3 for b = 0..nb-1 (nb even, 4nb-1 >= Dw).
+    // dd = 0 and dd beyond the distance cap read fl(1/dd) = NaN (every
+    // comparison false: a no-op target); positions past a lane's row end
+    // read -inf sentinels (t = -inf: hidden). So no partial-block code.
+    const int nb = ((Dw >> 2) + 2) & ~1;
+    unsigned ra = smem_u32(B + y0);   // row quad of block b
+    unsigned ra1 = smem_u32(B1 + y0); // shifted-copy quad of block b
+    unsigned ta = smem_u32(INV4);     // fl(1/dd) quad of block b
+    const unsigned xd = smem_u32(X4) - ta;
+    float4 qa = lds128(ra), qa1 = lds128(ra1);
+    float cvg = 0.f;
+    for (int b = 0; b < nb; b += 2) {
+      const float4 qb = lds128(ra + 16), qc = lds128(ra + 32);
+      const float4 qb1 = lds128(ra1 + 16), qc1 = lds128(ra1 + 32);
+      const float4 iv0 = lds128(ta), iv1 = lds128(ta + 16);
+      const float4 xx0 = lds128(ta + xd), xx1 = lds128(ta + xd + 16);
+      ra += 32;
+      ra1 += 32;
+      ta += 32;
+      float t[4][4];
+      tpair(f2(qa.x, qa.y), f2(qa.z, qa.w), nhf01, nhf23, nhl01, nhl23, iv0.x, t[0]);
+      tpair(f2(qa1.x, qa1.y), f2(qa1.z, qa1.w), nhf01, nhf23, nhl01, nhl23, iv0.y, t[1]);
+      tpair(f2(qa.z, qa.w), f2(qb.x, qb.y), nhf01, nhf23, nhl01, nhl23, iv0.z, t[2]);
+      tpair(f2(qa1.z, qa1.w), f2(qb1.x, qb1.y), nhf01, nhf23, nhl01, nhl23, iv0.w, t[3]);
+      block16(t, xx0, hi, lo, cv, cvg);
+      tpair(f2(qb.x, qb.y), f2(qb.z, qb.w), nhf01, nhf23, nhl01, nhl23, iv1.x, t[0]);
+      tpair(f2(qb1.x, qb1.y), f2(qb1.z, qb1.w), nhf01, nhf23, nhl01, nhl23, iv1.y, t[1]);
+      tpair(f2(qb.z, qb.w), f2(qc.x, qc.y), nhf01, nhf23, nhl01, nhl23, iv1.z, t[2]);
+      tpair(f2(qb1.z, qb1.w), f2(qc1.x, qc1.y), nhf01, nhf23, nhl01, nhl23, iv1.w, t[3]);
+      block16(t, xx1, hi, lo, cv, cvg);
+      qa = qc;
+      qa1 = qc1;
+      if ((b & 31) == 30 || b + 2 >= nb) {
         // band check of the window, then flush the exact float sums
         if (cvg != __fadd_rn(__fadd_rn(cv[0], cv[1]), __fadd_rn(cv[2], cv[3]))) flag = 1u;
         cvg = 0.f;
@@ -295,11 +255,6 @@ __device__ __forceinline__ void scan_task(const float* __restrict__ B,
           cv[p] = 0.f;
         }
       }
-    }
-    const int bt = max(1, blast + 1);
-    if (4 * bt <= Dw) {
-      const float4 qb = Q[bt + 1], qb1 = Q1[bt + 1];
-      partial(bt, 0, Dw - 4 * bt, qb, qb1);
     }
   }
 #pragma unroll
@@ -342,13 +297,16 @@ __global__ void __launch_bounds__(512, 2) scan_kernel(ScanArgs a) {
     ctrl[0] = it;
     if (it < a.n_items) issue(it);
   }
+  // fl(1/dd) and 2dd+1; dd = 0 and the table tail read NaN (no-op targets)
+  const float qnan = __int_as_float(0x7fc00000);
   for (int d = tid; d < lay.lt; d += nthreads) {
-    INV[d] = d == 0 ? 0.0f : __frcp_rn(static_cast<float>(d));
+    INV[d] = (d == 0 || d >= a.lmax + 8) ? qnan : __frcp_rn(static_cast<float>(d));
     XT[d] = static_cast<float>(2 * d + 1);
   }
   __syncthreads();
 
   unsigned phase = 0;
+  int table_cap = 2147483647;
   for (;;) {
     const int cur = ctrl[0];
     if (cur >= a.n_items) break;
@@ -358,6 +316,16 @@ __global__ void __launch_bounds__(512, 2) scan_kernel(ScanArgs a) {
     const int first = rg.x;
     const int L = rg.y - rg.x;
     const int off = first & 3;
+    // distance cap: fl(1/dd) reads NaN for dd > max_dd (rows of one sector
+    // share the cap; the table is rewritten when it changes)
+    const int want_cap = min(sd.max_dd, a.lmax + 8);
+    if (want_cap != table_cap) {
+      for (int d = tid; d < lay.lt; d += nthreads) {
+        INV[d] = (d == 0 || d > want_cap || d >= a.lmax + 8) ? qnan
+                                                             : __frcp_rn(static_cast<float>(d));
+      }
+      table_cap = want_cap;
+    }
     mbar_wait(bar, phase);
     phase ^= 1u;
     const float ninf = -INFINITY;
