@@ -231,7 +231,7 @@ struct sks_context {
   std::map<std::tuple<int, int, int, double, double, std::vector<int>>, std::unique_ptr<Plans>>
       cache;
   // work buffers
-  DevBuf sdem, cv, cvb, queue, counters, dem, map, vis;
+  DevBuf sdem, cv, cvb, queue, sorted, counters, dem, map, vis;
   cudaEvent_t ev[8] = {};
   long long launches = 0;
 
@@ -270,7 +270,8 @@ struct sks_context {
     cv.ensure(static_cast<size_t>(b.pool_elems) * sizeof(int), device);
     if (split_bwd) cvb.ensure(static_cast<size_t>(b.pool_elems) * sizeof(int), device);
     queue.ensure(static_cast<size_t>(b.fix_cap) * sizeof(unsigned long long), device);
-    counters.ensure(64, device);
+    sorted.ensure(static_cast<size_t>(b.fix_cap) * sizeof(unsigned long long), device);
+    counters.ensure(64 + 2 * kFixBuckets * sizeof(unsigned), device);
   }
 
   ScanArgs scan_args(const Batch& b, const BatchDev& bd, double h0) {
@@ -283,6 +284,8 @@ struct sks_context {
     a.fix_queue = queue.as<unsigned long long>();
     a.fix_count = counters.as<unsigned>() + 1;
     a.fix_cap = b.fix_cap;
+    a.fix_hist = counters.as<unsigned>() + 16;
+    a.fix_sorted = sorted.as<unsigned long long>();
     a.h0 = h0;
     a.dbg_j0 = -1;
     a.dbg_h = 0.0;
@@ -300,7 +303,8 @@ struct sks_context {
       cuda_check(cudaMemsetAsync(cvb.p, 0, static_cast<size_t>(b.pool_elems) * sizeof(int), st),
                  "memset cvb");
     }
-    cuda_check(cudaMemsetAsync(counters.p, 0, 64, st), "memset counters");
+    cuda_check(cudaMemsetAsync(counters.p, 0, 64 + 2 * kFixBuckets * sizeof(unsigned), st),
+               "memset counters");
     if (a.n_items > 0) {
       int grid = 0;
       cuda_check(scan_occupancy(a.lmax, &grid), "scan occupancy");
@@ -312,8 +316,9 @@ struct sks_context {
 
   void fixup_batch(const ScanArgs& a, cudaStream_t st) {
     if (a.n_items == 0) return;
+    cuda_check(launch_fixup_sort(a, sms * 4, st), "launch fixup sort");
     cuda_check(launch_fixup(a, sms * 8, st), "launch fixup");
-    ++launches;
+    launches += 3;
   }
 
   ~sks_context() {

@@ -51,6 +51,13 @@ constexpr float kBand = 5.9604644775390625e-07f;  // 10 * 2^-24
 
 __host__ __device__ inline int round4(int x) { return (x + 3) & ~3; }
 
+// Fixup queue bucketing: bucket of a POV group by its longest scan (D of its
+// first POV), longest first, so fixup warps get POVs of similar length.
+__device__ __forceinline__ int fix_bucket(int D) {
+  return kFixBuckets - 1 - min(kFixBuckets - 1, max(D, 0) >> 5);
+}
+
+
 struct SmemLayout {
   int lp;   // round4(lmax)
   int lb;   // row buffer length (floats)
@@ -408,6 +415,7 @@ __global__ void __launch_bounds__(512, 2) scan_kernel(ScanArgs a) {
       if (!any_valid) continue;
       if (flag) {
         const unsigned slot = atomicAdd(a.fix_count, 1u);
+        atomicAdd(a.fix_hist + fix_bucket(Dw - (lane * 4)), 1u);
         if (slot < a.fix_cap) {
           a.fix_queue[slot] = pack_fix(static_cast<unsigned>(item.s),
                                        static_cast<unsigned>(item.q),
@@ -430,6 +438,42 @@ __global__ void __launch_bounds__(512, 2) scan_kernel(ScanArgs a) {
   }
 }
 
+__device__ __forceinline__ int entry_D(const ScanArgs& a, unsigned long long v) {
+  const int s = static_cast<int>(v >> 45);
+  const int q = static_cast<int>((v >> 23) & 0x3fffffu);
+  const int g = static_cast<int>(v & 0x3fffffu);
+  const SectorDev& sd = a.b.sectors[s];
+  const int2 rg = a.b.ranges[sd.row_off + q];
+  return min(sd.max_dd, rg.y - rg.x - 1 - 4 * g);
+}
+
+// Exclusive prefix of the bucket histogram (one warp), then a scatter of the
+// queue into bucket order.
+__global__ void fixup_prefix_kernel(ScanArgs a) {
+  const int lane = threadIdx.x;
+  unsigned run = 0;
+  for (int b0 = 0; b0 < kFixBuckets; b0 += 32) {
+    const unsigned c = a.fix_hist[b0 + lane];
+    unsigned incl = c;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const unsigned u = __shfl_up_sync(0xffffffffu, incl, o);
+      if (lane >= o) incl += u;
+    }
+    a.fix_hist[kFixBuckets + b0 + lane] = run + incl - c;
+    run += __shfl_sync(0xffffffffu, incl, 31);
+  }
+}
+
+__global__ void fixup_scatter_kernel(ScanArgs a) {
+  const unsigned n = min(*a.fix_count, a.fix_cap);
+  for (unsigned e = blockIdx.x * blockDim.x + threadIdx.x; e < n; e += gridDim.x * blockDim.x) {
+    const unsigned long long v = a.fix_queue[e];
+    const unsigned pos = atomicAdd(a.fix_hist + kFixBuckets + fix_bucket(entry_D(a, v)), 1u);
+    a.fix_sorted[pos] = v;
+  }
+}
+
 // Exact resolution of flagged POV groups. One thread per (queue entry, POV):
 // the thread re-runs the same FP32 certified filter as the scan kernel (same
 // operations, so the same certified decisions) and resolves every target
@@ -445,7 +489,7 @@ __global__ void __launch_bounds__(256) fixup_kernel(ScanArgs a) {
   const unsigned long long stride = static_cast<unsigned long long>(gridDim.x) * blockDim.x;
   for (unsigned long long w = static_cast<unsigned long long>(blockIdx.x) * blockDim.x + threadIdx.x;
        w < total; w += stride) {
-    const unsigned long long v = a.fix_queue[w >> 2];
+    const unsigned long long v = a.fix_sorted[w >> 2];
     const int p = static_cast<int>(w & 3);
     const int s = static_cast<int>(v >> 45);
     const int q = static_cast<int>((v >> 23) & 0x3fffffu);
@@ -551,6 +595,13 @@ int launch_scan(const ScanArgs& a, int grid, void* stream) {
                                        static_cast<int>(smem));
   if (e != cudaSuccess) return static_cast<int>(e);
   fn<<<grid, scan_block_threads(a.lmax), smem, static_cast<cudaStream_t>(stream)>>>(a);
+  return static_cast<int>(cudaGetLastError());
+}
+
+int launch_fixup_sort(const ScanArgs& a, int grid, void* stream) {
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  fixup_prefix_kernel<<<1, 32, 0, st>>>(a);
+  fixup_scatter_kernel<<<grid, 256, 0, st>>>(a);
   return static_cast<int>(cudaGetLastError());
 }
 

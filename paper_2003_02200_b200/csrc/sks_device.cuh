@@ -59,6 +59,8 @@ struct ScanArgs {
   unsigned long long* fix_queue;
   unsigned* fix_count;    // zero before launch
   unsigned fix_cap;
+  unsigned* fix_hist;     // kFixBuckets counters + kFixBuckets offsets, zero before launch
+  unsigned long long* fix_sorted;  // queue bucketed by scan length, longest first
   double h0;
   // debug single-POV mode (sks_linear_viewshed_row): POV j0 of row 0 of
   // sector slot 0 uses the absolute height h_abs; its per-target decisions
@@ -69,6 +71,8 @@ struct ScanArgs {
   uint8_t* dbg_vis_bwd;
   int force_exact;        // every POV group goes through the FP64 fixup
 };
+
+inline constexpr int kFixBuckets = 64;  // fixup queue buckets of 32 dd each
 
 // Packed fixup entry: sector slot (10 b) | q (22 b) | dir (1 b) | group (22 b)
 __host__ __device__ inline unsigned long long pack_fix(unsigned s, unsigned q,
@@ -91,6 +95,7 @@ int scan_block_threads(int lmax);
 int launch_scan(const ScanArgs& a, int grid, void* stream);
 int scan_occupancy(int lmax, int* grid_out);
 int launch_fixup(const ScanArgs& a, int grid, void* stream);
+int launch_fixup_sort(const ScanArgs& a, int grid, void* stream);
 int launch_unskew(const BatchDev& b, const float* unused, double* map,
                   int dimy, int dimx, void* stream);
 int launch_unskew_from_vs(const BatchDev& b, const double* skw_vs,
