@@ -62,7 +62,7 @@ struct SmemLayout {
   int lp;   // round4(lmax)
   int lb;   // row buffer length (floats)
   int lt;   // dd table length (floats)
-  int staging, s, s1, r, r1, inv, xt, total;  // float offsets / total floats
+  int staging, s, s1, r, r1, inv, xt, wms, wmr, ip, total;  // float offsets / total floats
   __host__ __device__ SmemLayout(int lmax, bool shifted) {
     lp = round4(lmax);
     lb = lp + kPad;
@@ -74,7 +74,10 @@ struct SmemLayout {
     r1 = r + lb;
     inv = r1 + (shifted ? lb : 0);
     xt = inv + lt;
-    total = xt + lt;
+    wms = xt + lt;          // window max of S per quad (12 positions)
+    wmr = wms + lb / 4;     // same for R
+    ip = wmr + lb / 4;      // (fl(1/8g), fl(1/(8g+7))) per 8-dd group
+    total = ip + round4(lt / 4 + 8);
   }
 };
 
@@ -181,6 +184,18 @@ __device__ __forceinline__ float4 lds128(unsigned addr) {
   return v;
 }
 
+__device__ __forceinline__ float lds32(unsigned addr) {
+  float v;
+  asm("ld.shared.f32 %0, [%1];" : "=f"(v) : "r"(addr));
+  return v;
+}
+
+__device__ __forceinline__ float2 lds64(unsigned addr) {
+  float2 v;
+  asm("ld.shared.v2.f32 {%0, %1}, [%2];" : "=f"(v.x), "=f"(v.y) : "r"(addr));
+  return v;
+}
+
 // One 128-POV task: POVs y0..y0+3 per lane in buffer B (row copy, forward
 // direction in B's own coordinates), dd = 1..Dw. Returns per-POV cv and the
 // lane flag. kVis: debug path recording decisions of one POV.
@@ -191,7 +206,9 @@ __device__ __forceinline__ void scan_task(const float* __restrict__ B,
                                           const float4* __restrict__ X4, int y0, int L, int Dw,
                                           const float (&hf)[4], const float (&hl)[4],
                                           float (&hi)[4], float (&lo)[4], int (&cvi)[4],
-                                          unsigned& flag, int vis_p, uint8_t* vis) {
+                                          unsigned& flag, int vis_p, uint8_t* vis,
+                                          const float* __restrict__ WM,
+                                          const float2* __restrict__ IP, float hfm, float hlm) {
   float cv[4] = {0.f, 0.f, 0.f, 0.f};
   const float2 nhf01 = f2(-hf[0], -hf[1]), nhf23 = f2(-hf[2], -hf[3]);
   const float2 nhl01 = f2(-hl[0], -hl[1]), nhl23 = f2(-hl[2], -hl[3]);
@@ -229,9 +246,51 @@ __device__ __forceinline__ void scan_task(const float* __restrict__ B,
     unsigned ra1 = smem_u32(B1 + y0); // shifted-copy quad of block b
     unsigned ta = smem_u32(INV4);     // fl(1/dd) quad of block b
     const unsigned xd = smem_u32(X4) - ta;
+    unsigned wa = smem_u32(WM + (y0 >> 2));  // window max of the lane's next 2 blocks
+    unsigned pa = smem_u32(IP);               // inv pair of the next 2 blocks
     float4 qa = lds128(ra), qa1 = lds128(ra1);
     float cvg = 0.f;
+    int backoff = 0, wait = 1;  // skip-test back-off (b = 0 reads fl(1/0) = NaN anyway)
     for (int b = 0; b < nb; b += 2) {
+      // Hidden-block skip (warp-uniform): a monotone FP32 upper bound of
+      // every t of the lane's 32 targets in blocks b, b+1 — window max
+      // elevation, the lane's lowest observer, fl(1/dd) at both ends —
+      // inflated by 10u to cover the FP32 errors of t and of the bound
+      // must lie below the lane's lowest band edge lo. Then no
+      // target can be a record or fall in the band: nothing to do.
+      if (wait == 0) {
+        const float em = lds32(wa);
+        const float2 ipv = lds64(pa);
+        const float nn = __fadd_rn(__fsub_rn(em, hfm), -hlm);
+        const float2 bb = __fmul2_rn(f2(nn, nn), ipv);
+        const float bnd = fmaxf(bb.x, bb.y);
+        const float bc = __fmaf_rn(fabsf(bnd), kBand, bnd);
+        const float lom = fminf(fminf(lo[0], lo[1]), fminf(lo[2], lo[3]));
+        if (__all_sync(0xffffffffu, bc < lom)) {
+          backoff = 0;
+          ra += 32;
+          ra1 += 32;
+          ta += 32;
+          wa += 8;
+          pa += 8;
+          qa = lds128(ra);
+          qa1 = lds128(ra1);
+          if ((b & 31) == 30 || b + 2 >= nb) {
+            if (cvg != __fadd_rn(__fadd_rn(cv[0], cv[1]), __fadd_rn(cv[2], cv[3]))) flag = 1u;
+            cvg = 0.f;
+#pragma unroll
+            for (int p = 0; p < 4; ++p) {
+              cvi[p] += __float2int_rn(cv[p]);
+              cv[p] = 0.f;
+            }
+          }
+          continue;
+        }
+        backoff = min(2 * backoff + 1, 15);
+        wait = backoff;
+      } else {
+        --wait;
+      }
       const float4 qb = lds128(ra + 16), qc = lds128(ra + 32);
       const float4 qb1 = lds128(ra1 + 16), qc1 = lds128(ra1 + 32);
       const float4 iv0 = lds128(ta), iv1 = lds128(ta + 16);
@@ -239,6 +298,8 @@ __device__ __forceinline__ void scan_task(const float* __restrict__ B,
       ra += 32;
       ra1 += 32;
       ta += 32;
+      wa += 8;
+      pa += 8;
       float t[4][4];
       tpair(f2(qa.x, qa.y), f2(qa.z, qa.w), nhf01, nhf23, nhl01, nhl23, iv0.x, t[0]);
       tpair(f2(qa1.x, qa1.y), f2(qa1.z, qa1.w), nhf01, nhf23, nhl01, nhl23, iv0.y, t[1]);
@@ -281,9 +342,11 @@ __global__ void __launch_bounds__(512, 2) scan_kernel(ScanArgs a) {
   float* R1 = smem + lay.r1;
   float* INV = smem + lay.inv;
   float* XT = smem + lay.xt;
+  float* WMS = smem + lay.wms;
+  float* WMR = smem + lay.wmr;
+  float2* IP = reinterpret_cast<float2*>(smem + lay.ip);
   const int tid = threadIdx.x;
   const int lane = tid & 31;
-  const int warp = tid >> 5;
   const int nthreads = blockDim.x;
 
   auto issue = [&](int it) {
@@ -313,7 +376,7 @@ __global__ void __launch_bounds__(512, 2) scan_kernel(ScanArgs a) {
   __syncthreads();
 
   unsigned phase = 0;
-  int table_cap = 2147483647;
+  int table_cap = -1;  // forces the first row to write INV and IP
   for (;;) {
     const int cur = ctrl[0];
     if (cur >= a.n_items) break;
@@ -331,6 +394,14 @@ __global__ void __launch_bounds__(512, 2) scan_kernel(ScanArgs a) {
         INV[d] = (d == 0 || d > want_cap || d >= a.lmax + 8) ? qnan
                                                              : __frcp_rn(static_cast<float>(d));
       }
+      // (fl(1/8g), fl(1/(8g+7))) for the skip test; NaN (= never skip) for
+      // g = 0 and for groups reaching past the cap
+      for (int g = tid; g < lay.lt / 8; g += nthreads) {
+        const int d0 = 8 * g, d1 = 8 * g + 7;
+        IP[g] = (g == 0 || d1 > want_cap || d1 >= a.lmax + 8)
+                    ? make_float2(qnan, qnan)
+                    : make_float2(__frcp_rn(static_cast<float>(d0)), __frcp_rn(static_cast<float>(d1)));
+      }
       table_cap = want_cap;
     }
     mbar_wait(bar, phase);
@@ -343,6 +414,19 @@ __global__ void __launch_bounds__(512, 2) scan_kernel(ScanArgs a) {
         S1[x] = x + 1 < L ? staging[off + x + 1] : ninf;
         R1[x] = x + 1 < L ? staging[off + L - 2 - x] : ninf;
       }
+    }
+    // window maxima for the hidden-block skip: positions 4j..4j+11
+    for (int j = tid; j < lay.lb / 4; j += nthreads) {
+      float ms = -FLT_MAX, mr = -FLT_MAX;
+      for (int u = 0; u < 12; ++u) {
+        const int x = 4 * j + u;
+        if (x < L) {
+          ms = fmaxf(ms, staging[off + x]);
+          mr = fmaxf(mr, staging[off + L - 1 - x]);
+        }
+      }
+      WMS[j] = ms;
+      WMR[j] = mr;
     }
     if (tid == 0) ctrl[1] = 0;
     __syncthreads();
@@ -409,9 +493,20 @@ __global__ void __launch_bounds__(512, 2) scan_kernel(ScanArgs a) {
       }
       uint8_t* vis = nullptr;
       if (kVis && vis_p >= 0) vis = dir ? a.dbg_vis_bwd : a.dbg_vis_fwd;
+      // the lane's lowest observer, split like h (for the skip bound)
+      double hmin = INFINITY;
+#pragma unroll
+      for (int p = 0; p < 4; ++p) {
+        if (y0 + p < L) hmin = fmin(hmin, __dadd_rn(static_cast<double>(hf[p]), static_cast<double>(hl[p])));
+      }
+      float hfm = 0.f, hlm = 0.f;
+      if (hmin < INFINITY) {
+        hfm = __double2float_rn(hmin);
+        hlm = __double2float_rn(__dsub_rn(hmin, static_cast<double>(hfm)));
+      }
       scan_task<kShifted, kVis>(B, B1, reinterpret_cast<const float4*>(INV),
                                 reinterpret_cast<const float4*>(XT), y0, L, Dw, hf, hl, hi, lo,
-                                cvi, flag, vis ? vis_p : -1, vis);
+                                cvi, flag, vis ? vis_p : -1, vis, dir ? WMR : WMS, IP, hfm, hlm);
       if (!any_valid) continue;
       if (flag) {
         const unsigned slot = atomicAdd(a.fix_count, 1u);
