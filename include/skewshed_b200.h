@@ -66,6 +66,8 @@ typedef struct {
   long long flagged_groups;    /* POV groups re-run by the exact fixup */
   long long h2d_bytes;
   long long d2h_bytes;
+  long long skipped_target_slots; /* lane-target slots decided by the
+                                     certified hidden-block skip */
 } sks_stats;
 
 /* SectorPlan, skew.hpp:29-41. ops: 0 Transpose, 1 FlipCols, 2 FlipRows. */

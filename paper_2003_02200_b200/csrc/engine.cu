@@ -286,6 +286,7 @@ struct sks_context {
     a.fix_cap = b.fix_cap;
     a.fix_hist = counters.as<unsigned>() + 16;
     a.fix_sorted = sorted.as<unsigned long long>();
+    a.skipped = reinterpret_cast<unsigned long long*>(counters.as<unsigned>() + 8);
     a.h0 = h0;
     a.dbg_j0 = -1;
     a.dbg_h = 0.0;
@@ -389,7 +390,7 @@ void run_sectors(sks_context* ctx, const float* d_dem, int dimy, int dimx, doubl
   Plans& P = ctx->plans_for(dimy, dimx, cfg->ns, cellsize, cfg->max_distance, sectors);
   const long long launches0 = ctx->launches;
   double t_skew = 0, t_scan = 0, t_fix = 0, t_unskew = 0;
-  long long flagged = 0, evals = 0;
+  long long flagged = 0, evals = 0, skipped = 0;
   for (auto& bp : P.batches) {
     Batch& b = *bp;
     ctx->ensure_pools(b, false);
@@ -413,9 +414,12 @@ void run_sectors(sks_context* ctx, const float* d_dem, int dimy, int dimx, doubl
       t_scan += elapsed(ctx->ev[1], ctx->ev[2]);
       t_fix += elapsed(ctx->ev[2], ctx->ev[3]);
       t_unskew += elapsed(ctx->ev[3], ctx->ev[4]);
-      unsigned cnt[2] = {0, 0};
+      unsigned cnt[10] = {};
       cuda_check(cudaMemcpy(cnt, ctx->counters.p, sizeof(cnt), cudaMemcpyDeviceToHost), "counters");
       flagged += cnt[1];
+      unsigned long long sk = 0;
+      std::memcpy(&sk, cnt + 8, sizeof(sk));
+      skipped += static_cast<long long>(sk);
     }
     evals += b.target_evals;
   }
@@ -429,6 +433,7 @@ void run_sectors(sks_context* ctx, const float* d_dem, int dimy, int dimx, doubl
     stats->kernel_launches += ctx->launches - launches0;
     stats->target_evals += evals;
     stats->flagged_groups += flagged;
+    stats->skipped_target_slots += skipped;
   }
 }
 

@@ -208,7 +208,8 @@ __device__ __forceinline__ void scan_task(const float* __restrict__ B,
                                           float (&hi)[4], float (&lo)[4], int (&cvi)[4],
                                           unsigned& flag, int vis_p, uint8_t* vis,
                                           const float* __restrict__ WM,
-                                          const float2* __restrict__ IP, float hfm, float hlm) {
+                                          const float2* __restrict__ IP, float hfm, float hlm,
+                                          unsigned long long* skipped) {
   float cv[4] = {0.f, 0.f, 0.f, 0.f};
   const float2 nhf01 = f2(-hf[0], -hf[1]), nhf23 = f2(-hf[2], -hf[3]);
   const float2 nhl01 = f2(-hl[0], -hl[1]), nhl23 = f2(-hl[2], -hl[3]);
@@ -251,6 +252,7 @@ __device__ __forceinline__ void scan_task(const float* __restrict__ B,
     float4 qa = lds128(ra), qa1 = lds128(ra1);
     float cvg = 0.f;
     int backoff = 0, wait = 1;  // skip-test back-off (b = 0 reads fl(1/0) = NaN anyway)
+    unsigned nskip = 0;
     for (int b = 0; b < nb; b += 2) {
       // Hidden-block skip (warp-uniform): a monotone FP32 upper bound of
       // every t of the lane's 32 targets in blocks b, b+1 — window max
@@ -268,6 +270,7 @@ __device__ __forceinline__ void scan_task(const float* __restrict__ B,
         const float lom = fminf(fminf(lo[0], lo[1]), fminf(lo[2], lo[3]));
         if (__all_sync(0xffffffffu, bc < lom)) {
           backoff = 0;
+          ++nskip;
           ra += 32;
           ra1 += 32;
           ta += 32;
@@ -323,6 +326,10 @@ __device__ __forceinline__ void scan_task(const float* __restrict__ B,
           cv[p] = 0.f;
         }
       }
+    }
+    // 2 blocks x 4 dd x 4 POVs x 32 lanes per skipped pair
+    if (skipped != nullptr && nskip != 0 && (threadIdx.x & 31) == 0) {
+      atomicAdd(skipped, 1024ull * nskip);
     }
   }
 #pragma unroll
@@ -506,7 +513,8 @@ __global__ void __launch_bounds__(512, 2) scan_kernel(ScanArgs a) {
       }
       scan_task<kShifted, kVis>(B, B1, reinterpret_cast<const float4*>(INV),
                                 reinterpret_cast<const float4*>(XT), y0, L, Dw, hf, hl, hi, lo,
-                                cvi, flag, vis ? vis_p : -1, vis, dir ? WMR : WMS, IP, hfm, hlm);
+                                cvi, flag, vis ? vis_p : -1, vis, dir ? WMR : WMS, IP, hfm, hlm,
+                                a.skipped);
       if (!any_valid) continue;
       if (flag) {
         const unsigned slot = atomicAdd(a.fix_count, 1u);

@@ -61,6 +61,7 @@ struct ScanArgs {
   unsigned fix_cap;
   unsigned* fix_hist;     // kFixBuckets counters + kFixBuckets offsets, zero before launch
   unsigned long long* fix_sorted;  // queue bucketed by scan length, longest first
+  unsigned long long* skipped;     // lane-target slots decided by the hidden-block skip
   double h0;
   // debug single-POV mode (sks_linear_viewshed_row): POV j0 of row 0 of
   // sector slot 0 uses the absolute height h_abs; its per-target decisions

@@ -146,6 +146,7 @@ class EngineStats:
     flagged_groups: int = 0
     h2d_bytes: int = 0
     d2h_bytes: int = 0
+    skipped_target_slots: int = 0
 
     @classmethod
     def from_c(cls, s: _lib.StatsC) -> "EngineStats":
