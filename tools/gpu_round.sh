@@ -1,0 +1,18 @@
+#!/bin/bash
+# One GPU evidence pass: parity suite, smoke, bench (both arms), launch list, ncu full of the hot kernels.
+# usage: bash tools/gpu_round.sh TAG [skip_ref]
+TAG=${1:-run}
+OUT=gpurun_out/$TAG
+mkdir -p $OUT
+nvidia-smi > $OUT/gpuinfo.txt 2>&1
+timeout 1200 python -m pytest tests -m gpu -x -q > $OUT/pytest_gpu.log 2>&1; echo "pytest rc=$?" >> $OUT/pytest_gpu.log
+timeout 300 python -c "import __graft_entry__ as g; g.smoke()" > $OUT/smoke.log 2>&1; echo "smoke rc=$?" >> $OUT/smoke.log
+timeout 600 python bench.py > $OUT/bench.json 2> $OUT/bench.err
+if [ "$2" != "skip_ref" ]; then
+  timeout 600 python bench.py --impl reference > $OUT/bench_ref.json 2> $OUT/bench_ref.err
+fi
+timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file $OUT/launches.csv \
+  python tools/prof_step.py --steps 1 > $OUT/launches.log 2>&1
+timeout 900 ncu --set full --clock-control none --import-source on -k regex:"scan_kernel|relocate_kernel|fixup_kernel|unskew_kernel" -c 4 \
+  -o $OUT/full python tools/prof_step.py --steps 1 > $OUT/ncu_full.log 2>&1
+echo done
