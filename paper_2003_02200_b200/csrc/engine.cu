@@ -117,6 +117,16 @@ struct Plans {
   std::vector<std::unique_ptr<Batch>> batches;
 };
 
+// Target-lockstep scan (scan2.cu) unless disabled with SKS_SCAN=1 or the rows
+// are too long for its shared-memory slots.
+int scan2_slots_for(int lmax) {
+  static const bool off = [] {
+    const char* s = std::getenv("SKS_SCAN");
+    return s != nullptr && std::atoi(s) == 1;
+  }();
+  return off ? 0 : scan2_slots(lmax);
+}
+
 long long batch_budget_bytes() {
   if (const char* s = std::getenv("SKS_BATCH_GB")) {
     double gb = std::atof(s);
@@ -163,7 +173,7 @@ std::unique_ptr<Batch> make_batch(const std::vector<SectorPlanH>& plans,
       if (L >= 2 && p.max_dd > 0) {
         b->items.push_back(ScanItem{static_cast<int>(s), q});
         b->lmax = std::max(b->lmax, L);
-        b->fix_cap += 2u * static_cast<unsigned>((L + 3) / 4);
+        b->fix_cap += 2u * static_cast<unsigned>((L + 1) / 2);  // 2-POV groups x 2 directions
       }
     }
     b->target_evals += p.target_evals;
@@ -293,6 +303,7 @@ struct sks_context {
     a.dbg_vis_fwd = nullptr;
     a.dbg_vis_bwd = nullptr;
     a.force_exact = 0;
+    a.fix_group = scan2_slots_for(a.lmax) > 0 ? 2 : 4;
     return a;
   }
 
@@ -307,10 +318,15 @@ struct sks_context {
     cuda_check(cudaMemsetAsync(counters.p, 0, 64 + 2 * kFixBuckets * sizeof(unsigned), st),
                "memset counters");
     if (a.n_items > 0) {
-      int grid = 0;
-      cuda_check(scan_occupancy(a.lmax, &grid), "scan occupancy");
-      grid = std::min(grid, std::max(1, a.n_items));
-      cuda_check(launch_scan(a, grid, st), "launch scan");
+      const int nslots = scan2_slots_for(a.lmax);
+      if (nslots > 0) {
+        cuda_check(launch_scan2(a, nslots, st), "launch scan2");
+      } else {
+        int grid = 0;
+        cuda_check(scan_occupancy(a.lmax, &grid), "scan occupancy");
+        grid = std::min(grid, std::max(1, a.n_items));
+        cuda_check(launch_scan(a, grid, st), "launch scan");
+      }
       ++launches;
     }
   }

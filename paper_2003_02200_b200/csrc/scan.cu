@@ -40,6 +40,7 @@
 #include <cstdint>
 
 #include "sks_device.cuh"
+#include "sks_ptx.cuh"
 
 namespace sks {
 
@@ -50,13 +51,6 @@ constexpr int kPad = 144;    // -inf sentinels after each row copy
 constexpr float kBand = 5.9604644775390625e-07f;  // 10 * 2^-24
 
 __host__ __device__ inline int round4(int x) { return (x + 3) & ~3; }
-
-// Fixup queue bucketing: bucket of a POV group by its longest scan (D of its
-// first POV), longest first, so fixup warps get POVs of similar length.
-__device__ __forceinline__ int fix_bucket(int D) {
-  return kFixBuckets - 1 - min(kFixBuckets - 1, max(D, 0) >> 5);
-}
-
 
 struct SmemLayout {
   int lp;   // round4(lmax)
@@ -80,39 +74,6 @@ struct SmemLayout {
     total = ip + round4(lt / 4 + 8);
   }
 };
-
-// ---- PTX helpers: mbarrier + TMA bulk copy --------------------------------
-__device__ __forceinline__ unsigned smem_u32(const void* p) {
-  return static_cast<unsigned>(__cvta_generic_to_shared(p));
-}
-__device__ __forceinline__ void mbar_init(uint64_t* bar, unsigned count) {
-  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count));
-  asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-}
-__device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, unsigned bytes) {
-  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)),
-               "r"(bytes)
-               : "memory");
-}
-__device__ __forceinline__ void tma_bulk_g2s(void* dst, const void* src, unsigned bytes,
-                                             uint64_t* bar) {
-  asm volatile(
-      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
-          smem_u32(dst)),
-      "l"(src), "r"(bytes), "r"(smem_u32(bar))
-      : "memory");
-}
-__device__ __forceinline__ void mbar_wait(uint64_t* bar, unsigned parity) {
-  asm volatile(
-      "{\n\t.reg .pred p;\n\tWAIT_%=:\n\t"
-      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n\t"
-      "@!p bra WAIT_%=;\n\t}" ::"r"(smem_u32(bar)),
-      "r"(parity)
-      : "memory");
-}
-__device__ __forceinline__ void fence_proxy_async() {
-  asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-}
 
 // ---- the certified per-target step ----------------------------------------
 // Reference semantics of one target (scan.cpp:24-34) under the FP32 filter.
@@ -174,26 +135,6 @@ __device__ __forceinline__ void tpair(float2 e01, float2 e23, float2 nhf01, floa
   t[1] = a.y;
   t[2] = b.x;
   t[3] = b.y;
-}
-
-__device__ __forceinline__ float4 lds128(unsigned addr) {
-  float4 v;
-  asm("ld.shared.v4.f32 {%0, %1, %2, %3}, [%4];"
-      : "=f"(v.x), "=f"(v.y), "=f"(v.z), "=f"(v.w)
-      : "r"(addr));
-  return v;
-}
-
-__device__ __forceinline__ float lds32(unsigned addr) {
-  float v;
-  asm("ld.shared.f32 %0, [%1];" : "=f"(v) : "r"(addr));
-  return v;
-}
-
-__device__ __forceinline__ float2 lds64(unsigned addr) {
-  float2 v;
-  asm("ld.shared.v2.f32 {%0, %1}, [%2];" : "=f"(v.x), "=f"(v.y) : "r"(addr));
-  return v;
 }
 
 // One 128-POV task: POVs y0..y0+3 per lane in buffer B (row copy, forward
@@ -547,7 +488,7 @@ __device__ __forceinline__ int entry_D(const ScanArgs& a, unsigned long long v) 
   const int g = static_cast<int>(v & 0x3fffffu);
   const SectorDev& sd = a.b.sectors[s];
   const int2 rg = a.b.ranges[sd.row_off + q];
-  return min(sd.max_dd, rg.y - rg.x - 1 - 4 * g);
+  return min(sd.max_dd, rg.y - rg.x - 1 - a.fix_group * g);
 }
 
 // Exclusive prefix of the bucket histogram (one warp), then a scatter of the
@@ -588,12 +529,13 @@ __global__ void fixup_scatter_kernel(ScanArgs a) {
 // way every decision equals the reference's.
 __global__ void __launch_bounds__(256) fixup_kernel(ScanArgs a) {
   const unsigned n = min(*a.fix_count, a.fix_cap);
-  const unsigned long long total = 4ull * n;
+  const unsigned grp = static_cast<unsigned>(a.fix_group);
+  const unsigned long long total = static_cast<unsigned long long>(grp) * n;
   const unsigned long long stride = static_cast<unsigned long long>(gridDim.x) * blockDim.x;
   for (unsigned long long w = static_cast<unsigned long long>(blockIdx.x) * blockDim.x + threadIdx.x;
        w < total; w += stride) {
-    const unsigned long long v = a.fix_sorted[w >> 2];
-    const int p = static_cast<int>(w & 3);
+    const unsigned long long v = a.fix_sorted[w / grp];
+    const int p = static_cast<int>(w % grp);
     const int s = static_cast<int>(v >> 45);
     const int q = static_cast<int>((v >> 23) & 0x3fffffu);
     const int dir = static_cast<int>((v >> 22) & 1u);
@@ -602,7 +544,7 @@ __global__ void __launch_bounds__(256) fixup_kernel(ScanArgs a) {
     const int2 rg = a.b.ranges[sd.row_off + q];
     const int first = rg.x;
     const int L = rg.y - rg.x;
-    const int y = 4 * g + p;
+    const int y = a.fix_group * g + p;
     if (y >= L) continue;
     const float* rowp = a.b.sdem + sd.sdem_off + static_cast<long long>(q) * sd.pitch;
     int* dst = ((dir && a.b.cv_bwd) ? a.b.cv_bwd : a.b.cv) + sd.sdem_off +

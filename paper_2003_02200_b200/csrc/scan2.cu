@@ -1,0 +1,527 @@
+// Line-of-sight scan, target-lockstep mapping (sm_100a) — the production scan.
+//
+// Replaces sector_viewshed / linear_viewshed_row (reference scan.cpp:8-85),
+// with the same certified FP32 filter and FP64 fixup as scan.cu (DESIGN.md
+// §3.2): per target t = fl(fl(fl(e - hf) - hl) * fl(1/dd)), band
+// [lo, hi] = t_r -+ 10u|t_r| around the last record; t > hi is a record
+// (visible), t < lo hidden, anything else flags the POV pair for the exact
+// FP64 fixup kernel.
+//
+// Mapping. A task is 64 consecutive POVs of one skewed row in one direction;
+// lane l owns POVs y = 64c + 2l and 64c + 2l + 1. All lanes of a warp walk the
+// SAME target position k (not the same distance dd): a ridge at position k is
+// then one step for the whole warp, so the warp-uniform hidden-window skip
+// below removes far more work than a distance-lockstep walk (offline model,
+// fractal 2000^2: 27% of target slots evaluated vs 46%).
+//
+// Per group of 4 targets a lane loads one broadcast quad of elevations and,
+// per POV, one quad of fl(1/dd) from a table copy whose shift makes the quad
+// 16-byte aligned (4 shifted copies; dd = k - y differs per lane). The ring
+// sum cv = sum over visible targets of (2dd+1) is accumulated without a
+// per-lane table: records add (k + 2^22) to an integer (one predicated IADD3),
+// so after a 64-target window A = sum(k) + n*2^22 and
+// cv += 2*sum(k) - (2y-1)*n. Near hits (t >= lo) are counted in a float G;
+// G != n0 + n1 means a target fell in the uncertainty band.
+//
+// Hidden-window skip (exact, no inflation). For a window [k0, k0+w) and POV
+// p: N = fl(fl(em - hf) - hl) with em the window's maximum elevation, and
+// B = max(fl(N*fl(1/dl)), fl(N*fl(1/dh))), dl/dh the window's smallest and
+// largest dd. Rounding is monotone, so every t of the window is <= B (both
+// signs of N); if B < lo for every POV of the warp no target can
+// be a record or a band hit and the window is skipped. Coarse windows of 64
+// targets are tested first, then windows of 16.
+//
+// Scheduling. One persistent CTA per SM (32 warps) keeps up to 8 rows in
+// shared-memory slots. Warps claim tasks from any ready slot (CAS on the
+// slot's packed next/ntasks word); the warp that completes a row's last task
+// loads the next row (longest first, global counter) into that slot. There is
+// no CTA-wide barrier after the start-up.
+#include <cuda_runtime.h>
+
+#include <cfloat>
+#include <climits>
+#include <cstdint>
+
+#include "sks_device.cuh"
+#include "sks_ptx.cuh"
+
+namespace sks {
+
+namespace {
+
+constexpr int kTaskPovs = 64;
+constexpr int kW = 16;     // fine window (targets)
+constexpr int kH = 64;     // coarse window (targets); also the flush period
+constexpr int kOff = 128;  // table index offset (dd >= -kOff + 1 addressable)
+constexpr int kThreads = 1024;
+constexpr int kMaxSlots = 8;
+constexpr int kCtlInts = 16;  // per slot control block
+constexpr float kBand = 5.9604644775390625e-07f;  // 10 * 2^-24
+constexpr int kSumShift = 22;
+constexpr int kSumMask = (1 << kSumShift) - 1;
+
+struct Layout2 {
+  int lb;     // row buffer (floats) per direction
+  int nw16, nw64;
+  int T;      // table length per copy (floats)
+  int slot;   // floats per slot
+  int ctl;    // floats of control blocks
+  int tables; // offset of the 4 table copies
+  int slots;  // offset of slot 0
+  __host__ __device__ Layout2(int lmax) {
+    lb = ((lmax + 64 + 63) / 64) * 64;
+    nw16 = lb / 16;
+    nw64 = lb / 64;
+    T = ((kOff + lb + 16 + 3) / 4) * 4;
+    slot = 2 * lb + 4 * nw16 + 4 * nw64;
+    ctl = kMaxSlots * kCtlInts;
+    tables = ctl;
+    slots = tables + 4 * T;
+  }
+  __host__ __device__ int total(int nslots) const { return slots + nslots * slot; }
+};
+
+// control block of one slot (ints)
+enum : int { kWord = 0, kRemaining, kDead, kS, kQ, kL, kFirst, kCap };
+
+struct Slot {
+  const float* S;
+  const float* R;
+  const float2* WS16;
+  const float2* WR16;
+  const float2* WS64;
+  const float2* WR64;
+};
+
+__device__ __forceinline__ Slot slot_ptrs(float* base, const Layout2& lay) {
+  Slot s;
+  s.S = base;
+  s.R = base + lay.lb;
+  const float2* w = reinterpret_cast<const float2*>(base + 2 * lay.lb);
+  s.WS16 = w;
+  s.WR16 = w + lay.nw16;
+  s.WS64 = w + 2 * lay.nw16;
+  s.WR64 = w + 2 * lay.nw16 + lay.nw64;
+  return s;
+}
+
+// Loads the next row (longest first) into slot `sl`; one warp. Returns false
+// and marks the slot dead when the work list is exhausted.
+__device__ void load_slot(const ScanArgs& a, int* ctl, float* base, const Layout2& lay, int lane) {
+  int it = 0;
+  if (lane == 0) it = static_cast<int>(atomicAdd(a.item_counter, 1u));
+  it = __shfl_sync(0xffffffffu, it, 0);
+  if (it >= a.n_items) {
+    if (lane == 0) atomicExch(ctl + kDead, 1);
+    return;
+  }
+  const ScanItem item = a.items[it];
+  const SectorDev& sd = a.b.sectors[item.s];
+  const int2 rg = a.b.ranges[sd.row_off + item.q];
+  const int L = rg.y - rg.x;
+  const float* src = a.b.sdem + sd.sdem_off + static_cast<long long>(item.q) * sd.pitch + rg.x;
+  float* S = base;
+  float* R = base + lay.lb;
+  const float ninf = -INFINITY;
+#pragma unroll 4
+  for (int x = lane; x < lay.lb; x += 32) S[x] = x < L ? __ldg(src + x) : ninf;
+  __syncwarp();
+  for (int x = lane; x < lay.lb; x += 32) R[x] = x < L ? S[L - 1 - x] : ninf;
+  __syncwarp();
+  float2* w16s = reinterpret_cast<float2*>(base + 2 * lay.lb);
+  float2* w16r = w16s + lay.nw16;
+  float2* w64s = w16s + 2 * lay.nw16;
+  float2* w64r = w64s + lay.nw64;
+  const unsigned sa = smem_u32(S), ra = smem_u32(R);
+  for (int w = lane; w < lay.nw16; w += 32) {
+    float ms = -INFINITY, mr = -INFINITY;
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      const float4 a4 = lds128(sa + 64 * w + 16 * u);
+      const float4 b4 = lds128(ra + 64 * w + 16 * u);
+      ms = fmaxf(ms, fmaxf(fmaxf(a4.x, a4.y), fmaxf(a4.z, a4.w)));
+      mr = fmaxf(mr, fmaxf(fmaxf(b4.x, b4.y), fmaxf(b4.z, b4.w)));
+    }
+    w16s[w] = make_float2(ms, ms);
+    w16r[w] = make_float2(mr, mr);
+  }
+  __syncwarp();
+  for (int w = lane; w < lay.nw64; w += 32) {
+    float ms = -INFINITY, mr = -INFINITY;
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      ms = fmaxf(ms, w16s[4 * w + u].x);
+      mr = fmaxf(mr, w16r[4 * w + u].x);
+    }
+    w64s[w] = make_float2(ms, ms);
+    w64r[w] = make_float2(mr, mr);
+  }
+  __syncwarp();
+  if (lane == 0) {
+    const int ntasks = 2 * ((L + kTaskPovs - 1) / kTaskPovs);
+    volatile int* v = ctl;
+    v[kS] = item.s;
+    v[kQ] = item.q;
+    v[kL] = L;
+    v[kFirst] = rg.x;
+    v[kCap] = sd.max_dd;
+    __threadfence_block();
+    atomicExch(ctl + kRemaining, ntasks);
+    __threadfence_block();
+    atomicExch(reinterpret_cast<unsigned*>(ctl + kWord), static_cast<unsigned>(ntasks) << 16);
+  }
+  __syncwarp();
+}
+
+// Per-lane state of one task (two POVs).
+struct Pov2 {
+  int y0;          // first POV (buffer coordinates); second is y0 + 1
+  bool v0, v1;     // POV exists (y < L)
+  float hf0, hf1, hl0, hl1;
+  float hi0, hi1, lo0, lo1;
+  int A0, A1;      // sum(k) + n * 2^22 of records in the current flush window
+  float G;         // near hits (t >= lo) in the current flush window
+  int cv0, cv1;    // exact ring sums
+  unsigned flag;
+};
+
+__device__ __forceinline__ void flush(Pov2& P) {
+  const int n0 = P.A0 >> kSumShift, n1 = P.A1 >> kSumShift;
+  if (__float2int_rn(P.G) != n0 + n1) P.flag = 1u;
+  P.cv0 += 2 * (P.A0 & kSumMask) - (2 * P.y0 - 1) * n0;
+  P.cv1 += 2 * (P.A1 & kSumMask) - (2 * P.y0 + 1) * n1;
+  P.A0 = 0;
+  P.A1 = 0;
+  P.G = 0.f;
+}
+
+// one target of one POV (reference semantics scan.cpp:24-34 under the filter)
+__device__ __forceinline__ bool step(float t, float& hi, float& lo, int& A, float& G, int kb) {
+  const bool pa = t > hi;
+  const bool pg = t >= lo;
+  if (pa) {
+    const float at = fabsf(t);
+    hi = __fmaf_rn(at, kBand, t);
+    lo = __fmaf_rn(at, -kBand, t);
+    A += kb;
+  }
+  if (pg) G = __fadd_rn(G, 1.0f);
+  return pa;
+}
+
+// Skip test for window [k0, k0 + w): see the file header.
+template <bool kHl>
+__device__ __forceinline__ bool window_hidden(const Pov2& P, float2 em2, unsigned iv0, int k0, int w) {
+  float2 N = __fadd2_rn(em2, make_float2(-P.hf0, -P.hf1));
+  if (kHl) N = __fadd2_rn(N, make_float2(-P.hl0, -P.hl1));
+  const int d0 = k0 - P.y0;  // POV0's smallest dd; POV1's is d0 - 1
+  const float2 ivl = make_float2(lds32(iv0 + 4 * d0), lds32(iv0 + 4 * (d0 - 1)));
+  const float2 ivh = make_float2(lds32(iv0 + 4 * (d0 + w - 1)), lds32(iv0 + 4 * (d0 + w - 2)));
+  const float2 b1 = __fmul2_rn(N, ivl);
+  const float2 b2 = __fmul2_rn(N, ivh);
+  const bool ok0 = !P.v0 || (b1.x < P.lo0 && b2.x < P.lo0);
+  const bool ok1 = !P.v1 || (b1.y < P.lo1 && b2.y < P.lo1);
+  return __all_sync(0xffffffffu, ok0 && ok1);
+}
+
+// Evaluates targets k0 .. k0+15 for both POVs.
+template <bool kHl, bool kVis>
+__device__ __forceinline__ void eval16(Pov2& P, unsigned sb, unsigned ivb0, unsigned ivb1, int k0,
+                                       int vis_p, uint8_t* vis, int vis_D) {
+#pragma unroll
+  for (int g = 0; g < 4; ++g) {
+    const int k = k0 + 4 * g;
+    const float4 e = lds128(sb + 4 * k);
+    const float4 q0 = lds128(ivb0 + 4 * k);
+    const float4 q1 = lds128(ivb1 + 4 * k);
+    float2 n0a = __fadd2_rn(make_float2(e.x, e.y), make_float2(-P.hf0, -P.hf0));
+    float2 n0b = __fadd2_rn(make_float2(e.z, e.w), make_float2(-P.hf0, -P.hf0));
+    float2 n1a = __fadd2_rn(make_float2(e.x, e.y), make_float2(-P.hf1, -P.hf1));
+    float2 n1b = __fadd2_rn(make_float2(e.z, e.w), make_float2(-P.hf1, -P.hf1));
+    if (kHl) {
+      n0a = __fadd2_rn(n0a, make_float2(-P.hl0, -P.hl0));
+      n0b = __fadd2_rn(n0b, make_float2(-P.hl0, -P.hl0));
+      n1a = __fadd2_rn(n1a, make_float2(-P.hl1, -P.hl1));
+      n1b = __fadd2_rn(n1b, make_float2(-P.hl1, -P.hl1));
+    }
+    const float2 t0a = __fmul2_rn(n0a, make_float2(q0.x, q0.y));
+    const float2 t0b = __fmul2_rn(n0b, make_float2(q0.z, q0.w));
+    const float2 t1a = __fmul2_rn(n1a, make_float2(q1.x, q1.y));
+    const float2 t1b = __fmul2_rn(n1b, make_float2(q1.z, q1.w));
+    const float t0[4] = {t0a.x, t0a.y, t0b.x, t0b.y};
+    const float t1[4] = {t1a.x, t1a.y, t1b.x, t1b.y};
+    const int kb = k + (1 << kSumShift);
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+      const bool a0 = step(t0[i], P.hi0, P.lo0, P.A0, P.G, kb + i);
+      const bool a1 = step(t1[i], P.hi1, P.lo1, P.A1, P.G, kb + i);
+      if (kVis && vis_p >= 0) {
+        const int d = k + i - (P.y0 + vis_p);
+        if (d >= 1 && d <= vis_D) vis[d - 1] = (vis_p == 0 ? a0 : a1) ? 1 : 0;
+      }
+    }
+  }
+}
+
+template <bool kHl, bool kVis>
+__device__ void run_task(const ScanArgs& a, const Layout2& lay, const Slot& sl, const float* IV,
+                         int dir, int chunk, int L, int cap, Pov2& P, int vis_p, uint8_t* vis,
+                         int vis_D, unsigned long long& skipped) {
+  const float* B = dir ? sl.R : sl.S;
+  const float2* W16 = dir ? sl.WR16 : sl.WS16;
+  const float2* W64 = dir ? sl.WR64 : sl.WS64;
+  const unsigned sb = smem_u32(B);
+  const unsigned iv0 = smem_u32(IV) + 4u * kOff;  // fl(1/d) at iv0 + 4d (copy 0)
+  // per POV: the table copy r with (k - y - r) % 4 == 0 for k % 4 == 0
+  const int y1 = P.y0 + 1;
+  const int r0 = (-P.y0) & 3, r1 = (-y1) & 3;
+  const unsigned ivb0 = smem_u32(IV + r0 * lay.T) + 4u * static_cast<unsigned>(kOff - r0 - P.y0);
+  const unsigned ivb1 = smem_u32(IV + r1 * lay.T) + 4u * static_cast<unsigned>(kOff - r1 - y1);
+  const unsigned w16a = smem_u32(W16), w64a = smem_u32(W64);
+  const int ymin = chunk * kTaskPovs;
+  const bool capped = cap < L - 1;
+  // last target every POV of the task may still use (windows wholly inside
+  // run in the main loop; the remainder is the masked tail)
+  const int kmain = capped ? ymin + cap : INT_MAX / 2;
+  const int klast = L - 1;
+  int k0 = ymin;
+  unsigned long long nskip = 0;
+  while (k0 <= klast) {
+    if (!kVis && k0 + kH - 1 <= kmain) {
+      const float2 em = lds64(w64a + 8 * (k0 / kH));
+      if (window_hidden<kHl>(P, em, iv0, k0, kH)) {
+        k0 += kH;
+        nskip += kH;
+        continue;
+      }
+    }
+    const int kc = k0 + kH;
+    bool any = false;
+    while (k0 < kc && k0 <= klast && k0 + kW - 1 <= kmain) {
+      if (!kVis) {
+        const float2 em = lds64(w16a + 8 * (k0 / kW));
+        if (window_hidden<kHl>(P, em, iv0, k0, kW)) {
+          k0 += kW;
+          nskip += kW;
+          continue;
+        }
+      }
+      eval16<kHl, kVis>(P, sb, ivb0, ivb1, k0, vis_p, vis, vis_D);
+      any = true;
+      k0 += kW;
+    }
+    if (any) flush(P);
+    if (k0 < kc && k0 <= klast) break;  // next window crosses the cap: tail
+  }
+  if (capped) {
+    // masked tail: targets beyond some POVs' distance cap
+    const int ylast = min(L - 1, ymin + kTaskPovs - 1);
+    const int kt_end = min(klast, ylast + cap);
+    const float* IVf = IV + kOff;
+    int cnt = 0;
+    for (int k = k0; k <= kt_end; ++k) {
+      const float e = B[k];
+      const int d0 = k - P.y0, d1 = d0 - 1;
+      const bool m0 = P.v0 && d0 >= 1 && d0 <= cap;
+      const bool m1 = P.v1 && d1 >= 1 && d1 <= cap;
+      const float qn = __int_as_float(0x7fc00000);
+      float t0 = __fmul_rn(__fadd_rn(__fadd_rn(e, -P.hf0), -P.hl0), m0 ? IVf[d0] : qn);
+      float t1 = __fmul_rn(__fadd_rn(__fadd_rn(e, -P.hf1), -P.hl1), m1 ? IVf[d1] : qn);
+      const int kb = k + (1 << kSumShift);
+      const bool a0 = step(t0, P.hi0, P.lo0, P.A0, P.G, kb);
+      const bool a1 = step(t1, P.hi1, P.lo1, P.A1, P.G, kb);
+      if (kVis && vis_p >= 0) {
+        const int d = vis_p == 0 ? d0 : d1;
+        if (d >= 1 && d <= vis_D) vis[d - 1] = (vis_p == 0 ? a0 : a1) ? 1 : 0;
+      }
+      if (++cnt == kH) {
+        flush(P);
+        cnt = 0;
+      }
+    }
+    flush(P);
+  }
+  skipped += nskip;
+}
+
+__global__ void __launch_bounds__(kThreads, 1) scan2_kernel(ScanArgs a, int nslots, int lmax) {
+  extern __shared__ __align__(16) float smem[];
+  const Layout2 lay(lmax);
+  int* ctl_all = reinterpret_cast<int*>(smem);
+  float* IV = smem + lay.tables;
+  float* slots = smem + lay.slots;
+  const int tid = threadIdx.x;
+  const int lane = tid & 31;
+  const int warp = tid >> 5;
+
+  // fl(1/d) tables, 4 copies shifted by r: IV[r][i] = fl(1/(i - kOff + r)),
+  // NaN for d <= 0 (a no-op target: every comparison is false)
+  const float qnan = __int_as_float(0x7fc00000);
+  for (int i = tid; i < 4 * lay.T; i += blockDim.x) {
+    const int r = i / lay.T, j = i - r * lay.T;
+    const int d = j - kOff + r;
+    IV[i] = d >= 1 ? __frcp_rn(static_cast<float>(d)) : qnan;
+  }
+  for (int i = tid; i < kMaxSlots * kCtlInts; i += blockDim.x) ctl_all[i] = 0;
+  __syncthreads();
+  if (warp < nslots) load_slot(a, ctl_all + warp * kCtlInts, slots + warp * lay.slot, lay, lane);
+
+  unsigned long long skipped = 0;
+  int cur = warp % nslots;
+  for (;;) {
+    int sl = -1, task = 0, alldead = 0;
+    if (lane == 0) {
+      for (int t = 0; t < nslots && sl < 0; ++t) {
+        const int i = (cur + t) % nslots;
+        unsigned* wp = reinterpret_cast<unsigned*>(ctl_all + i * kCtlInts + kWord);
+        unsigned w = *reinterpret_cast<volatile unsigned*>(wp);
+        while ((w & 0xffffu) < (w >> 16)) {
+          const unsigned old = atomicCAS(wp, w, w + 1u);
+          if (old == w) {
+            sl = i;
+            task = static_cast<int>(w & 0xffffu);
+            break;
+          }
+          w = old;
+        }
+      }
+      if (sl < 0) {
+        alldead = 1;
+        for (int i = 0; i < nslots; ++i) {
+          if (*reinterpret_cast<volatile int*>(ctl_all + i * kCtlInts + kDead) == 0) alldead = 0;
+        }
+      }
+    }
+    sl = __shfl_sync(0xffffffffu, sl, 0);
+    if (sl < 0) {
+      if (__shfl_sync(0xffffffffu, alldead, 0)) break;
+      __nanosleep(200);
+      continue;
+    }
+    task = __shfl_sync(0xffffffffu, task, 0);
+    cur = sl;
+    __threadfence_block();
+    int* ctl = ctl_all + sl * kCtlInts;
+    const volatile int* vc = ctl;
+    const int s = vc[kS], q = vc[kQ], L = vc[kL], first = vc[kFirst], cap = vc[kCap];
+    const Slot sp = slot_ptrs(slots + sl * lay.slot, lay);
+    const int dir = task & 1, chunk = task >> 1;
+    const float* B = dir ? sp.R : sp.S;
+
+    Pov2 P;
+    P.y0 = chunk * kTaskPovs + 2 * lane;
+    P.v0 = P.y0 < L;
+    P.v1 = P.y0 + 1 < L;
+    P.A0 = P.A1 = 0;
+    P.G = 0.f;
+    P.cv0 = P.cv1 = 0;
+    P.flag = a.force_exact ? 1u : 0u;
+    int vis_p = -1, vis_D = 0;
+    float hf[2], hl[2];
+#pragma unroll
+    for (int p = 0; p < 2; ++p) {
+      const int y = P.y0 + p;
+      hf[p] = 0.f;
+      hl[p] = 0.f;
+      if (y < L) {
+        const int x = dir ? (L - 1 - y) : y;
+        double h;
+        if (a.dbg_j0 >= 0 && s == 0 && q == 0 && first + x == a.dbg_j0) {
+          h = a.dbg_h;
+          vis_p = p;
+          vis_D = min(cap, L - 1 - y);
+        } else {
+          h = __dadd_rn(static_cast<double>(B[y]), a.h0);
+        }
+        const float hff = __double2float_rn(h);
+        const double hld = __dsub_rn(h, static_cast<double>(hff));
+        const float hlf = __double2float_rn(hld);
+        // filter preconditions: h = hf + hl exactly, far from overflow
+        if (static_cast<double>(hlf) != hld || !(fabsf(hff) < 1e30f)) P.flag = 1u;
+        hf[p] = hff;
+        hl[p] = hlf;
+      }
+    }
+    P.hf0 = hf[0];
+    P.hf1 = hf[1];
+    P.hl0 = hl[0];
+    P.hl1 = hl[1];
+    P.hi0 = P.v0 ? -INFINITY : INFINITY;
+    P.lo0 = P.v0 ? -FLT_MAX : INFINITY;
+    P.hi1 = P.v1 ? -INFINITY : INFINITY;
+    P.lo1 = P.v1 ? -FLT_MAX : INFINITY;
+    uint8_t* vis = nullptr;
+    if (vis_p >= 0) vis = dir ? a.dbg_vis_bwd : a.dbg_vis_fwd;
+    const bool vis_mode = a.dbg_vis_fwd != nullptr || a.dbg_vis_bwd != nullptr;
+    const bool any_hl = __any_sync(0xffffffffu, P.hl0 != 0.f || P.hl1 != 0.f);
+    if (vis_mode) {
+      if (any_hl) {
+        run_task<true, true>(a, lay, sp, IV, dir, chunk, L, cap, P, vis ? vis_p : -1, vis, vis_D, skipped);
+      } else {
+        run_task<false, true>(a, lay, sp, IV, dir, chunk, L, cap, P, vis ? vis_p : -1, vis, vis_D, skipped);
+      }
+    } else if (any_hl) {
+      run_task<true, false>(a, lay, sp, IV, dir, chunk, L, cap, P, -1, nullptr, 0, skipped);
+    } else {
+      run_task<false, false>(a, lay, sp, IV, dir, chunk, L, cap, P, -1, nullptr, 0, skipped);
+    }
+
+    if (P.v0 || P.v1) {
+      if (P.flag) {
+        const unsigned slot = atomicAdd(a.fix_count, 1u);
+        atomicAdd(a.fix_hist + fix_bucket(min(cap, L - 1 - P.y0)), 1u);
+        if (slot < a.fix_cap) {
+          a.fix_queue[slot] = pack_fix(static_cast<unsigned>(s), static_cast<unsigned>(q),
+                                       static_cast<unsigned>(dir), static_cast<unsigned>(P.y0 >> 1));
+        }
+      } else {
+        const SectorDev& sd = a.b.sectors[s];
+        int* dst = ((dir && a.b.cv_bwd) ? a.b.cv_bwd : a.b.cv) + sd.sdem_off +
+                   static_cast<long long>(q) * sd.pitch + first;
+        if (P.v0 && P.cv0 != 0) atomicAdd(dst + (dir ? L - 1 - P.y0 : P.y0), P.cv0);
+        if (P.v1 && P.cv1 != 0) atomicAdd(dst + (dir ? L - 2 - P.y0 : P.y0 + 1), P.cv1);
+      }
+    }
+    __syncwarp();
+    int last = 0;
+    if (lane == 0) last = atomicSub(ctl + kRemaining, 1) == 1;
+    if (__shfl_sync(0xffffffffu, last, 0)) load_slot(a, ctl, slots + sl * lay.slot, lay, lane);
+  }
+  if (a.skipped != nullptr && lane == 0 && skipped != 0) {
+    atomicAdd(a.skipped, 64ull * skipped);
+  }
+}
+
+}  // namespace
+
+// Slots that fit the opt-in shared memory for rows up to lmax (0: use the
+// distance-lockstep kernel of scan.cu instead).
+int scan2_slots(int lmax) {
+  const Layout2 lay(lmax);
+  const long long cap = 227 * 1024;
+  const long long fixed = 4LL * lay.slots;
+  const long long per = 4LL * lay.slot;
+  if (lmax >= 65536 - 64) return 0;
+  long long n = (cap - fixed) / per;
+  if (n < 2) return 0;
+  return static_cast<int>(n > kMaxSlots ? kMaxSlots : n);
+}
+
+size_t scan2_smem_bytes(int lmax, int nslots) {
+  return static_cast<size_t>(Layout2(lmax).total(nslots)) * sizeof(float);
+}
+
+int launch_scan2(const ScanArgs& a, int nslots, void* stream) {
+  int dev = 0;
+  cudaGetDevice(&dev);
+  int sms = 0;
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  const size_t smem = scan2_smem_bytes(a.lmax, nslots);
+  cudaError_t e = cudaFuncSetAttribute(scan2_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                       static_cast<int>(smem));
+  if (e != cudaSuccess) return static_cast<int>(e);
+  scan2_kernel<<<sms, kThreads, smem, static_cast<cudaStream_t>(stream)>>>(a, nslots, a.lmax);
+  return static_cast<int>(cudaGetLastError());
+}
+
+}  // namespace sks

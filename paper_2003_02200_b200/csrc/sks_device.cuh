@@ -71,9 +71,16 @@ struct ScanArgs {
   uint8_t* dbg_vis_fwd;
   uint8_t* dbg_vis_bwd;
   int force_exact;        // every POV group goes through the FP64 fixup
+  int fix_group;          // POVs per fixup entry: 2 (scan2_kernel) or 4 (scan_kernel)
 };
 
 inline constexpr int kFixBuckets = 64;  // fixup queue buckets of 32 dd each
+
+// Fixup queue bucketing: bucket of a POV group by its longest scan D,
+// longest first, so fixup warps get POVs of similar length.
+__device__ __forceinline__ int fix_bucket(int D) {
+  return kFixBuckets - 1 - min(kFixBuckets - 1, max(D, 0) >> 5);
+}
 
 // Packed fixup entry: sector slot (10 b) | q (22 b) | dir (1 b) | group (22 b)
 __host__ __device__ inline unsigned long long pack_fix(unsigned s, unsigned q,
@@ -96,6 +103,9 @@ int scan_block_threads(int lmax);
 int launch_scan(const ScanArgs& a, int grid, void* stream);
 int scan_occupancy(int lmax, int* grid_out);
 int launch_fixup(const ScanArgs& a, int grid, void* stream);
+int scan2_slots(int lmax);  // 0: rows too long for the target-lockstep kernel
+size_t scan2_smem_bytes(int lmax, int nslots);
+int launch_scan2(const ScanArgs& a, int nslots, void* stream);
 int launch_fixup_sort(const ScanArgs& a, int grid, void* stream);
 int launch_unskew(const BatchDev& b, const float* unused, double* map,
                   int dimy, int dimx, void* stream);
