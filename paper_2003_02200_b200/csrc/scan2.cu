@@ -31,7 +31,7 @@
 // be a record or a band hit and the window is skipped. Coarse windows of 64
 // targets are tested first, then windows of 16.
 //
-// Scheduling. One persistent CTA per SM (32 warps) keeps up to 8 rows in
+// Scheduling. One persistent CTA per SM (24 warps) keeps up to 8 rows in
 // shared-memory slots. Warps claim tasks from any ready slot (CAS on the
 // slot's packed next/ntasks word); the warp that completes a row's last task
 // loads the next row (longest first, global counter) into that slot. There is
@@ -41,6 +41,7 @@
 #include <cfloat>
 #include <climits>
 #include <cstdint>
+#include <cstdlib>
 
 #include "sks_device.cuh"
 #include "sks_ptx.cuh"
@@ -53,7 +54,7 @@ constexpr int kTaskPovs = 64;
 constexpr int kW = 16;     // fine window (targets)
 constexpr int kH = 64;     // coarse window (targets); also the flush period
 constexpr int kOff = 128;  // table index offset (dd >= -kOff + 1 addressable)
-constexpr int kThreads = 1024;
+constexpr int kThreads = 768;  // 24 warps: 80 registers, no spills (1024 spills at 64)
 constexpr int kMaxSlots = 8;
 constexpr int kCtlInts = 16;  // per slot control block
 constexpr float kBand = 5.9604644775390625e-07f;  // 10 * 2^-24
@@ -63,21 +64,29 @@ constexpr int kSumMask = (1 << kSumShift) - 1;
 struct Layout2 {
   int lb;     // row buffer (floats) per direction
   int nw16, nw64;
-  int T;      // table length per copy (floats)
+  int T;      // table length per copy (floats, a multiple of 32)
+  int TB;     // reversed bound table length
   int slot;   // floats per slot
   int ctl;    // floats of control blocks
   int tables; // offset of the 4 table copies
+  int rb;     // offset of the reversed bound table
   int slots;  // offset of slot 0
   __host__ __device__ Layout2(int lmax) {
     lb = ((lmax + 64 + 63) / 64) * 64;
     nw16 = lb / 16;
     nw64 = lb / 64;
-    T = ((kOff + lb + 16 + 3) / 4) * 4;
+    T = ((kOff + lb + 16 + 31) / 32) * 32;
+    TB = ((lb + 80 + 3) / 4) * 4;
     slot = 2 * lb + 4 * nw16 + 4 * nw64;
     ctl = kMaxSlots * kCtlInts;
     tables = ctl;
-    slots = tables + 4 * T;
+    rb = tables + 4 * T + 32;
+    slots = rb + TB;
   }
+  // Copy r starts at r*T plus a bank offset (in quads: 0, 0, 5, 4) so that
+  // the two copies one LDS.128 reads (0/2 for the first POV of even/odd
+  // lanes, 3/1 for the second) hit disjoint banks in every quarter-warp.
+  __host__ __device__ int copy(int r) const { return tables + r * T + 4 * ((0x4500 >> (4 * r)) & 15); }
   __host__ __device__ int total(int nslots) const { return slots + nslots * slot; }
 };
 
@@ -195,8 +204,25 @@ __device__ __forceinline__ void flush(Pov2& P) {
   P.G = 0.f;
 }
 
-// one target of one POV (reference semantics scan.cpp:24-34 under the filter)
-__device__ __forceinline__ bool step(float t, float& hi, float& lo, int& A, float& G, int kb) {
+// One target of one POV (reference semantics scan.cpp:24-34 under the
+// filter): record if t > hi (band update, A += kb), near hit if t >= lo.
+// Written in PTX so every update stays a single predicated instruction
+// (C++ lets ptxas turn the integer add into SEL + IADD3).
+__device__ __forceinline__ void step(float t, float& hi, float& lo, int& A, float& G, int kb) {
+  asm("{\n\t.reg .pred pa, pg;\n\t.reg .f32 at;\n\t"
+      "setp.gt.f32 pa, %4, %0;\n\t"
+      "setp.ge.f32 pg, %4, %1;\n\t"
+      "abs.f32 at, %4;\n\t"
+      "@pa fma.rn.f32 %0, at, %6, %4;\n\t"
+      "@pa fma.rn.f32 %1, at, %7, %4;\n\t"
+      "@pa add.s32 %2, %2, %5;\n\t"
+      "@pg add.rn.f32 %3, %3, 0f3F800000;\n\t}"
+      : "+f"(hi), "+f"(lo), "+r"(A), "+f"(G)
+      : "f"(t), "r"(kb), "f"(kBand), "f"(-kBand));
+}
+
+// Same with the decision returned (debug visibility capture).
+__device__ __forceinline__ bool step_vis(float t, float& hi, float& lo, int& A, float& G, int kb) {
   const bool pa = t > hi;
   const bool pg = t >= lo;
   if (pa) {
@@ -209,19 +235,20 @@ __device__ __forceinline__ bool step(float t, float& hi, float& lo, int& A, floa
   return pa;
 }
 
-// Skip test for window [k0, k0 + w): see the file header.
+// Skip test for window [k0, k0 + w): see the file header. rb0 addresses
+// RB[C - (k0 - y0)] for k0 = 0; the pair there is (1/dl0, 1/dl1) (both POVs'
+// smallest dd, clamped to 1) and w floats lower (1/(dl0 + w), 1/(dl1 + w)),
+// one past each POV's largest dd, still a bound because fl(1/d) is monotone.
+// Absent POVs have hf = +inf, so N = -inf and they never block a skip.
 template <bool kHl>
-__device__ __forceinline__ bool window_hidden(const Pov2& P, float2 em2, unsigned iv0, int k0, int w) {
+__device__ __forceinline__ bool window_hidden(const Pov2& P, float2 em2, unsigned rb0, int k0, int w) {
   float2 N = __fadd2_rn(em2, make_float2(-P.hf0, -P.hf1));
   if (kHl) N = __fadd2_rn(N, make_float2(-P.hl0, -P.hl1));
-  const int d0 = k0 - P.y0;  // POV0's smallest dd; POV1's is d0 - 1
-  const float2 ivl = make_float2(lds32(iv0 + 4 * d0), lds32(iv0 + 4 * (d0 - 1)));
-  const float2 ivh = make_float2(lds32(iv0 + 4 * (d0 + w - 1)), lds32(iv0 + 4 * (d0 + w - 2)));
-  const float2 b1 = __fmul2_rn(N, ivl);
-  const float2 b2 = __fmul2_rn(N, ivh);
-  const bool ok0 = !P.v0 || (b1.x < P.lo0 && b2.x < P.lo0);
-  const bool ok1 = !P.v1 || (b1.y < P.lo1 && b2.y < P.lo1);
-  return __all_sync(0xffffffffu, ok0 && ok1);
+  const unsigned ra = rb0 - 4u * static_cast<unsigned>(k0);
+  const float2 b1 = __fmul2_rn(N, lds64(ra));
+  const float2 b2 = __fmul2_rn(N, lds64(ra - 4u * static_cast<unsigned>(w)));
+  const bool ok = (b1.x < P.lo0) & (b2.x < P.lo0) & (b1.y < P.lo1) & (b2.y < P.lo1);
+  return __all_sync(0xffffffffu, ok);
 }
 
 // Evaluates targets k0 .. k0+15 for both POVs.
@@ -253,11 +280,16 @@ __device__ __forceinline__ void eval16(Pov2& P, unsigned sb, unsigned ivb0, unsi
     const int kb = k + (1 << kSumShift);
 #pragma unroll
     for (int i = 0; i < 4; ++i) {
-      const bool a0 = step(t0[i], P.hi0, P.lo0, P.A0, P.G, kb + i);
-      const bool a1 = step(t1[i], P.hi1, P.lo1, P.A1, P.G, kb + i);
-      if (kVis && vis_p >= 0) {
-        const int d = k + i - (P.y0 + vis_p);
-        if (d >= 1 && d <= vis_D) vis[d - 1] = (vis_p == 0 ? a0 : a1) ? 1 : 0;
+      if (kVis) {
+        const bool a0 = step_vis(t0[i], P.hi0, P.lo0, P.A0, P.G, kb + i);
+        const bool a1 = step_vis(t1[i], P.hi1, P.lo1, P.A1, P.G, kb + i);
+        if (vis_p >= 0) {
+          const int d = k + i - (P.y0 + vis_p);
+          if (d >= 1 && d <= vis_D) vis[d - 1] = (vis_p == 0 ? a0 : a1) ? 1 : 0;
+        }
+      } else {
+        step(t0[i], P.hi0, P.lo0, P.A0, P.G, kb + i);
+        step(t1[i], P.hi1, P.lo1, P.A1, P.G, kb + i);
       }
     }
   }
@@ -271,12 +303,12 @@ __device__ void run_task(const ScanArgs& a, const Layout2& lay, const Slot& sl, 
   const float2* W16 = dir ? sl.WR16 : sl.WS16;
   const float2* W64 = dir ? sl.WR64 : sl.WS64;
   const unsigned sb = smem_u32(B);
-  const unsigned iv0 = smem_u32(IV) + 4u * kOff;  // fl(1/d) at iv0 + 4d (copy 0)
+  const unsigned rb0 = smem_u32(IV + lay.rb) + 4u * static_cast<unsigned>(lay.lb + P.y0);
   // per POV: the table copy r with (k - y - r) % 4 == 0 for k % 4 == 0
   const int y1 = P.y0 + 1;
   const int r0 = (-P.y0) & 3, r1 = (-y1) & 3;
-  const unsigned ivb0 = smem_u32(IV + r0 * lay.T) + 4u * static_cast<unsigned>(kOff - r0 - P.y0);
-  const unsigned ivb1 = smem_u32(IV + r1 * lay.T) + 4u * static_cast<unsigned>(kOff - r1 - y1);
+  const unsigned ivb0 = smem_u32(IV + lay.copy(r0)) + 4u * static_cast<unsigned>(kOff - r0 - P.y0);
+  const unsigned ivb1 = smem_u32(IV + lay.copy(r1)) + 4u * static_cast<unsigned>(kOff - r1 - y1);
   const unsigned w16a = smem_u32(W16), w64a = smem_u32(W64);
   const int ymin = chunk * kTaskPovs;
   const bool capped = cap < L - 1;
@@ -288,8 +320,8 @@ __device__ void run_task(const ScanArgs& a, const Layout2& lay, const Slot& sl, 
   unsigned long long nskip = 0;
   while (k0 <= klast) {
     if (!kVis && k0 + kH - 1 <= kmain) {
-      const float2 em = lds64(w64a + 8 * (k0 / kH));
-      if (window_hidden<kHl>(P, em, iv0, k0, kH)) {
+      const float2 em = lds64(w64a + (static_cast<unsigned>(k0) >> 3));
+      if (window_hidden<kHl>(P, em, rb0, k0, kH)) {
         k0 += kH;
         nskip += kH;
         continue;
@@ -299,8 +331,8 @@ __device__ void run_task(const ScanArgs& a, const Layout2& lay, const Slot& sl, 
     bool any = false;
     while (k0 < kc && k0 <= klast && k0 + kW - 1 <= kmain) {
       if (!kVis) {
-        const float2 em = lds64(w16a + 8 * (k0 / kW));
-        if (window_hidden<kHl>(P, em, iv0, k0, kW)) {
+        const float2 em = lds64(w16a + (static_cast<unsigned>(k0) >> 1));
+        if (window_hidden<kHl>(P, em, rb0, k0, kW)) {
           k0 += kW;
           nskip += kW;
           continue;
@@ -317,7 +349,7 @@ __device__ void run_task(const ScanArgs& a, const Layout2& lay, const Slot& sl, 
     // masked tail: targets beyond some POVs' distance cap
     const int ylast = min(L - 1, ymin + kTaskPovs - 1);
     const int kt_end = min(klast, ylast + cap);
-    const float* IVf = IV + kOff;
+    const float* IVf = IV + lay.copy(0) + kOff;
     int cnt = 0;
     for (int k = k0; k <= kt_end; ++k) {
       const float e = B[k];
@@ -328,8 +360,8 @@ __device__ void run_task(const ScanArgs& a, const Layout2& lay, const Slot& sl, 
       float t0 = __fmul_rn(__fadd_rn(__fadd_rn(e, -P.hf0), -P.hl0), m0 ? IVf[d0] : qn);
       float t1 = __fmul_rn(__fadd_rn(__fadd_rn(e, -P.hf1), -P.hl1), m1 ? IVf[d1] : qn);
       const int kb = k + (1 << kSumShift);
-      const bool a0 = step(t0, P.hi0, P.lo0, P.A0, P.G, kb);
-      const bool a1 = step(t1, P.hi1, P.lo1, P.A1, P.G, kb);
+      const bool a0 = step_vis(t0, P.hi0, P.lo0, P.A0, P.G, kb);
+      const bool a1 = step_vis(t1, P.hi1, P.lo1, P.A1, P.G, kb);
       if (kVis && vis_p >= 0) {
         const int d = vis_p == 0 ? d0 : d1;
         if (d >= 1 && d <= vis_D) vis[d - 1] = (vis_p == 0 ? a0 : a1) ? 1 : 0;
@@ -344,11 +376,12 @@ __device__ void run_task(const ScanArgs& a, const Layout2& lay, const Slot& sl, 
   skipped += nskip;
 }
 
-__global__ void __launch_bounds__(kThreads, 1) scan2_kernel(ScanArgs a, int nslots, int lmax) {
+template <int kThr>
+__global__ void __launch_bounds__(kThr, 1) scan2_kernel(ScanArgs a, int nslots, int lmax) {
   extern __shared__ __align__(16) float smem[];
   const Layout2 lay(lmax);
   int* ctl_all = reinterpret_cast<int*>(smem);
-  float* IV = smem + lay.tables;
+  float* IV = smem;  // table copies at lay.copy(r)
   float* slots = smem + lay.slots;
   const int tid = threadIdx.x;
   const int lane = tid & 31;
@@ -360,7 +393,12 @@ __global__ void __launch_bounds__(kThreads, 1) scan2_kernel(ScanArgs a, int nslo
   for (int i = tid; i < 4 * lay.T; i += blockDim.x) {
     const int r = i / lay.T, j = i - r * lay.T;
     const int d = j - kOff + r;
-    IV[i] = d >= 1 ? __frcp_rn(static_cast<float>(d)) : qnan;
+    smem[lay.copy(r) + j] = d >= 1 ? __frcp_rn(static_cast<float>(d)) : qnan;
+  }
+  // reversed bound table RB[m] = fl(1/max(C - m, 1)), C = lb (window bounds:
+  // targets with dd <= 0 are no-ops, so dd is clamped to 1)
+  for (int m = tid; m < lay.TB; m += blockDim.x) {
+    smem[lay.rb + m] = __frcp_rn(static_cast<float>(max(lay.lb - m, 1)));
   }
   for (int i = tid; i < kMaxSlots * kCtlInts; i += blockDim.x) ctl_all[i] = 0;
   __syncthreads();
@@ -421,7 +459,7 @@ __global__ void __launch_bounds__(kThreads, 1) scan2_kernel(ScanArgs a, int nslo
 #pragma unroll
     for (int p = 0; p < 2; ++p) {
       const int y = P.y0 + p;
-      hf[p] = 0.f;
+      hf[p] = INFINITY;  // absent POV: N = -inf in the skip test
       hl[p] = 0.f;
       if (y < L) {
         const int x = dir ? (L - 1 - y) : y;
@@ -511,17 +549,30 @@ size_t scan2_smem_bytes(int lmax, int nslots) {
   return static_cast<size_t>(Layout2(lmax).total(nslots)) * sizeof(float);
 }
 
+template <int kThr>
+static int launch_scan2_t(const ScanArgs& a, int nslots, int sms, cudaStream_t st) {
+  const size_t smem = scan2_smem_bytes(a.lmax, nslots);
+  cudaError_t e = cudaFuncSetAttribute(scan2_kernel<kThr>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                       static_cast<int>(smem));
+  if (e != cudaSuccess) return static_cast<int>(e);
+  scan2_kernel<kThr><<<sms, kThr, smem, st>>>(a, nslots, a.lmax);
+  return static_cast<int>(cudaGetLastError());
+}
+
 int launch_scan2(const ScanArgs& a, int nslots, void* stream) {
   int dev = 0;
   cudaGetDevice(&dev);
   int sms = 0;
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-  const size_t smem = scan2_smem_bytes(a.lmax, nslots);
-  cudaError_t e = cudaFuncSetAttribute(scan2_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                       static_cast<int>(smem));
-  if (e != cudaSuccess) return static_cast<int>(e);
-  scan2_kernel<<<sms, kThreads, smem, static_cast<cudaStream_t>(stream)>>>(a, nslots, a.lmax);
-  return static_cast<int>(cudaGetLastError());
+  // CTA size (experiments): SKS_SCAN2_THREADS = 512, 768 (default) or 1024
+  static const int thr = [] {
+    const char* s = std::getenv("SKS_SCAN2_THREADS");
+    return s != nullptr ? std::atoi(s) : kThreads;
+  }();
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  if (thr == 1024) return launch_scan2_t<1024>(a, nslots, sms, st);
+  if (thr == 512) return launch_scan2_t<512>(a, nslots, sms, st);
+  return launch_scan2_t<kThreads>(a, nslots, sms, st);
 }
 
 }  // namespace sks
