@@ -13,7 +13,9 @@ import os
 import numpy as np
 
 HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(HERE, "libskewshed_b200.so")
+# SKS_LIB selects a variant build of the same library (kernel experiments,
+# paper_2003_02200_b200/build.py -D ... --out ...); default: the in-tree build.
+LIB_PATH = os.environ.get("SKS_LIB") or os.path.join(HERE, "libskewshed_b200.so")
 
 if not os.path.exists(LIB_PATH):
     raise ImportError(

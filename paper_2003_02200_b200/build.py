@@ -39,17 +39,20 @@ def needs_build() -> bool:
     return any(os.path.getmtime(d) > t for d in deps)
 
 
-def build(force: bool = False, verbose: bool = False) -> str:
-    if not force and not needs_build():
+def build(force: bool = False, verbose: bool = False, defines=(), out: str = None) -> str:
+    """Builds LIB (or, for kernel-variant experiments, `out` with extra -D defines)."""
+    lib = out or LIB
+    if not force and not defines and out is None and not needs_build():
         return LIB
-    objdir = os.path.join(HERE, "_obj")
+    objdir = os.path.join(HERE, "_obj" + ("_" + "_".join(d.replace("=", "") for d in defines) if defines else ""))
     os.makedirs(objdir, exist_ok=True)
     objs = []
     for src in sources():
         obj = os.path.join(objdir, os.path.basename(src) + ".o")
-        cmd = ["nvcc", *NVCC_FLAGS, "-c", src, "-o", obj]
+        dflags = [f"-D{d}" for d in defines]
+        cmd = ["nvcc", *NVCC_FLAGS, *dflags, "-c", src, "-o", obj]
         if src.endswith(".cpp"):
-            cmd = ["nvcc", *NVCC_FLAGS, "-x", "cu", "-c", src, "-o", obj]
+            cmd = ["nvcc", *NVCC_FLAGS, *dflags, "-x", "cu", "-c", src, "-o", obj]
         r = subprocess.run(cmd, capture_output=True, text=True)
         if r.returncode != 0:
             sys.stderr.write(r.stdout + r.stderr)
@@ -57,16 +60,24 @@ def build(force: bool = False, verbose: bool = False) -> str:
         if verbose:
             sys.stderr.write(r.stderr)
         objs.append(obj)
-    tmp = LIB + ".tmp"
+    tmp = lib + ".tmp"
     cmd = ["nvcc", "-gencode", "arch=compute_100a,code=sm_100a", "-shared", "-cudart", "static",
            "-o", tmp, *objs, "-lpthread"]
     r = subprocess.run(cmd, capture_output=True, text=True)
     if r.returncode != 0:
         sys.stderr.write(r.stdout + r.stderr)
         raise RuntimeError("nvcc link failed")
-    os.replace(tmp, LIB)
-    return LIB
+    os.replace(tmp, lib)
+    return lib
 
 
 if __name__ == "__main__":
-    print(build(force="--force" in sys.argv, verbose="-v" in sys.argv))
+    import argparse
+
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--force", action="store_true")
+    ap.add_argument("-v", action="store_true")
+    ap.add_argument("-D", action="append", default=[], help="extra define (variant builds)")
+    ap.add_argument("--out", default=None, help="output .so (variant builds)")
+    a = ap.parse_args()
+    print(build(force=a.force, verbose=a.v, defines=a.D, out=a.out))

@@ -13,6 +13,7 @@
 #include <algorithm>
 #include <chrono>
 #include <cmath>
+#include <cstdio>
 #include <cstring>
 #include <map>
 #include <memory>
@@ -94,6 +95,10 @@ struct DevBuf {
 
 int round_up(int x, int m) { return (x + m - 1) / m * m; }
 
+// device counters: [0] scan item, [1] flagged groups, [4] fixup item,
+// [8..9] skipped target slots (u64)
+constexpr size_t kCounterBytes = 64;
+
 // One batch of sectors, fully prepared on the host and mirrored on device.
 struct Batch {
   std::vector<int> slots;  // indices into Plans::plans, ascending k
@@ -106,10 +111,11 @@ struct Batch {
   long long pool_elems = 0;  // sdem / cv pool elements
   int lmax = 0;
   unsigned fix_cap = 0;
+  std::vector<unsigned> fix_off;  // per item: fixup queue segment offset
   int tiles_x = 0, tiles_total = 0;
   long long target_evals = 0;
   // device copies
-  DevBuf d_sectors, d_dest, d_fracf, d_fracd, d_ranges, d_items;
+  DevBuf d_sectors, d_dest, d_fracf, d_fracd, d_ranges, d_items, d_fix_off;
 };
 
 struct Plans {
@@ -173,7 +179,6 @@ std::unique_ptr<Batch> make_batch(const std::vector<SectorPlanH>& plans,
       if (L >= 2 && p.max_dd > 0) {
         b->items.push_back(ScanItem{static_cast<int>(s), q});
         b->lmax = std::max(b->lmax, L);
-        b->fix_cap += 2u * static_cast<unsigned>((L + 1) / 2);  // 2-POV groups x 2 directions
       }
     }
     b->target_evals += p.target_evals;
@@ -188,6 +193,14 @@ std::unique_ptr<Batch> make_batch(const std::vector<SectorPlanH>& plans,
     const int2 ry = b->ranges[b->sdev[y.s].row_off + y.q];
     return (rx.y - rx.x) > (ry.y - ry.x);
   });
+  // fixup queue segments, in item order: 2 entries per 2-POV group (both
+  // directions), the exact bound
+  b->fix_off.resize(b->items.size());
+  for (size_t i = 0; i < b->items.size(); ++i) {
+    const int2 r = b->ranges[b->sdev[b->items[i].s].row_off + b->items[i].q];
+    b->fix_off[i] = b->fix_cap;
+    b->fix_cap += 2u * static_cast<unsigned>((r.y - r.x + 1) / 2);
+  }
   b->tiles_x = (max_cols + relocate_tile_cols() - 1) / relocate_tile_cols();
   b->tiles_total = b->tiles_x * ((max_rows + relocate_tile_rows() - 1) / relocate_tile_rows());
   if (b->fix_cap == 0) b->fix_cap = 1;
@@ -202,6 +215,7 @@ std::unique_ptr<Batch> make_batch(const std::vector<SectorPlanH>& plans,
   up(b->d_fracd, b->fracd.data(), b->fracd.size() * sizeof(double));
   up(b->d_ranges, b->ranges.data(), b->ranges.size() * sizeof(int2));
   up(b->d_items, b->items.data(), b->items.size() * sizeof(ScanItem));
+  up(b->d_fix_off, b->fix_off.data(), b->fix_off.size() * sizeof(unsigned));
   return b;
 }
 
@@ -241,7 +255,7 @@ struct sks_context {
   std::map<std::tuple<int, int, int, double, double, std::vector<int>>, std::unique_ptr<Plans>>
       cache;
   // work buffers
-  DevBuf sdem, cv, cvb, queue, sorted, counters, dem, map, vis;
+  DevBuf sdem, cv, cvb, queue, fixcnt, counters, dem, map, vis;
   cudaEvent_t ev[8] = {};
   long long launches = 0;
 
@@ -279,9 +293,9 @@ struct sks_context {
     sdem.ensure(static_cast<size_t>(b.pool_elems) * sizeof(float), device);
     cv.ensure(static_cast<size_t>(b.pool_elems) * sizeof(int), device);
     if (split_bwd) cvb.ensure(static_cast<size_t>(b.pool_elems) * sizeof(int), device);
-    queue.ensure(static_cast<size_t>(b.fix_cap) * sizeof(unsigned long long), device);
-    sorted.ensure(static_cast<size_t>(b.fix_cap) * sizeof(unsigned long long), device);
-    counters.ensure(64 + 2 * kFixBuckets * sizeof(unsigned), device);
+    queue.ensure(static_cast<size_t>(b.fix_cap) * sizeof(unsigned), device);
+    fixcnt.ensure(std::max<size_t>(b.items.size(), 1) * sizeof(unsigned), device);
+    counters.ensure(kCounterBytes, device);
   }
 
   ScanArgs scan_args(const Batch& b, const BatchDev& bd, double h0) {
@@ -291,11 +305,11 @@ struct sks_context {
     a.n_items = static_cast<int>(b.items.size());
     a.lmax = std::max(b.lmax, 4);
     a.item_counter = counters.as<unsigned>();
-    a.fix_queue = queue.as<unsigned long long>();
+    a.fix_queue = queue.as<unsigned>();
+    a.fix_off = b.d_fix_off.as<unsigned>();
+    a.fix_cnt = fixcnt.as<unsigned>();
     a.fix_count = counters.as<unsigned>() + 1;
-    a.fix_cap = b.fix_cap;
-    a.fix_hist = counters.as<unsigned>() + 16;
-    a.fix_sorted = sorted.as<unsigned long long>();
+    a.fix_item_counter = counters.as<unsigned>() + 4;
     a.skipped = reinterpret_cast<unsigned long long*>(counters.as<unsigned>() + 8);
     a.h0 = h0;
     a.dbg_j0 = -1;
@@ -315,8 +329,10 @@ struct sks_context {
       cuda_check(cudaMemsetAsync(cvb.p, 0, static_cast<size_t>(b.pool_elems) * sizeof(int), st),
                  "memset cvb");
     }
-    cuda_check(cudaMemsetAsync(counters.p, 0, 64 + 2 * kFixBuckets * sizeof(unsigned), st),
-               "memset counters");
+    cuda_check(cudaMemsetAsync(counters.p, 0, kCounterBytes, st), "memset counters");
+    if (!b.items.empty()) {
+      cuda_check(cudaMemsetAsync(fixcnt.p, 0, b.items.size() * sizeof(unsigned), st), "memset fix_cnt");
+    }
     if (a.n_items > 0) {
       const int nslots = scan2_slots_for(a.lmax);
       if (nslots > 0) {
@@ -333,9 +349,8 @@ struct sks_context {
 
   void fixup_batch(const ScanArgs& a, cudaStream_t st) {
     if (a.n_items == 0) return;
-    cuda_check(launch_fixup_sort(a, sms * 4, st), "launch fixup sort");
-    cuda_check(launch_fixup(a, sms * 8, st), "launch fixup");
-    launches += 3;
+    cuda_check(launch_fixup(a, st), "launch fixup");
+    launches += 1;
   }
 
   ~sks_context() {
@@ -433,6 +448,29 @@ void run_sectors(sks_context* ctx, const float* d_dem, int dimy, int dimx, doubl
       unsigned cnt[10] = {};
       cuda_check(cudaMemcpy(cnt, ctx->counters.p, sizeof(cnt), cudaMemcpyDeviceToHost), "counters");
       flagged += cnt[1];
+      if (std::getenv("SKS_FIXUP_REPORT") != nullptr && !b.items.empty()) {
+        // distribution of queued POV groups over rows (diagnostics)
+        std::vector<unsigned> fc(b.items.size());
+        cuda_check(cudaMemcpy(fc.data(), ctx->fixcnt.p, fc.size() * sizeof(unsigned), cudaMemcpyDeviceToHost),
+                   "fix_cnt");
+        long long rows = 0, chunks = 0, tot = 0, work = 0, maxw = 0;
+        unsigned mx = 0;
+        for (size_t i = 0; i < fc.size(); ++i) {
+          if (fc[i] == 0) continue;
+          const int2 r = b.ranges[b.sdev[b.items[i].s].row_off + b.items[i].q];
+          ++rows;
+          tot += fc[i];
+          mx = std::max(mx, fc[i]);
+          chunks += (fc[i] * a.fix_group + 31) / 32;
+          const long long w = static_cast<long long>((fc[i] * a.fix_group + 31) / 32) * (r.y - r.x);
+          work += w;
+          maxw = std::max(maxw, w);
+        }
+        std::fprintf(stderr,
+                     "fixup: %lld groups in %lld rows (of %zu), max %u per row, %lld warp-chunks, "
+                     "chunk-work %lld (max %lld)\n",
+                     tot, rows, fc.size(), mx, chunks, work, maxw);
+      }
       unsigned long long sk = 0;
       std::memcpy(&sk, cnt + 8, sizeof(sk));
       skipped += static_cast<long long>(sk);

@@ -458,14 +458,9 @@ __global__ void __launch_bounds__(512, 2) scan_kernel(ScanArgs a) {
                                 a.skipped);
       if (!any_valid) continue;
       if (flag) {
-        const unsigned slot = atomicAdd(a.fix_count, 1u);
-        atomicAdd(a.fix_hist + fix_bucket(Dw - (lane * 4)), 1u);
-        if (slot < a.fix_cap) {
-          a.fix_queue[slot] = pack_fix(static_cast<unsigned>(item.s),
-                                       static_cast<unsigned>(item.q),
-                                       static_cast<unsigned>(dir),
-                                       static_cast<unsigned>(y0 >> 2));
-        }
+        atomicAdd(a.fix_count, 1u);
+        const unsigned slot = atomicAdd(a.fix_cnt + cur, 1u);
+        a.fix_queue[a.fix_off[cur] + slot] = pack_fix(static_cast<unsigned>(dir), static_cast<unsigned>(y0 >> 2));
       } else {
         int* dst = dir ? cvrow_b : cvrow;
 #pragma unroll
@@ -479,127 +474,6 @@ __global__ void __launch_bounds__(512, 2) scan_kernel(ScanArgs a) {
       }
     }
     __syncthreads();
-  }
-}
-
-__device__ __forceinline__ int entry_D(const ScanArgs& a, unsigned long long v) {
-  const int s = static_cast<int>(v >> 45);
-  const int q = static_cast<int>((v >> 23) & 0x3fffffu);
-  const int g = static_cast<int>(v & 0x3fffffu);
-  const SectorDev& sd = a.b.sectors[s];
-  const int2 rg = a.b.ranges[sd.row_off + q];
-  return min(sd.max_dd, rg.y - rg.x - 1 - a.fix_group * g);
-}
-
-// Exclusive prefix of the bucket histogram (one warp), then a scatter of the
-// queue into bucket order.
-__global__ void fixup_prefix_kernel(ScanArgs a) {
-  const int lane = threadIdx.x;
-  unsigned run = 0;
-  for (int b0 = 0; b0 < kFixBuckets; b0 += 32) {
-    const unsigned c = a.fix_hist[b0 + lane];
-    unsigned incl = c;
-#pragma unroll
-    for (int o = 1; o < 32; o <<= 1) {
-      const unsigned u = __shfl_up_sync(0xffffffffu, incl, o);
-      if (lane >= o) incl += u;
-    }
-    a.fix_hist[kFixBuckets + b0 + lane] = run + incl - c;
-    run += __shfl_sync(0xffffffffu, incl, 31);
-  }
-}
-
-__global__ void fixup_scatter_kernel(ScanArgs a) {
-  const unsigned n = min(*a.fix_count, a.fix_cap);
-  for (unsigned e = blockIdx.x * blockDim.x + threadIdx.x; e < n; e += gridDim.x * blockDim.x) {
-    const unsigned long long v = a.fix_queue[e];
-    const unsigned pos = atomicAdd(a.fix_hist + kFixBuckets + fix_bucket(entry_D(a, v)), 1u);
-    a.fix_sorted[pos] = v;
-  }
-}
-
-// Exact resolution of flagged POV groups. One thread per (queue entry, POV):
-// the thread re-runs the same FP32 certified filter as the scan kernel (same
-// operations, so the same certified decisions) and resolves every target
-// that falls inside the uncertainty band exactly: theta_k and the running
-// maximum theta_r (r = index of the last record, tracked here) are computed
-// with the reference's IEEE FP64 operations ((double)row[k] - h) / dd
-// (scan.cpp:24-25) and compared strictly. POVs whose h does not split
-// exactly into two floats run the FP64 recurrence on every target. Either
-// way every decision equals the reference's.
-__global__ void __launch_bounds__(256) fixup_kernel(ScanArgs a) {
-  const unsigned n = min(*a.fix_count, a.fix_cap);
-  const unsigned grp = static_cast<unsigned>(a.fix_group);
-  const unsigned long long total = static_cast<unsigned long long>(grp) * n;
-  const unsigned long long stride = static_cast<unsigned long long>(gridDim.x) * blockDim.x;
-  for (unsigned long long w = static_cast<unsigned long long>(blockIdx.x) * blockDim.x + threadIdx.x;
-       w < total; w += stride) {
-    const unsigned long long v = a.fix_sorted[w / grp];
-    const int p = static_cast<int>(w % grp);
-    const int s = static_cast<int>(v >> 45);
-    const int q = static_cast<int>((v >> 23) & 0x3fffffu);
-    const int dir = static_cast<int>((v >> 22) & 1u);
-    const int g = static_cast<int>(v & 0x3fffffu);
-    const SectorDev& sd = a.b.sectors[s];
-    const int2 rg = a.b.ranges[sd.row_off + q];
-    const int first = rg.x;
-    const int L = rg.y - rg.x;
-    const int y = a.fix_group * g + p;
-    if (y >= L) continue;
-    const float* rowp = a.b.sdem + sd.sdem_off + static_cast<long long>(q) * sd.pitch;
-    int* dst = ((dir && a.b.cv_bwd) ? a.b.cv_bwd : a.b.cv) + sd.sdem_off +
-               static_cast<long long>(q) * sd.pitch;
-    const int x = dir ? (L - 1 - y) : y;
-    const int j0 = first + x;
-    const int sg = dir ? -1 : 1;
-    const bool dbg = a.dbg_j0 >= 0 && s == 0 && q == 0 && j0 == a.dbg_j0;
-    const double h = dbg ? a.dbg_h : __dadd_rn(static_cast<double>(rowp[j0]), a.h0);
-    const int D = min(sd.max_dd, dir ? x : (L - 1 - x));
-    uint8_t* vis = dbg ? (dir ? a.dbg_vis_bwd : a.dbg_vis_fwd) : nullptr;
-    const float hf = __double2float_rn(h);
-    const double hld = __dsub_rn(h, static_cast<double>(hf));
-    const float hl = __double2float_rn(hld);
-    const bool exact_all = a.force_exact || static_cast<double>(hl) != hld || !(fabsf(hf) < 1e30f);
-    float hi = -INFINITY, lo = -FLT_MAX;
-    int r = 0;            // last record (0: none yet, max = -inf)
-    double M = -INFINITY; // exact max theta when Mvalid
-    bool Mvalid = true;
-    long long cv = 0;
-    for (int dd = 1; dd <= D; ++dd) {
-      const float e = rowp[j0 + sg * dd];
-      bool above;
-      if (!exact_all) {
-        const float inv = __frcp_rn(static_cast<float>(dd));
-        const float t = __fmul_rn(__fadd_rn(__fsub_rn(e, hf), -hl), inv);
-        if (t > hi) {
-          above = true;
-          Mvalid = false;
-        } else if (t >= lo) {
-          const double th = __ddiv_rn(__dsub_rn(static_cast<double>(e), h), static_cast<double>(dd));
-          if (!Mvalid) {
-            M = __ddiv_rn(__dsub_rn(static_cast<double>(rowp[j0 + sg * r]), h), static_cast<double>(r));
-            Mvalid = true;
-          }
-          above = th > M;
-          if (above) M = th;
-        } else {
-          above = false;
-        }
-        if (above) {
-          const float at = fabsf(t);
-          hi = __fmaf_rn(at, kBand, t);
-          lo = __fmaf_rn(at, -kBand, t);
-          r = dd;
-        }
-      } else {
-        const double th = __ddiv_rn(__dsub_rn(static_cast<double>(e), h), static_cast<double>(dd));
-        above = th > M;
-        if (above) M = th;
-      }
-      if (above) cv += 2LL * dd + 1;
-      if (vis) vis[dd - 1] = above ? 1 : 0;
-    }
-    if (cv != 0) atomicAdd(dst + j0, static_cast<int>(cv));
   }
 }
 
@@ -640,18 +514,6 @@ int launch_scan(const ScanArgs& a, int grid, void* stream) {
                                        static_cast<int>(smem));
   if (e != cudaSuccess) return static_cast<int>(e);
   fn<<<grid, scan_block_threads(a.lmax), smem, static_cast<cudaStream_t>(stream)>>>(a);
-  return static_cast<int>(cudaGetLastError());
-}
-
-int launch_fixup_sort(const ScanArgs& a, int grid, void* stream) {
-  cudaStream_t st = static_cast<cudaStream_t>(stream);
-  fixup_prefix_kernel<<<1, 32, 0, st>>>(a);
-  fixup_scatter_kernel<<<grid, 256, 0, st>>>(a);
-  return static_cast<int>(cudaGetLastError());
-}
-
-int launch_fixup(const ScanArgs& a, int grid, void* stream) {
-  fixup_kernel<<<grid, 256, 0, static_cast<cudaStream_t>(stream)>>>(a);
   return static_cast<int>(cudaGetLastError());
 }
 

@@ -18,9 +18,10 @@
 // per POV, one quad of fl(1/dd) from a table copy whose shift makes the quad
 // 16-byte aligned (4 shifted copies; dd = k - y differs per lane). The ring
 // sum cv = sum over visible targets of (2dd+1) is accumulated without a
-// per-lane table: records add (k + 2^22) to an integer (one predicated IADD3),
-// so after a 64-target window A = sum(k) + n*2^22 and
-// cv += 2*sum(k) - (2y-1)*n. Near hits (t >= lo) are counted in a float G;
+// per-lane table: records add (k + 2^22) to an integer (one predicated IADD3;
+// one accumulator per slot of a 4-target group so that the added register is
+// the group's, not the target's), so after a 64-target window
+// A = sum(k) + n*2^22 and cv += 2*sum(k) - (2y-1)*n. Near hits (t >= lo) are counted in a float G;
 // G != n0 + n1 means a target fell in the uncertainty band.
 //
 // Hidden-window skip (exact, no inflation). For a window [k0, k0+w) and POV
@@ -51,7 +52,10 @@ namespace sks {
 namespace {
 
 constexpr int kTaskPovs = 64;
-constexpr int kW = 16;     // fine window (targets)
+#ifndef SKS_FINE_W
+#define SKS_FINE_W 16
+#endif
+constexpr int kW = SKS_FINE_W;  // fine window (targets): 8 or 16
 constexpr int kH = 64;     // coarse window (targets); also the flush period
 constexpr int kOff = 128;  // table index offset (dd >= -kOff + 1 addressable)
 constexpr int kThreads = 768;  // 24 warps: 80 registers, no spills (1024 spills at 64)
@@ -73,7 +77,7 @@ struct Layout2 {
   int slots;  // offset of slot 0
   __host__ __device__ Layout2(int lmax) {
     lb = ((lmax + 64 + 63) / 64) * 64;
-    nw16 = lb / 16;
+    nw16 = lb / kW;
     nw64 = lb / 64;
     T = ((kOff + lb + 16 + 31) / 32) * 32;
     TB = ((lb + 80 + 3) / 4) * 4;
@@ -91,7 +95,7 @@ struct Layout2 {
 };
 
 // control block of one slot (ints)
-enum : int { kWord = 0, kRemaining, kDead, kS, kQ, kL, kFirst, kCap };
+enum : int { kWord = 0, kRemaining, kDead, kS, kQ, kL, kFirst, kCap, kItem };
 
 struct Slot {
   const float* S;
@@ -145,9 +149,9 @@ __device__ void load_slot(const ScanArgs& a, int* ctl, float* base, const Layout
   for (int w = lane; w < lay.nw16; w += 32) {
     float ms = -INFINITY, mr = -INFINITY;
 #pragma unroll
-    for (int u = 0; u < 4; ++u) {
-      const float4 a4 = lds128(sa + 64 * w + 16 * u);
-      const float4 b4 = lds128(ra + 64 * w + 16 * u);
+    for (int u = 0; u < kW / 4; ++u) {
+      const float4 a4 = lds128(sa + 4 * kW * w + 16 * u);
+      const float4 b4 = lds128(ra + 4 * kW * w + 16 * u);
       ms = fmaxf(ms, fmaxf(fmaxf(a4.x, a4.y), fmaxf(a4.z, a4.w)));
       mr = fmaxf(mr, fmaxf(fmaxf(b4.x, b4.y), fmaxf(b4.z, b4.w)));
     }
@@ -158,9 +162,9 @@ __device__ void load_slot(const ScanArgs& a, int* ctl, float* base, const Layout
   for (int w = lane; w < lay.nw64; w += 32) {
     float ms = -INFINITY, mr = -INFINITY;
 #pragma unroll
-    for (int u = 0; u < 4; ++u) {
-      ms = fmaxf(ms, w16s[4 * w + u].x);
-      mr = fmaxf(mr, w16r[4 * w + u].x);
+    for (int u = 0; u < kH / kW; ++u) {
+      ms = fmaxf(ms, w16s[(kH / kW) * w + u].x);
+      mr = fmaxf(mr, w16r[(kH / kW) * w + u].x);
     }
     w64s[w] = make_float2(ms, ms);
     w64r[w] = make_float2(mr, mr);
@@ -174,6 +178,7 @@ __device__ void load_slot(const ScanArgs& a, int* ctl, float* base, const Layout
     v[kL] = L;
     v[kFirst] = rg.x;
     v[kCap] = sd.max_dd;
+    v[kItem] = it;
     __threadfence_block();
     atomicExch(ctl + kRemaining, ntasks);
     __threadfence_block();
@@ -188,19 +193,27 @@ struct Pov2 {
   bool v0, v1;     // POV exists (y < L)
   float hf0, hf1, hl0, hl1;
   float hi0, hi1, lo0, lo1;
-  int A0, A1;      // sum(k) + n * 2^22 of records in the current flush window
+  int A0[4], A1[4];  // per target slot i of a 4-target group: sum(k - i) + n * 2^22 of records
   float G;         // near hits (t >= lo) in the current flush window
   int cv0, cv1;    // exact ring sums
   unsigned flag;
 };
 
 __device__ __forceinline__ void flush(Pov2& P) {
-  const int n0 = P.A0 >> kSumShift, n1 = P.A1 >> kSumShift;
+  int n0 = 0, n1 = 0, s0 = 0, s1 = 0;
+#pragma unroll
+  for (int i = 0; i < 4; ++i) {
+    const int c0 = P.A0[i] >> kSumShift, c1 = P.A1[i] >> kSumShift;
+    n0 += c0;
+    n1 += c1;
+    s0 += (P.A0[i] & kSumMask) + i * c0;
+    s1 += (P.A1[i] & kSumMask) + i * c1;
+    P.A0[i] = 0;
+    P.A1[i] = 0;
+  }
   if (__float2int_rn(P.G) != n0 + n1) P.flag = 1u;
-  P.cv0 += 2 * (P.A0 & kSumMask) - (2 * P.y0 - 1) * n0;
-  P.cv1 += 2 * (P.A1 & kSumMask) - (2 * P.y0 + 1) * n1;
-  P.A0 = 0;
-  P.A1 = 0;
+  P.cv0 += 2 * s0 - (2 * P.y0 - 1) * n0;
+  P.cv1 += 2 * s1 - (2 * P.y0 + 1) * n1;
   P.G = 0.f;
 }
 
@@ -251,12 +264,12 @@ __device__ __forceinline__ bool window_hidden(const Pov2& P, float2 em2, unsigne
   return __all_sync(0xffffffffu, ok);
 }
 
-// Evaluates targets k0 .. k0+15 for both POVs.
+// Evaluates targets k0 .. k0+kW-1 for both POVs.
 template <bool kHl, bool kVis>
 __device__ __forceinline__ void eval16(Pov2& P, unsigned sb, unsigned ivb0, unsigned ivb1, int k0,
                                        int vis_p, uint8_t* vis, int vis_D) {
 #pragma unroll
-  for (int g = 0; g < 4; ++g) {
+  for (int g = 0; g < kW / 4; ++g) {
     const int k = k0 + 4 * g;
     const float4 e = lds128(sb + 4 * k);
     const float4 q0 = lds128(ivb0 + 4 * k);
@@ -277,19 +290,21 @@ __device__ __forceinline__ void eval16(Pov2& P, unsigned sb, unsigned ivb0, unsi
     const float2 t1b = __fmul2_rn(n1b, make_float2(q1.z, q1.w));
     const float t0[4] = {t0a.x, t0a.y, t0b.x, t0b.y};
     const float t1[4] = {t1a.x, t1a.y, t1b.x, t1b.y};
+    // every record of slot i adds the group's k + 2^22 (one register for
+    // the group; the slot offset i is added back at the flush)
     const int kb = k + (1 << kSumShift);
 #pragma unroll
     for (int i = 0; i < 4; ++i) {
       if (kVis) {
-        const bool a0 = step_vis(t0[i], P.hi0, P.lo0, P.A0, P.G, kb + i);
-        const bool a1 = step_vis(t1[i], P.hi1, P.lo1, P.A1, P.G, kb + i);
+        const bool a0 = step_vis(t0[i], P.hi0, P.lo0, P.A0[i], P.G, kb);
+        const bool a1 = step_vis(t1[i], P.hi1, P.lo1, P.A1[i], P.G, kb);
         if (vis_p >= 0) {
           const int d = k + i - (P.y0 + vis_p);
           if (d >= 1 && d <= vis_D) vis[d - 1] = (vis_p == 0 ? a0 : a1) ? 1 : 0;
         }
       } else {
-        step(t0[i], P.hi0, P.lo0, P.A0, P.G, kb + i);
-        step(t1[i], P.hi1, P.lo1, P.A1, P.G, kb + i);
+        step(t0[i], P.hi0, P.lo0, P.A0[i], P.G, kb);
+        step(t1[i], P.hi1, P.lo1, P.A1[i], P.G, kb);
       }
     }
   }
@@ -318,6 +333,10 @@ __device__ void run_task(const ScanArgs& a, const Layout2& lay, const Slot& sl, 
   const int klast = L - 1;
   int k0 = ymin;
   unsigned long long nskip = 0;
+  // Flush after 32 evaluated windows: each of the 4 slot accumulators then
+  // holds <= 128 records with sum(k) < 128 * 2^15 (k < lb < 32768) and
+  // n * 2^22 <= 2^29 (A stays exact); G <= 1024.
+  int nev = 0;
   while (k0 <= klast) {
     if (!kVis && k0 + kH - 1 <= kmain) {
       const float2 em = lds64(w64a + (static_cast<unsigned>(k0) >> 3));
@@ -328,10 +347,9 @@ __device__ void run_task(const ScanArgs& a, const Layout2& lay, const Slot& sl, 
       }
     }
     const int kc = k0 + kH;
-    bool any = false;
     while (k0 < kc && k0 <= klast && k0 + kW - 1 <= kmain) {
       if (!kVis) {
-        const float2 em = lds64(w16a + (static_cast<unsigned>(k0) >> 1));
+        const float2 em = lds64(w16a + 8u * (static_cast<unsigned>(k0) / kW));
         if (window_hidden<kHl>(P, em, rb0, k0, kW)) {
           k0 += kW;
           nskip += kW;
@@ -339,12 +357,15 @@ __device__ void run_task(const ScanArgs& a, const Layout2& lay, const Slot& sl, 
         }
       }
       eval16<kHl, kVis>(P, sb, ivb0, ivb1, k0, vis_p, vis, vis_D);
-      any = true;
+      if (++nev == 32) {
+        flush(P);
+        nev = 0;
+      }
       k0 += kW;
     }
-    if (any) flush(P);
     if (k0 < kc && k0 <= klast) break;  // next window crosses the cap: tail
   }
+  flush(P);
   if (capped) {
     // masked tail: targets beyond some POVs' distance cap
     const int ylast = min(L - 1, ymin + kTaskPovs - 1);
@@ -360,8 +381,8 @@ __device__ void run_task(const ScanArgs& a, const Layout2& lay, const Slot& sl, 
       float t0 = __fmul_rn(__fadd_rn(__fadd_rn(e, -P.hf0), -P.hl0), m0 ? IVf[d0] : qn);
       float t1 = __fmul_rn(__fadd_rn(__fadd_rn(e, -P.hf1), -P.hl1), m1 ? IVf[d1] : qn);
       const int kb = k + (1 << kSumShift);
-      const bool a0 = step_vis(t0, P.hi0, P.lo0, P.A0, P.G, kb);
-      const bool a1 = step_vis(t1, P.hi1, P.lo1, P.A1, P.G, kb);
+      const bool a0 = step_vis(t0, P.hi0, P.lo0, P.A0[0], P.G, kb);
+      const bool a1 = step_vis(t1, P.hi1, P.lo1, P.A1[0], P.G, kb);
       if (kVis && vis_p >= 0) {
         const int d = vis_p == 0 ? d0 : d1;
         if (d >= 1 && d <= vis_D) vis[d - 1] = (vis_p == 0 ? a0 : a1) ? 1 : 0;
@@ -441,7 +462,7 @@ __global__ void __launch_bounds__(kThr, 1) scan2_kernel(ScanArgs a, int nslots, 
     __threadfence_block();
     int* ctl = ctl_all + sl * kCtlInts;
     const volatile int* vc = ctl;
-    const int s = vc[kS], q = vc[kQ], L = vc[kL], first = vc[kFirst], cap = vc[kCap];
+    const int s = vc[kS], q = vc[kQ], L = vc[kL], first = vc[kFirst], cap = vc[kCap], item = vc[kItem];
     const Slot sp = slot_ptrs(slots + sl * lay.slot, lay);
     const int dir = task & 1, chunk = task >> 1;
     const float* B = dir ? sp.R : sp.S;
@@ -450,7 +471,8 @@ __global__ void __launch_bounds__(kThr, 1) scan2_kernel(ScanArgs a, int nslots, 
     P.y0 = chunk * kTaskPovs + 2 * lane;
     P.v0 = P.y0 < L;
     P.v1 = P.y0 + 1 < L;
-    P.A0 = P.A1 = 0;
+#pragma unroll
+    for (int i = 0; i < 4; ++i) P.A0[i] = P.A1[i] = 0;
     P.G = 0.f;
     P.cv0 = P.cv1 = 0;
     P.flag = a.force_exact ? 1u : 0u;
@@ -506,12 +528,9 @@ __global__ void __launch_bounds__(kThr, 1) scan2_kernel(ScanArgs a, int nslots, 
 
     if (P.v0 || P.v1) {
       if (P.flag) {
-        const unsigned slot = atomicAdd(a.fix_count, 1u);
-        atomicAdd(a.fix_hist + fix_bucket(min(cap, L - 1 - P.y0)), 1u);
-        if (slot < a.fix_cap) {
-          a.fix_queue[slot] = pack_fix(static_cast<unsigned>(s), static_cast<unsigned>(q),
-                                       static_cast<unsigned>(dir), static_cast<unsigned>(P.y0 >> 1));
-        }
+        atomicAdd(a.fix_count, 1u);
+        const unsigned slot = atomicAdd(a.fix_cnt + item, 1u);
+        a.fix_queue[a.fix_off[item] + slot] = pack_fix(static_cast<unsigned>(dir), static_cast<unsigned>(P.y0 >> 1));
       } else {
         const SectorDev& sd = a.b.sectors[s];
         int* dst = ((dir && a.b.cv_bwd) ? a.b.cv_bwd : a.b.cv) + sd.sdem_off +
@@ -539,7 +558,7 @@ int scan2_slots(int lmax) {
   const long long cap = 227 * 1024;
   const long long fixed = 4LL * lay.slots;
   const long long per = 4LL * lay.slot;
-  if (lmax >= 65536 - 64) return 0;
+  if (lmax >= 32768 - 128) return 0;  // k < 2^15 keeps the flush sums exact
   long long n = (cap - fixed) / per;
   if (n < 2) return 0;
   return static_cast<int>(n > kMaxSlots ? kMaxSlots : n);

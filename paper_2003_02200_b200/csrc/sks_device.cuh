@@ -56,11 +56,14 @@ struct ScanArgs {
   int n_items;
   int lmax;               // longest row length in the batch
   unsigned* item_counter; // zero before launch
-  unsigned long long* fix_queue;
-  unsigned* fix_count;    // zero before launch
-  unsigned fix_cap;
-  unsigned* fix_hist;     // kFixBuckets counters + kFixBuckets offsets, zero before launch
-  unsigned long long* fix_sorted;  // queue bucketed by scan length, longest first
+  // Fixup queue: item it owns the segment fix_queue[fix_off[it] ..) of
+  // 2*ceil(L/2) entries (the exact bound: one per POV group and direction);
+  // fix_cnt[it] counts its entries. Entry = dir << 31 | group index.
+  unsigned* fix_queue;
+  const unsigned* fix_off;
+  unsigned* fix_cnt;      // n_items counters, zero before launch
+  unsigned* fix_count;    // total flagged groups (stats), zero before launch
+  unsigned* fix_item_counter;  // fixup kernel work counter, zero before launch
   unsigned long long* skipped;     // lane-target slots decided by the hidden-block skip
   double h0;
   // debug single-POV mode (sks_linear_viewshed_row): POV j0 of row 0 of
@@ -74,23 +77,7 @@ struct ScanArgs {
   int fix_group;          // POVs per fixup entry: 2 (scan2_kernel) or 4 (scan_kernel)
 };
 
-inline constexpr int kFixBuckets = 64;  // fixup queue buckets of 32 dd each
-
-// Fixup queue bucketing: bucket of a POV group by its longest scan D,
-// longest first, so fixup warps get POVs of similar length.
-__device__ __forceinline__ int fix_bucket(int D) {
-  return kFixBuckets - 1 - min(kFixBuckets - 1, max(D, 0) >> 5);
-}
-
-// Packed fixup entry: sector slot (10 b) | q (22 b) | dir (1 b) | group (22 b)
-__host__ __device__ inline unsigned long long pack_fix(unsigned s, unsigned q,
-                                                       unsigned dir,
-                                                       unsigned g) {
-  return (static_cast<unsigned long long>(s) << 45) |
-         (static_cast<unsigned long long>(q) << 23) |
-         (static_cast<unsigned long long>(dir) << 22) |
-         static_cast<unsigned long long>(g);
-}
+__host__ __device__ inline unsigned pack_fix(unsigned dir, unsigned g) { return (dir << 31) | g; }
 
 // Kernel entry points (launch wrappers). All return the launch error.
 // grid: (tiles_total, n_sectors); tile t -> (t / tiles_x, t % tiles_x)
@@ -102,11 +89,10 @@ size_t scan_smem_bytes(int lmax, bool shifted);
 int scan_block_threads(int lmax);
 int launch_scan(const ScanArgs& a, int grid, void* stream);
 int scan_occupancy(int lmax, int* grid_out);
-int launch_fixup(const ScanArgs& a, int grid, void* stream);
+int launch_fixup(const ScanArgs& a, void* stream);  // fixup.cu
 int scan2_slots(int lmax);  // 0: rows too long for the target-lockstep kernel
 size_t scan2_smem_bytes(int lmax, int nslots);
 int launch_scan2(const ScanArgs& a, int nslots, void* stream);
-int launch_fixup_sort(const ScanArgs& a, int grid, void* stream);
 int launch_unskew(const BatchDev& b, const float* unused, double* map,
                   int dimy, int dimx, void* stream);
 int launch_unskew_from_vs(const BatchDev& b, const double* skw_vs,
