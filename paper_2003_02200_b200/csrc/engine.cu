@@ -193,13 +193,13 @@ std::unique_ptr<Batch> make_batch(const std::vector<SectorPlanH>& plans,
     const int2 ry = b->ranges[b->sdev[y.s].row_off + y.q];
     return (rx.y - rx.x) > (ry.y - ry.x);
   });
-  // fixup queue segments, in item order: 2 entries per 2-POV group (both
-  // directions), the exact bound
+  // fixup queue segments, in item order: one entry per POV and direction,
+  // the exact bound
   b->fix_off.resize(b->items.size());
   for (size_t i = 0; i < b->items.size(); ++i) {
     const int2 r = b->ranges[b->sdev[b->items[i].s].row_off + b->items[i].q];
     b->fix_off[i] = b->fix_cap;
-    b->fix_cap += 2u * static_cast<unsigned>((r.y - r.x + 1) / 2);
+    b->fix_cap += 2u * static_cast<unsigned>(r.y - r.x);
   }
   b->tiles_x = (max_cols + relocate_tile_cols() - 1) / relocate_tile_cols();
   b->tiles_total = b->tiles_x * ((max_rows + relocate_tile_rows() - 1) / relocate_tile_rows());
@@ -255,7 +255,7 @@ struct sks_context {
   std::map<std::tuple<int, int, int, double, double, std::vector<int>>, std::unique_ptr<Plans>>
       cache;
   // work buffers
-  DevBuf sdem, cv, cvb, queue, fixcnt, counters, dem, map, vis;
+  DevBuf sdem, cv, cvb, queue, fixcnt, wm16, counters, dem, map, vis;
   cudaEvent_t ev[8] = {};
   long long launches = 0;
 
@@ -295,6 +295,7 @@ struct sks_context {
     if (split_bwd) cvb.ensure(static_cast<size_t>(b.pool_elems) * sizeof(int), device);
     queue.ensure(static_cast<size_t>(b.fix_cap) * sizeof(unsigned), device);
     fixcnt.ensure(std::max<size_t>(b.items.size(), 1) * sizeof(unsigned), device);
+    wm16.ensure(static_cast<size_t>(b.pool_elems / 16 + 1) * sizeof(float), device);
     counters.ensure(kCounterBytes, device);
   }
 
@@ -310,6 +311,7 @@ struct sks_context {
     a.fix_cnt = fixcnt.as<unsigned>();
     a.fix_count = counters.as<unsigned>() + 1;
     a.fix_item_counter = counters.as<unsigned>() + 4;
+    a.wm16 = scan2_slots_for(std::max(b.lmax, 4)) > 0 ? wm16.as<float>() : nullptr;
     a.skipped = reinterpret_cast<unsigned long long*>(counters.as<unsigned>() + 8);
     a.h0 = h0;
     a.dbg_j0 = -1;
@@ -317,7 +319,7 @@ struct sks_context {
     a.dbg_vis_fwd = nullptr;
     a.dbg_vis_bwd = nullptr;
     a.force_exact = 0;
-    a.fix_group = scan2_slots_for(a.lmax) > 0 ? 2 : 4;
+    a.fix_group = scan2_slots_for(a.lmax) > 0 ? 1 : 4;  // POVs per fixup entry
     return a;
   }
 

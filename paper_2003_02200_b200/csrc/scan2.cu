@@ -4,7 +4,7 @@
 // with the same certified FP32 filter and FP64 fixup as scan.cu (DESIGN.md
 // §3.2): per target t = fl(fl(fl(e - hf) - hl) * fl(1/dd)), band
 // [lo, hi] = t_r -+ 10u|t_r| around the last record; t > hi is a record
-// (visible), t < lo hidden, anything else flags the POV pair for the exact
+// (visible), t < lo hidden, anything else flags the POV for the exact
 // FP64 fixup kernel.
 //
 // Mapping. A task is 64 consecutive POVs of one skewed row in one direction;
@@ -21,8 +21,8 @@
 // per-lane table: records add (k + 2^22) to an integer (one predicated IADD3;
 // one accumulator per slot of a 4-target group so that the added register is
 // the group's, not the target's), so after a 64-target window
-// A = sum(k) + n*2^22 and cv += 2*sum(k) - (2y-1)*n. Near hits (t >= lo) are counted in a float G;
-// G != n0 + n1 means a target fell in the uncertainty band.
+// A = sum(k) + n*2^22 and cv += 2*sum(k) - (2y-1)*n. Near hits (t >= lo) are counted per POV in a float G;
+// G != n means a target fell in the uncertainty band (the POV alone is queued).
 //
 // Hidden-window skip (exact, no inflation). For a window [k0, k0+w) and POV
 // p: N = fl(fl(em - hf) - hl) with em the window's maximum elevation, and
@@ -157,6 +157,9 @@ __device__ void load_slot(const ScanArgs& a, int* ctl, float* base, const Layout
     }
     w16s[w] = make_float2(ms, ms);
     w16r[w] = make_float2(mr, mr);
+    if (kW == 16 && a.wm16 != nullptr && 16 * w < L) {
+      a.wm16[(sd.sdem_off + static_cast<long long>(item.q) * sd.pitch) / 16 + w] = ms;
+    }
   }
   __syncwarp();
   for (int w = lane; w < lay.nw64; w += 32) {
@@ -194,9 +197,9 @@ struct Pov2 {
   float hf0, hf1, hl0, hl1;
   float hi0, hi1, lo0, lo1;
   int A0[4], A1[4];  // per target slot i of a 4-target group: sum(k - i) + n * 2^22 of records
-  float G;         // near hits (t >= lo) in the current flush window
+  float G0, G1;    // near hits (t >= lo) in the current flush window, per POV
   int cv0, cv1;    // exact ring sums
-  unsigned flag;
+  unsigned flag0, flag1;  // POV must go to the exact fixup
 };
 
 __device__ __forceinline__ void flush(Pov2& P) {
@@ -211,10 +214,12 @@ __device__ __forceinline__ void flush(Pov2& P) {
     P.A0[i] = 0;
     P.A1[i] = 0;
   }
-  if (__float2int_rn(P.G) != n0 + n1) P.flag = 1u;
+  if (__float2int_rn(P.G0) != n0) P.flag0 = 1u;
+  if (__float2int_rn(P.G1) != n1) P.flag1 = 1u;
   P.cv0 += 2 * s0 - (2 * P.y0 - 1) * n0;
   P.cv1 += 2 * s1 - (2 * P.y0 + 1) * n1;
-  P.G = 0.f;
+  P.G0 = 0.f;
+  P.G1 = 0.f;
 }
 
 // One target of one POV (reference semantics scan.cpp:24-34 under the
@@ -296,15 +301,15 @@ __device__ __forceinline__ void eval16(Pov2& P, unsigned sb, unsigned ivb0, unsi
 #pragma unroll
     for (int i = 0; i < 4; ++i) {
       if (kVis) {
-        const bool a0 = step_vis(t0[i], P.hi0, P.lo0, P.A0[i], P.G, kb);
-        const bool a1 = step_vis(t1[i], P.hi1, P.lo1, P.A1[i], P.G, kb);
+        const bool a0 = step_vis(t0[i], P.hi0, P.lo0, P.A0[i], P.G0, kb);
+        const bool a1 = step_vis(t1[i], P.hi1, P.lo1, P.A1[i], P.G1, kb);
         if (vis_p >= 0) {
           const int d = k + i - (P.y0 + vis_p);
           if (d >= 1 && d <= vis_D) vis[d - 1] = (vis_p == 0 ? a0 : a1) ? 1 : 0;
         }
       } else {
-        step(t0[i], P.hi0, P.lo0, P.A0[i], P.G, kb);
-        step(t1[i], P.hi1, P.lo1, P.A1[i], P.G, kb);
+        step(t0[i], P.hi0, P.lo0, P.A0[i], P.G0, kb);
+        step(t1[i], P.hi1, P.lo1, P.A1[i], P.G1, kb);
       }
     }
   }
@@ -381,8 +386,8 @@ __device__ void run_task(const ScanArgs& a, const Layout2& lay, const Slot& sl, 
       float t0 = __fmul_rn(__fadd_rn(__fadd_rn(e, -P.hf0), -P.hl0), m0 ? IVf[d0] : qn);
       float t1 = __fmul_rn(__fadd_rn(__fadd_rn(e, -P.hf1), -P.hl1), m1 ? IVf[d1] : qn);
       const int kb = k + (1 << kSumShift);
-      const bool a0 = step_vis(t0, P.hi0, P.lo0, P.A0[0], P.G, kb);
-      const bool a1 = step_vis(t1, P.hi1, P.lo1, P.A1[0], P.G, kb);
+      const bool a0 = step_vis(t0, P.hi0, P.lo0, P.A0[0], P.G0, kb);
+      const bool a1 = step_vis(t1, P.hi1, P.lo1, P.A1[0], P.G1, kb);
       if (kVis && vis_p >= 0) {
         const int d = vis_p == 0 ? d0 : d1;
         if (d >= 1 && d <= vis_D) vis[d - 1] = (vis_p == 0 ? a0 : a1) ? 1 : 0;
@@ -473,9 +478,9 @@ __global__ void __launch_bounds__(kThr, 1) scan2_kernel(ScanArgs a, int nslots, 
     P.v1 = P.y0 + 1 < L;
 #pragma unroll
     for (int i = 0; i < 4; ++i) P.A0[i] = P.A1[i] = 0;
-    P.G = 0.f;
+    P.G0 = P.G1 = 0.f;
     P.cv0 = P.cv1 = 0;
-    P.flag = a.force_exact ? 1u : 0u;
+    P.flag0 = P.flag1 = a.force_exact ? 1u : 0u;
     int vis_p = -1, vis_D = 0;
     float hf[2], hl[2];
 #pragma unroll
@@ -497,7 +502,9 @@ __global__ void __launch_bounds__(kThr, 1) scan2_kernel(ScanArgs a, int nslots, 
         const double hld = __dsub_rn(h, static_cast<double>(hff));
         const float hlf = __double2float_rn(hld);
         // filter preconditions: h = hf + hl exactly, far from overflow
-        if (static_cast<double>(hlf) != hld || !(fabsf(hff) < 1e30f)) P.flag = 1u;
+        if (static_cast<double>(hlf) != hld || !(fabsf(hff) < 1e30f)) {
+          if (p == 0) P.flag0 = 1u; else P.flag1 = 1u;
+        }
         hf[p] = hff;
         hl[p] = hlf;
       }
@@ -526,17 +533,25 @@ __global__ void __launch_bounds__(kThr, 1) scan2_kernel(ScanArgs a, int nslots, 
       run_task<false, false>(a, lay, sp, IV, dir, chunk, L, cap, P, -1, nullptr, 0, skipped);
     }
 
-    if (P.v0 || P.v1) {
-      if (P.flag) {
-        atomicAdd(a.fix_count, 1u);
-        const unsigned slot = atomicAdd(a.fix_cnt + item, 1u);
-        a.fix_queue[a.fix_off[item] + slot] = pack_fix(static_cast<unsigned>(dir), static_cast<unsigned>(P.y0 >> 1));
-      } else {
-        const SectorDev& sd = a.b.sectors[s];
-        int* dst = ((dir && a.b.cv_bwd) ? a.b.cv_bwd : a.b.cv) + sd.sdem_off +
-                   static_cast<long long>(q) * sd.pitch + first;
-        if (P.v0 && P.cv0 != 0) atomicAdd(dst + (dir ? L - 1 - P.y0 : P.y0), P.cv0);
-        if (P.v1 && P.cv1 != 0) atomicAdd(dst + (dir ? L - 2 - P.y0 : P.y0 + 1), P.cv1);
+    {
+      // per POV: exact result, or a fixup queue entry (fix_group 1: entry = POV)
+      const SectorDev& sd = a.b.sectors[s];
+      int* dst = ((dir && a.b.cv_bwd) ? a.b.cv_bwd : a.b.cv) + sd.sdem_off +
+                 static_cast<long long>(q) * sd.pitch + first;
+#pragma unroll
+      for (int p = 0; p < 2; ++p) {
+        const bool v = p ? P.v1 : P.v0;
+        const unsigned fl = p ? P.flag1 : P.flag0;
+        const int cvp = p ? P.cv1 : P.cv0;
+        const int y = P.y0 + p;
+        if (!v) continue;
+        if (fl) {
+          atomicAdd(a.fix_count, 1u);
+          const unsigned slot = atomicAdd(a.fix_cnt + item, 1u);
+          a.fix_queue[a.fix_off[item] + slot] = pack_fix(static_cast<unsigned>(dir), static_cast<unsigned>(y));
+        } else if (cvp != 0) {
+          atomicAdd(dst + (dir ? L - 1 - y : y), cvp);
+        }
       }
     }
     __syncwarp();

@@ -57,13 +57,17 @@ struct ScanArgs {
   int lmax;               // longest row length in the batch
   unsigned* item_counter; // zero before launch
   // Fixup queue: item it owns the segment fix_queue[fix_off[it] ..) of
-  // 2*ceil(L/2) entries (the exact bound: one per POV group and direction);
+  // 2*L entries (the exact bound: one per POV and direction);
   // fix_cnt[it] counts its entries. Entry = dir << 31 | group index.
   unsigned* fix_queue;
   const unsigned* fix_off;
   unsigned* fix_cnt;      // n_items counters, zero before launch
   unsigned* fix_count;    // total flagged groups (stats), zero before launch
   unsigned* fix_item_counter;  // fixup kernel work counter, zero before launch
+  // Window maxima of every scanned row (forward orientation, 16 positions
+  // each) at (sdem_off + q * pitch) / 16 + w, written by scan2's row loader
+  // for the fixup's per-POV skip; nullptr: no skip (distance-lockstep scan).
+  float* wm16;
   unsigned long long* skipped;     // lane-target slots decided by the hidden-block skip
   double h0;
   // debug single-POV mode (sks_linear_viewshed_row): POV j0 of row 0 of
@@ -74,7 +78,7 @@ struct ScanArgs {
   uint8_t* dbg_vis_fwd;
   uint8_t* dbg_vis_bwd;
   int force_exact;        // every POV group goes through the FP64 fixup
-  int fix_group;          // POVs per fixup entry: 2 (scan2_kernel) or 4 (scan_kernel)
+  int fix_group;          // POVs per fixup entry: 1 (scan2_kernel) or 4 (scan_kernel)
 };
 
 __host__ __device__ inline unsigned pack_fix(unsigned dir, unsigned g) { return (dir << 31) | g; }
