@@ -56,6 +56,9 @@ constexpr int kTaskPovs = 64;
 #define SKS_FINE_W 16
 #endif
 constexpr int kW = SKS_FINE_W;  // fine window (targets): 8 or 16
+#ifndef SKS_NEAR_NOTEST
+#define SKS_NEAR_NOTEST 64
+#endif
 constexpr int kH = 64;     // coarse window (targets); also the flush period
 constexpr int kOff = 128;  // table index offset (dd >= -kOff + 1 addressable)
 constexpr int kThreads = 768;  // 24 warps: 80 registers, no spills (1024 spills at 64)
@@ -342,8 +345,11 @@ __device__ void run_task(const ScanArgs& a, const Layout2& lay, const Slot& sl, 
   // holds <= 128 records with sum(k) < 128 * 2^15 (k < lb < 32768) and
   // n * 2^22 <= 2^29 (A stays exact); G <= 1024.
   int nev = 0;
+  // the first coarse window holds the task triangle and every POV's nearest
+  // targets, where almost no window is hidden: no skip tests there
+  const int ktest = ymin + SKS_NEAR_NOTEST;
   while (k0 <= klast) {
-    if (!kVis && k0 + kH - 1 <= kmain) {
+    if (!kVis && k0 >= ktest && k0 + kH - 1 <= kmain) {
       const float2 em = lds64(w64a + (static_cast<unsigned>(k0) >> 3));
       if (window_hidden<kHl>(P, em, rb0, k0, kH)) {
         k0 += kH;
@@ -353,7 +359,7 @@ __device__ void run_task(const ScanArgs& a, const Layout2& lay, const Slot& sl, 
     }
     const int kc = k0 + kH;
     while (k0 < kc && k0 <= klast && k0 + kW - 1 <= kmain) {
-      if (!kVis) {
+      if (!kVis && k0 >= ktest) {
         const float2 em = lds64(w16a + 8u * (static_cast<unsigned>(k0) / kW));
         if (window_hidden<kHl>(P, em, rb0, k0, kW)) {
           k0 += kW;
