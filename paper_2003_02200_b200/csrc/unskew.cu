@@ -9,8 +9,8 @@
 // adds the interpolated value. All FP64 operations are explicit _rn
 // intrinsics in the reference's order, so the per-cell sum is bit-identical
 // to total_viewshed_raw when sectors are accumulated on one GPU.
-// HBM roofline: per sector ~4-8 B of cv gathered + 16 B of map RMW per cell
-// (the map RMW is amortised over the whole batch: 16 B per cell per batch).
+// HBM roofline: per sector ~8 B of cv gathered per cell (the cv block a tile
+// needs, staged by unskew_tiled_kernel) + 16 B of map RMW per cell per batch.
 #include <cuda_runtime.h>
 
 #include "sks_device.cuh"
@@ -71,6 +71,90 @@ __global__ void __launch_bounds__(256) unskew_kernel(BatchDev b, const double* _
   map[idx] = acc;
 }
 
+// Tiled form of unskew_kernel<true> (same per-cell arithmetic, same
+// ascending-k order). A CTA owns a 32x32 tile of DEM cells (each thread 4
+// cells of one column); per sector it stages the block of cv rows the tile
+// gathers from (<= 66 rows x 32 columns, loaded along j, i.e. coalesced for
+// transposed sectors too) plus the tile's dest/frac columns in shared
+// memory, then every cell reads its two values from there.
+constexpr int kUT = 32;           // tile edge (cells)
+constexpr int kUR = 2 * kUT + 2;  // cv rows a tile can touch (shear <= 45 deg)
+
+__global__ void __launch_bounds__(256) unskew_tiled_kernel(BatchDev b, double* __restrict__ map,
+                                                           int dimy, int dimx) {
+  __shared__ int scv[kUR][kUT + 1];
+  __shared__ int sdest[kUT];
+  __shared__ double sfrac[kUT];
+  const int tx = threadIdx.x & 31;
+  const int ty = threadIdx.x >> 5;  // 0..7
+  const int y0 = blockIdx.y * kUT, x0 = blockIdx.x * kUT;
+  const int ye = min(dimy, y0 + kUT) - 1, xe = min(dimx, x0 + kUT) - 1;  // last cell of the tile
+  const int sj = x0 + tx;
+  double acc[4];
+#pragma unroll
+  for (int u = 0; u < 4; ++u) {
+    const int si = y0 + ty + 8 * u;
+    acc[u] = (si < dimy && sj < dimx) ? map[static_cast<long long>(si) * dimx + sj] : 0.0;
+  }
+  for (int s = 0; s < b.n_sectors; ++s) {
+    const SectorDev& sd = b.sectors[s];
+    const int* iv = sd.inv;
+    // pre_ops ranges of the tile: the affine maps are axis permutations/flips,
+    // so the extremes are at the corners
+    const int ia = iv[0] * y0 + iv[1] * x0 + iv[2], ib = iv[0] * ye + iv[1] * xe + iv[2];
+    const int ja = iv[3] * y0 + iv[4] * x0 + iv[5], jb = iv[3] * ye + iv[4] * xe + iv[5];
+    const int i_lo = min(ia, ib), i_hi = max(ia, ib);
+    const int j_lo = min(ja, jb), j_hi = max(ja, jb);
+    const int nj = j_hi - j_lo + 1;
+    const int* dest = b.dest + sd.col_off;
+    const int d_lo = __ldg(dest + j_lo), d_hi = __ldg(dest + j_hi);
+    const int p_lo = sd.base + i_lo - d_hi - 1;  // includes the p-1 rows
+    const int np = sd.base + i_hi - d_lo - p_lo + 1;
+    __syncthreads();  // previous sector's smem reads are done
+    if (threadIdx.x < nj) {
+      sdest[threadIdx.x] = __ldg(dest + j_lo + threadIdx.x);
+      sfrac[threadIdx.x] = __ldg(b.fracd + sd.col_off + j_lo + threadIdx.x);
+    }
+    const int* cvb = b.cv + sd.sdem_off + static_cast<long long>(p_lo) * sd.pitch + j_lo;
+    for (int r = ty; r < np; r += 8) {
+      if (tx < nj) scv[r][tx] = __ldg(cvb + static_cast<long long>(r) * sd.pitch + tx);
+    }
+    __syncthreads();
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      const int si = y0 + ty + 8 * u;
+      if (si >= dimy || sj >= dimx) continue;
+      const int i = iv[0] * si + iv[1] * sj + iv[2];
+      const int j = iv[3] * si + iv[4] * sj + iv[5];
+      const int jl = j - j_lo;
+      const int p = sd.base + i - sdest[jl];
+      const double r = sfrac[jl];
+      const double omr = __dsub_rn(1.0, r);
+      const double w_p = (i + 1 < sd.rows) ? __dadd_rn(omr, r) : omr;
+      const double w_m = (i >= 1) ? __dadd_rn(omr, r) : r;
+      const bool a = full_d(w_p);
+      const bool c = full_d(w_m);
+      double va = 0.0, vb = 0.0;
+      if (a) va = __dmul_rn(static_cast<double>(scv[p - p_lo][jl]), sd.correction);
+      if (!a || c) vb = __dmul_rn(static_cast<double>(scv[p - 1 - p_lo][jl]), sd.correction);
+      double v;
+      if (a && c) {
+        v = __dadd_rn(__dmul_rn(omr, va), __dmul_rn(r, vb));
+      } else if (a) {
+        v = va;
+      } else {
+        v = vb;
+      }
+      acc[u] = __dadd_rn(acc[u], v);
+    }
+  }
+#pragma unroll
+  for (int u = 0; u < 4; ++u) {
+    const int si = y0 + ty + 8 * u;
+    if (si < dimy && sj < dimx) map[static_cast<long long>(si) * dimx + sj] = acc[u];
+  }
+}
+
 __global__ void scale_kernel(double* map, long long n, double factor) {
   const long long i = static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x;
   if (i < n) map[i] = __dmul_rn(map[i], factor);
@@ -90,11 +174,8 @@ __global__ void cv_to_vs_kernel(const int* cvf, const int* cvb, double* out, lon
 
 int launch_unskew(const BatchDev& b, const float*, double* map, int dimy, int dimx,
                   void* stream) {
-  const long long n = static_cast<long long>(dimy) * dimx;
-  const int threads = 256;
-  const unsigned grid = static_cast<unsigned>((n + threads - 1) / threads);
-  unskew_kernel<true><<<grid, threads, 0, static_cast<cudaStream_t>(stream)>>>(b, nullptr, map,
-                                                                               dimy, dimx);
+  dim3 grid((dimx + kUT - 1) / kUT, (dimy + kUT - 1) / kUT);
+  unskew_tiled_kernel<<<grid, 256, 0, static_cast<cudaStream_t>(stream)>>>(b, map, dimy, dimx);
   return static_cast<int>(cudaGetLastError());
 }
 
