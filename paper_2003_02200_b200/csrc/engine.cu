@@ -255,7 +255,8 @@ struct sks_context {
   std::map<std::tuple<int, int, int, double, double, std::vector<int>>, std::unique_ptr<Plans>>
       cache;
   // work buffers
-  DevBuf sdem, cv, cvb, queue, fixcnt, wm16, counters, dem, map, vis;
+  DevBuf sdem, cv, cvb, queue, fixcnt, wm16, counters, dem, map, vis, check;
+  unsigned long long* h_check = nullptr;  // pinned: device DEM scan result
   cudaEvent_t ev[8] = {};
   long long launches = 0;
 
@@ -360,6 +361,7 @@ struct sks_context {
       if (e) cudaEventDestroy(e);
     }
     if (own_stream) cudaStreamDestroy(own_stream);
+    if (h_check) cudaFreeHost(h_check);
   }
 };
 
@@ -496,20 +498,49 @@ void run_sectors(sks_context* ctx, const float* d_dem, int dimy, int dimx, doubl
 void total_host(sks_context* ctx, const float* dem, int dimy, int dimx, double cellsize,
                 const sks_run_config* cfg, int raw, double* out, sks_stats* stats) {
   auto t0 = std::chrono::steady_clock::now();
-  require_valid(dem, dimy, dimx, cellsize, cfg);
+  if (!cfg) throw std::invalid_argument("null run config");
+  if (!dem) throw std::invalid_argument("null DEM");
   if (!out) throw std::invalid_argument("null output");
+  // validate(Dem) then validate(RunConfig) (engine.cpp:68-81), in the
+  // reference's order; the O(N) cell scan runs on device after the upload
+  std::string err = validate_grid_header(dimy, dimx, cellsize);
+  if (!err.empty()) throw std::invalid_argument(err);
   ctx->activate();
   std::lock_guard<std::mutex> lk(ctx->mu);
   const size_t n = static_cast<size_t>(dimy) * dimx;
-  const bool exact = !filter_preconditions_hold(dem, n, cfg->h0);
   cudaStream_t st = ctx->own_stream;
   ctx->dem.ensure(n * sizeof(float), ctx->device);
   ctx->map.ensure(n * sizeof(double), ctx->device);
+  ctx->check.ensure(2 * sizeof(unsigned long long), ctx->device);
+  if (ctx->h_check == nullptr) {
+    cuda_check(cudaHostAlloc(reinterpret_cast<void**>(&ctx->h_check), 2 * sizeof(unsigned long long),
+                             cudaHostAllocDefault),
+               "pinned check");
+  }
   cuda_check(cudaMemcpyAsync(ctx->dem.p, dem, n * sizeof(float), cudaMemcpyHostToDevice, st), "H2D dem");
+  cuda_check(cudaMemsetAsync(ctx->check.p, 0xff, sizeof(unsigned long long), st), "memset check");
+  cuda_check(cudaMemsetAsync(static_cast<char*>(ctx->check.p) + 8, 0, sizeof(unsigned long long), st),
+             "memset check");
+  cuda_check(launch_dem_check(ctx->dem.as<float>(), static_cast<long long>(n),
+                              ctx->check.as<unsigned long long>(), st),
+             "launch dem check");
+  ++ctx->launches;
+  cuda_check(cudaMemcpyAsync(ctx->h_check, ctx->check.p, 2 * sizeof(unsigned long long),
+                             cudaMemcpyDeviceToHost, st),
+             "D2H check");
+  cuda_check(cudaStreamSynchronize(st), "sync check");
+  if (ctx->h_check[0] != ~0ull) {
+    throw std::invalid_argument(nonfinite_message(static_cast<long long>(ctx->h_check[0]), dimx));
+  }
+  err = validate_config(cfg->ns, cfg->h0, cfg->max_distance);
+  if (!err.empty()) throw std::invalid_argument(err);
+  const double plo = std::ldexp(1.0, -40), phi = std::ldexp(1.0, 40);
+  const bool exact = ctx->h_check[1] != 0 || (cfg->h0 != 0.0 && (cfg->h0 < plo || cfg->h0 > phi));
   cuda_check(cudaMemsetAsync(ctx->map.p, 0, n * sizeof(double), st), "memset map");
   std::vector<int> all(cfg->ns / 2);
   std::iota(all.begin(), all.end(), 0);
   sks_stats local{};
+  local.kernel_launches += 1;  // dem_check
   run_sectors(ctx, ctx->dem.as<float>(), dimy, dimx, cellsize, cfg, all, ctx->map.as<double>(), st,
               stats ? &local : nullptr, exact);
   if (!raw) {

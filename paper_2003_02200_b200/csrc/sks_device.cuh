@@ -102,6 +102,7 @@ int launch_unskew(const BatchDev& b, const float* unused, double* map,
 int launch_unskew_from_vs(const BatchDev& b, const double* skw_vs,
                           double* map, int dimy, int dimx, void* stream);
 int launch_scale(double* map, long long n, double factor, void* stream);
+int launch_dem_check(const float* dem, long long n, unsigned long long* res, void* stream);
 int launch_cv_to_vs(const int* cvf, const int* cvb, double* out,
                     long long n, double correction, void* stream);
 

@@ -389,9 +389,7 @@ void make_synthetic(int kind, int dimy, int dimx, uint32_t seed, float* out) {
   }
 }
 
-std::string validate_inputs(const float* dem, int dimy, int dimx,
-                            double cellsize, const float* nodata, int ns,
-                            double h0, double max_distance) {
+std::string validate_grid_header(int dimy, int dimx, double cellsize) {
   std::ostringstream os;
   if (dimy < 2 || dimx < 2) {
     os << "invalid grid: grid must be at least 2x2, got " << dimy << "x" << dimx;
@@ -401,24 +399,17 @@ std::string validate_inputs(const float* dem, int dimy, int dimx,
     os << "invalid grid: cellsize must be a positive finite number, got " << cellsize;
     return os.str();
   }
-  for (int i = 0; i < dimy; ++i) {
-    for (int j = 0; j < dimx; ++j) {
-      float v = dem[static_cast<size_t>(i) * dimx + j];
-      if (nodata && v == *nodata) continue;
-      if (!std::isfinite(v)) {
-        os << "invalid grid: non-finite elevation at cell (" << i << ", " << j << ")";
-        return os.str();
-      }
-    }
-  }
-  if (nodata) {
-    size_t n = static_cast<size_t>(dimy) * dimx;
-    for (size_t i = 0; i < n; ++i) {
-      if (dem[i] == *nodata) {
-        return "grid contains nodata cells; fill them before running the engine";
-      }
-    }
-  }
+  return "";
+}
+
+std::string nonfinite_message(long long idx, int dimx) {
+  std::ostringstream os;
+  os << "invalid grid: non-finite elevation at cell (" << idx / dimx << ", " << idx % dimx << ")";
+  return os.str();
+}
+
+std::string validate_config(int ns, double h0, double max_distance) {
+  std::ostringstream os;
   if (ns < 2 || ns % 2 != 0) {
     os << "invalid config: ns must be an even integer >= 2, got " << ns;
     return os.str();
@@ -432,6 +423,27 @@ std::string validate_inputs(const float* dem, int dimy, int dimx,
     return os.str();
   }
   return "";
+}
+
+std::string validate_inputs(const float* dem, int dimy, int dimx,
+                            double cellsize, const float* nodata, int ns,
+                            double h0, double max_distance) {
+  std::string e = validate_grid_header(dimy, dimx, cellsize);
+  if (!e.empty()) return e;
+  const size_t n = static_cast<size_t>(dimy) * dimx;
+  for (size_t i = 0; i < n; ++i) {
+    const float v = dem[i];
+    if (nodata && v == *nodata) continue;
+    if (!std::isfinite(v)) return nonfinite_message(static_cast<long long>(i), dimx);
+  }
+  if (nodata) {
+    for (size_t i = 0; i < n; ++i) {
+      if (dem[i] == *nodata) {
+        return "grid contains nodata cells; fill them before running the engine";
+      }
+    }
+  }
+  return validate_config(ns, h0, max_distance);
 }
 
 }  // namespace sks

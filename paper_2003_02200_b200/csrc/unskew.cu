@@ -155,6 +155,23 @@ __global__ void __launch_bounds__(256) unskew_tiled_kernel(BatchDev b, double* _
   }
 }
 
+// Input scan of the DEM on device (total_host): res[0] = first non-finite
+// cell index (row-major, as validate(Dem) reports it, dem.cpp:36-60), res[1]
+// != 0 if a nonzero |e| lies outside the FP32 filter's proven range
+// [2^-40, 2^40]. res = {ULLONG_MAX, 0} before launch.
+__global__ void dem_check_kernel(const float* __restrict__ dem, long long n,
+                                 unsigned long long* res) {
+  const long long stride = static_cast<long long>(gridDim.x) * blockDim.x;
+  bool oor = false;
+  for (long long i = static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x; i < n; i += stride) {
+    const float v = __ldg(dem + i);
+    if (!isfinite(v)) atomicMin(res, static_cast<unsigned long long>(i));
+    const float a = fabsf(v);
+    if (a != 0.f && (a < 0x1p-40f || a > 0x1p40f)) oor = true;
+  }
+  if (__any_sync(0xffffffffu, oor) && (threadIdx.x & 31) == 0) res[1] = 1ull;
+}
+
 __global__ void scale_kernel(double* map, long long n, double factor) {
   const long long i = static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x;
   if (i < n) map[i] = __dmul_rn(map[i], factor);
@@ -186,6 +203,15 @@ int launch_unskew_from_vs(const BatchDev& b, const double* skw_vs, double* map, 
   const unsigned grid = static_cast<unsigned>((n + threads - 1) / threads);
   unskew_kernel<false><<<grid, threads, 0, static_cast<cudaStream_t>(stream)>>>(b, skw_vs, map,
                                                                                 dimy, dimx);
+  return static_cast<int>(cudaGetLastError());
+}
+
+int launch_dem_check(const float* dem, long long n, unsigned long long* res, void* stream) {
+  const int threads = 256;
+  long long blocks = (n + threads * 8 - 1) / (threads * 8);
+  if (blocks < 1) blocks = 1;
+  if (blocks > 4096) blocks = 4096;
+  dem_check_kernel<<<static_cast<unsigned>(blocks), threads, 0, static_cast<cudaStream_t>(stream)>>>(dem, n, res);
   return static_cast<int>(cudaGetLastError());
 }
 
