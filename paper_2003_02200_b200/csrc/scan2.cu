@@ -69,31 +69,33 @@ constexpr int kSumShift = 22;
 constexpr int kSumMask = (1 << kSumShift) - 1;
 
 struct Layout2 {
+  int nc;     // fl(1/dd) table copies: 4 (quad loads) or 2 (pair loads, long rows)
   int lb;     // row buffer (floats) per direction
   int nw16, nw64;
   int T;      // table length per copy (floats, a multiple of 32)
-  int TB;     // reversed bound table length
   int slot;   // floats per slot
   int ctl;    // floats of control blocks
-  int tables; // offset of the 4 table copies
-  int rb;     // offset of the reversed bound table
+  int tables; // offset of the table copies
   int slots;  // offset of slot 0
-  __host__ __device__ Layout2(int lmax) {
+  __host__ __device__ Layout2(int lmax, int ncopies) {
+    nc = ncopies;
     lb = ((lmax + 64 + 63) / 64) * 64;
     nw16 = lb / kW;
     nw64 = lb / 64;
     T = ((kOff + lb + 16 + 31) / 32) * 32;
-    TB = ((lb + 80 + 3) / 4) * 4;
     slot = 2 * lb + 4 * nw16 + 4 * nw64;
     ctl = kMaxSlots * kCtlInts;
     tables = ctl;
-    rb = tables + 4 * T + 32;
-    slots = rb + TB;
+    slots = tables + nc * T + 32;
   }
-  // Copy r starts at r*T plus a bank offset (in quads: 0, 0, 5, 4) so that
-  // the two copies one LDS.128 reads (0/2 for the first POV of even/odd
-  // lanes, 3/1 for the second) hit disjoint banks in every quarter-warp.
-  __host__ __device__ int copy(int r) const { return tables + r * T + 4 * ((0x4500 >> (4 * r)) & 15); }
+  // Copy r (IV_r[i] = fl(1/(i - kOff + r))) starts at r*T plus, with 4
+  // copies, a bank offset (in quads: 0, 0, 5, 4) so that the two copies one
+  // LDS.128 reads (0/2 for the first POV of even/odd lanes, 3/1 for the
+  // second) hit disjoint banks in every quarter-warp. With 2 copies the
+  // first POV of every lane reads copy 0 and the second copy 1.
+  __host__ __device__ int copy(int r) const {
+    return tables + r * T + (nc == 4 ? 4 * ((0x4500 >> (4 * r)) & 15) : 0);
+  }
   __host__ __device__ int total(int nslots) const { return slots + nslots * slot; }
 };
 
@@ -256,32 +258,42 @@ __device__ __forceinline__ bool step_vis(float t, float& hi, float& lo, int& A, 
   return pa;
 }
 
-// Skip test for window [k0, k0 + w): see the file header. rb0 addresses
-// RB[C - (k0 - y0)] for k0 = 0; the pair there is (1/dl0, 1/dl1) (both POVs'
-// smallest dd, clamped to 1) and w floats lower (1/(dl0 + w), 1/(dl1 + w)),
-// one past each POV's largest dd, still a bound because fl(1/d) is monotone.
+// Skip test for window [k0, k0 + w): see the file header. tb addresses
+// table copy 1 so that the pair at tb + 4*k0 is (fl(1/dl1), fl(1/dl0)) —
+// both POVs' smallest dd, the second POV first — and the pair w floats on
+// is (fl(1/(dh1 + 1)), fl(1/(dh0 + 1))), one past each POV's largest dd
+// (still a bound: fl(1/d) is monotone); the N pair is ordered to match. A
+// dd <= 0 reads NaN and fails the test (never skipped: conservative).
 // Absent POVs have hf = +inf, so N = -inf and they never block a skip.
 template <bool kHl>
-__device__ __forceinline__ bool window_hidden(const Pov2& P, float2 em2, unsigned rb0, int k0, int w) {
-  float2 N = __fadd2_rn(em2, make_float2(-P.hf0, -P.hf1));
-  if (kHl) N = __fadd2_rn(N, make_float2(-P.hl0, -P.hl1));
-  const unsigned ra = rb0 - 4u * static_cast<unsigned>(k0);
+__device__ __forceinline__ bool window_hidden(const Pov2& P, float2 em2, unsigned tb, int k0, int w) {
+  float2 N = __fadd2_rn(em2, make_float2(-P.hf1, -P.hf0));
+  if (kHl) N = __fadd2_rn(N, make_float2(-P.hl1, -P.hl0));
+  const unsigned ra = tb + 4u * static_cast<unsigned>(k0);
   const float2 b1 = __fmul2_rn(N, lds64(ra));
-  const float2 b2 = __fmul2_rn(N, lds64(ra - 4u * static_cast<unsigned>(w)));
-  const bool ok = (b1.x < P.lo0) & (b2.x < P.lo0) & (b1.y < P.lo1) & (b2.y < P.lo1);
+  const float2 b2 = __fmul2_rn(N, lds64(ra + 4u * static_cast<unsigned>(w)));
+  const bool ok = (b1.x < P.lo1) & (b2.x < P.lo1) & (b1.y < P.lo0) & (b2.y < P.lo0);
   return __all_sync(0xffffffffu, ok);
 }
 
 // Evaluates targets k0 .. k0+kW-1 for both POVs.
-template <bool kHl, bool kVis>
+template <bool kHl, bool kVis, int kNC>
 __device__ __forceinline__ void eval16(Pov2& P, unsigned sb, unsigned ivb0, unsigned ivb1, int k0,
                                        int vis_p, uint8_t* vis, int vis_D) {
 #pragma unroll
   for (int g = 0; g < kW / 4; ++g) {
     const int k = k0 + 4 * g;
     const float4 e = lds128(sb + 4 * k);
-    const float4 q0 = lds128(ivb0 + 4 * k);
-    const float4 q1 = lds128(ivb1 + 4 * k);
+    float4 q0, q1;
+    if (kNC == 4) {
+      q0 = lds128(ivb0 + 4 * k);
+      q1 = lds128(ivb1 + 4 * k);
+    } else {
+      const float2 a0 = lds64(ivb0 + 4 * k), b0 = lds64(ivb0 + 4 * k + 8);
+      const float2 a1 = lds64(ivb1 + 4 * k), b1 = lds64(ivb1 + 4 * k + 8);
+      q0 = make_float4(a0.x, a0.y, b0.x, b0.y);
+      q1 = make_float4(a1.x, a1.y, b1.x, b1.y);
+    }
     float2 n0a = __fadd2_rn(make_float2(e.x, e.y), make_float2(-P.hf0, -P.hf0));
     float2 n0b = __fadd2_rn(make_float2(e.z, e.w), make_float2(-P.hf0, -P.hf0));
     float2 n1a = __fadd2_rn(make_float2(e.x, e.y), make_float2(-P.hf1, -P.hf1));
@@ -318,7 +330,7 @@ __device__ __forceinline__ void eval16(Pov2& P, unsigned sb, unsigned ivb0, unsi
   }
 }
 
-template <bool kHl, bool kVis>
+template <bool kHl, bool kVis, int kNC>
 __device__ void run_task(const ScanArgs& a, const Layout2& lay, const Slot& sl, const float* IV,
                          int dir, int chunk, int L, int cap, Pov2& P, int vis_p, uint8_t* vis,
                          int vis_D, unsigned long long& skipped) {
@@ -326,10 +338,12 @@ __device__ void run_task(const ScanArgs& a, const Layout2& lay, const Slot& sl, 
   const float2* W16 = dir ? sl.WR16 : sl.WS16;
   const float2* W64 = dir ? sl.WR64 : sl.WS64;
   const unsigned sb = smem_u32(B);
-  const unsigned rb0 = smem_u32(IV + lay.rb) + 4u * static_cast<unsigned>(lay.lb + P.y0);
-  // per POV: the table copy r with (k - y - r) % 4 == 0 for k % 4 == 0
+  // copy 1 holds fl(1/d) at element d + kOff - 1 (window tests, pair loads)
+  const unsigned tb = smem_u32(IV + lay.copy(1)) + 4u * static_cast<unsigned>(kOff - 2 - P.y0);
+  // per POV: the table copy r with (k - y - r) % kNC == 0 for k % 4 == 0
+  // (y0 is even: with 2 copies the first POV reads copy 0, the second copy 1)
   const int y1 = P.y0 + 1;
-  const int r0 = (-P.y0) & 3, r1 = (-y1) & 3;
+  const int r0 = (-P.y0) & (kNC - 1), r1 = (-y1) & (kNC - 1);
   const unsigned ivb0 = smem_u32(IV + lay.copy(r0)) + 4u * static_cast<unsigned>(kOff - r0 - P.y0);
   const unsigned ivb1 = smem_u32(IV + lay.copy(r1)) + 4u * static_cast<unsigned>(kOff - r1 - y1);
   const unsigned w16a = smem_u32(W16), w64a = smem_u32(W64);
@@ -351,7 +365,7 @@ __device__ void run_task(const ScanArgs& a, const Layout2& lay, const Slot& sl, 
   while (k0 <= klast) {
     if (!kVis && k0 >= ktest && k0 + kH - 1 <= kmain) {
       const float2 em = lds64(w64a + (static_cast<unsigned>(k0) >> 3));
-      if (window_hidden<kHl>(P, em, rb0, k0, kH)) {
+      if (window_hidden<kHl>(P, em, tb, k0, kH)) {
         k0 += kH;
         nskip += kH;
         continue;
@@ -361,13 +375,13 @@ __device__ void run_task(const ScanArgs& a, const Layout2& lay, const Slot& sl, 
     while (k0 < kc && k0 <= klast && k0 + kW - 1 <= kmain) {
       if (!kVis && k0 >= ktest) {
         const float2 em = lds64(w16a + 8u * (static_cast<unsigned>(k0) / kW));
-        if (window_hidden<kHl>(P, em, rb0, k0, kW)) {
+        if (window_hidden<kHl>(P, em, tb, k0, kW)) {
           k0 += kW;
           nskip += kW;
           continue;
         }
       }
-      eval16<kHl, kVis>(P, sb, ivb0, ivb1, k0, vis_p, vis, vis_D);
+      eval16<kHl, kVis, kNC>(P, sb, ivb0, ivb1, k0, vis_p, vis, vis_D);
       if (++nev == 32) {
         flush(P);
         nev = 0;
@@ -408,10 +422,10 @@ __device__ void run_task(const ScanArgs& a, const Layout2& lay, const Slot& sl, 
   skipped += nskip;
 }
 
-template <int kThr>
+template <int kThr, int kNC>
 __global__ void __launch_bounds__(kThr, 1) scan2_kernel(ScanArgs a, int nslots, int lmax) {
   extern __shared__ __align__(16) float smem[];
-  const Layout2 lay(lmax);
+  const Layout2 lay(lmax, kNC);
   int* ctl_all = reinterpret_cast<int*>(smem);
   float* IV = smem;  // table copies at lay.copy(r)
   float* slots = smem + lay.slots;
@@ -422,15 +436,10 @@ __global__ void __launch_bounds__(kThr, 1) scan2_kernel(ScanArgs a, int nslots, 
   // fl(1/d) tables, 4 copies shifted by r: IV[r][i] = fl(1/(i - kOff + r)),
   // NaN for d <= 0 (a no-op target: every comparison is false)
   const float qnan = __int_as_float(0x7fc00000);
-  for (int i = tid; i < 4 * lay.T; i += blockDim.x) {
+  for (int i = tid; i < kNC * lay.T; i += blockDim.x) {
     const int r = i / lay.T, j = i - r * lay.T;
     const int d = j - kOff + r;
     smem[lay.copy(r) + j] = d >= 1 ? __frcp_rn(static_cast<float>(d)) : qnan;
-  }
-  // reversed bound table RB[m] = fl(1/max(C - m, 1)), C = lb (window bounds:
-  // targets with dd <= 0 are no-ops, so dd is clamped to 1)
-  for (int m = tid; m < lay.TB; m += blockDim.x) {
-    smem[lay.rb + m] = __frcp_rn(static_cast<float>(max(lay.lb - m, 1)));
   }
   for (int i = tid; i < kMaxSlots * kCtlInts; i += blockDim.x) ctl_all[i] = 0;
   __syncthreads();
@@ -529,14 +538,14 @@ __global__ void __launch_bounds__(kThr, 1) scan2_kernel(ScanArgs a, int nslots, 
     const bool any_hl = __any_sync(0xffffffffu, P.hl0 != 0.f || P.hl1 != 0.f);
     if (vis_mode) {
       if (any_hl) {
-        run_task<true, true>(a, lay, sp, IV, dir, chunk, L, cap, P, vis ? vis_p : -1, vis, vis_D, skipped);
+        run_task<true, true, kNC>(a, lay, sp, IV, dir, chunk, L, cap, P, vis ? vis_p : -1, vis, vis_D, skipped);
       } else {
-        run_task<false, true>(a, lay, sp, IV, dir, chunk, L, cap, P, vis ? vis_p : -1, vis, vis_D, skipped);
+        run_task<false, true, kNC>(a, lay, sp, IV, dir, chunk, L, cap, P, vis ? vis_p : -1, vis, vis_D, skipped);
       }
     } else if (any_hl) {
-      run_task<true, false>(a, lay, sp, IV, dir, chunk, L, cap, P, -1, nullptr, 0, skipped);
+      run_task<true, false, kNC>(a, lay, sp, IV, dir, chunk, L, cap, P, -1, nullptr, 0, skipped);
     } else {
-      run_task<false, false>(a, lay, sp, IV, dir, chunk, L, cap, P, -1, nullptr, 0, skipped);
+      run_task<false, false, kNC>(a, lay, sp, IV, dir, chunk, L, cap, P, -1, nullptr, 0, skipped);
     }
 
     {
@@ -572,30 +581,45 @@ __global__ void __launch_bounds__(kThr, 1) scan2_kernel(ScanArgs a, int nslots, 
 
 }  // namespace
 
-// Slots that fit the opt-in shared memory for rows up to lmax (0: use the
-// distance-lockstep kernel of scan.cu instead).
-int scan2_slots(int lmax) {
-  const Layout2 lay(lmax);
+// Table copies and slots that fit the opt-in shared memory for rows up to
+// lmax: 4 copies with >= 2 slots (rows up to ~5 800 cells), else 2 copies
+// with >= 1 slot (rows up to ~13 000 cells); 0 slots: use the
+// distance-lockstep kernel of scan.cu instead.
+static void scan2_config(int lmax, int* copies, int* slots) {
+  *copies = 0;
+  *slots = 0;
+  if (lmax >= 32768 - 128) return;  // k < 2^15 keeps the flush sums exact
   const long long cap = 227 * 1024;
-  const long long fixed = 4LL * lay.slots;
-  const long long per = 4LL * lay.slot;
-  if (lmax >= 32768 - 128) return 0;  // k < 2^15 keeps the flush sums exact
-  long long n = (cap - fixed) / per;
-  if (n < 2) return 0;
-  return static_cast<int>(n > kMaxSlots ? kMaxSlots : n);
+  for (int nc : {4, 2}) {
+    const Layout2 lay(lmax, nc);
+    const long long n = (cap - 4LL * lay.slots) / (4LL * lay.slot);
+    if (n >= (nc == 4 ? 2 : 1)) {
+      *copies = nc;
+      *slots = static_cast<int>(n > kMaxSlots ? kMaxSlots : n);
+      return;
+    }
+  }
+}
+
+int scan2_slots(int lmax) {
+  int c = 0, n = 0;
+  scan2_config(lmax, &c, &n);
+  return n;
 }
 
 size_t scan2_smem_bytes(int lmax, int nslots) {
-  return static_cast<size_t>(Layout2(lmax).total(nslots)) * sizeof(float);
+  int c = 0, n = 0;
+  scan2_config(lmax, &c, &n);
+  return static_cast<size_t>(Layout2(lmax, c > 0 ? c : 4).total(nslots)) * sizeof(float);
 }
 
-template <int kThr>
+template <int kThr, int kNC>
 static int launch_scan2_t(const ScanArgs& a, int nslots, int sms, cudaStream_t st) {
-  const size_t smem = scan2_smem_bytes(a.lmax, nslots);
-  cudaError_t e = cudaFuncSetAttribute(scan2_kernel<kThr>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                       static_cast<int>(smem));
+  const size_t smem = static_cast<size_t>(Layout2(a.lmax, kNC).total(nslots)) * sizeof(float);
+  cudaError_t e = cudaFuncSetAttribute(scan2_kernel<kThr, kNC>,
+                                       cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
   if (e != cudaSuccess) return static_cast<int>(e);
-  scan2_kernel<kThr><<<sms, kThr, smem, st>>>(a, nslots, a.lmax);
+  scan2_kernel<kThr, kNC><<<sms, kThr, smem, st>>>(a, nslots, a.lmax);
   return static_cast<int>(cudaGetLastError());
 }
 
@@ -604,15 +628,12 @@ int launch_scan2(const ScanArgs& a, int nslots, void* stream) {
   cudaGetDevice(&dev);
   int sms = 0;
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-  // CTA size (experiments): SKS_SCAN2_THREADS = 512, 768 (default) or 1024
-  static const int thr = [] {
-    const char* s = std::getenv("SKS_SCAN2_THREADS");
-    return s != nullptr ? std::atoi(s) : kThreads;
-  }();
+  int copies = 0, fit = 0;
+  scan2_config(a.lmax, &copies, &fit);
+  if (copies == 0 || nslots < 1 || nslots > fit) return static_cast<int>(cudaErrorInvalidValue);
   cudaStream_t st = static_cast<cudaStream_t>(stream);
-  if (thr == 1024) return launch_scan2_t<1024>(a, nslots, sms, st);
-  if (thr == 512) return launch_scan2_t<512>(a, nslots, sms, st);
-  return launch_scan2_t<kThreads>(a, nslots, sms, st);
+  return copies == 4 ? launch_scan2_t<kThreads, 4>(a, nslots, sms, st)
+                     : launch_scan2_t<kThreads, 2>(a, nslots, sms, st);
 }
 
 }  // namespace sks

@@ -133,6 +133,22 @@ def test_scan_long_rows_sampled_pov_parity(ora):
                 assert cvf[q, j0] == f and cvb[q, j0] == b, (k, q, j0)
 
 
+def test_scan_very_long_rows_two_copy_tables(ora):
+    """Rows of 7000 cells: beyond the 4-copy table layout, scan2 runs with 2
+    fl(1/dd) copies (pair loads) and one row slot (config 5 path). Every POV
+    of every row, both directions, against the reference, capped and not."""
+    L = 7000
+    dem = sk.make_synthetic(sk.SyntheticKind.Fractal, 6, L, 10.0, 21).values
+    vals = np.ascontiguousarray(dem, np.float32)
+    rr = np.zeros((6, 2), np.int32)
+    rr[:, 1] = L
+    rr[3] = (5, L - 7)  # a ragged row
+    for max_dd in (NO_CAP, 3001):
+        ref = ora.sector_viewshed(vals, rr, 6, 0, 0.0, 1.5, max_dd)
+        ours = sk.sector_viewshed(sk.SkwGrid(vals, rr, 0, 6, 0.0), 1.5, max_dd)
+        assert np.array_equal(b64(ours), b64(ref)), max_dd
+
+
 def test_visibility_vectors(ora):
     rng = np.random.default_rng(7)
     for trial in range(60):
