@@ -325,9 +325,14 @@ struct sks_context {
   }
 
   // scan + fixup of one batch whose sDEM is already in the pool
-  void scan_batch(const Batch& b, const ScanArgs& a, cudaStream_t st, bool split_bwd) {
-    cuda_check(cudaMemsetAsync(cv.p, 0, static_cast<size_t>(b.pool_elems) * sizeof(int), st),
-               "memset cv");
+  // zero_cv: the cv pool must be cleared here (debug paths that upload an
+  // sDEM directly); after relocate_kernel it already is (the kernel zeroes
+  // the cv cells of every tile it writes).
+  void scan_batch(const Batch& b, const ScanArgs& a, cudaStream_t st, bool split_bwd, bool zero_cv) {
+    if (zero_cv) {
+      cuda_check(cudaMemsetAsync(cv.p, 0, static_cast<size_t>(b.pool_elems) * sizeof(int), st),
+                 "memset cv");
+    }
     if (split_bwd) {
       cuda_check(cudaMemsetAsync(cvb.p, 0, static_cast<size_t>(b.pool_elems) * sizeof(int), st),
                  "memset cvb");
@@ -436,7 +441,7 @@ void run_sectors(sks_context* ctx, const float* d_dem, int dimy, int dimx, doubl
     cuda_check(launch_relocate_grid(d_dem, bd, b.tiles_x, b.tiles_total, st), "launch relocate");
     ++ctx->launches;
     if (stats) cuda_check(cudaEventRecord(ctx->ev[1], st), "event");
-    ctx->scan_batch(b, a, st, false);
+    ctx->scan_batch(b, a, st, false, false);
     if (stats) cuda_check(cudaEventRecord(ctx->ev[2], st), "event");
     ctx->fixup_batch(a, st);
     if (stats) cuda_check(cudaEventRecord(ctx->ev[3], st), "event");
@@ -873,7 +878,7 @@ void debug_scan(sks_context* ctx, const float* values, const int* ranges, int sk
       a.dbg_vis_bwd = dvis + std::max(vis_len, 1);
     }
   }
-  ctx->scan_batch(*b, a, st, true);
+  ctx->scan_batch(*b, a, st, true, true);
   ctx->fixup_batch(a, st);
   cvf.assign(static_cast<size_t>(skw_rows) * cols, 0);
   cvb.assign(static_cast<size_t>(skw_rows) * cols, 0);

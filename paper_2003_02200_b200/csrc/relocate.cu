@@ -87,33 +87,49 @@ relocate_kernel(const float* __restrict__ dem, BatchDev b, int tiles_x) {
   }
   __syncthreads();
 
+  // Output: a thread owns 4 consecutive columns x 4 consecutive rows. Along
+  // a column the carry source of row q is the main source of row q+1, so
+  // each column needs 5 source values for its 4 outputs (register carry).
+  // Each output row leaves as one 16-byte store; the cv pool cells of the
+  // same tile are zeroed with it (this replaces a memset of the whole pool).
   float* out = b.sdem + sd.sdem_off;
-  // 16 threads x 4 columns per output row, 16 rows per pass.
+  int* cvz = b.cv + sd.sdem_off;
   const int cx = (threadIdx.x & 15) * 4;
-  for (int r = threadIdx.x >> 4; r < kTQ; r += kThreads / 16) {
-    const int q = q0 + r;
-    if (q >= sd.skw_rows) break;
-    float v[4];
+  const int r0 = (threadIdx.x >> 4) * 4;
+  float v[4][4];  // [row][col]
 #pragma unroll
-    for (int c = 0; c < 4; ++c) {
-      const int jj = cx + c;
-      float acc = 0.0f;
-      if (jj < jn) {
-        const float f = s_frac[jj];
-        const float a = __fsub_rn(1.0f, f);
-        const int im = q - sd.base + s_dest[jj];
-        if (im >= 0 && im < sd.rows) {
-          acc = __fadd_rn(acc, __fmul_rn(a, src[im - i_lo][jj]));
-        }
-        if (im + 1 >= 0 && im + 1 < sd.rows) {
-          acc = __fadd_rn(acc, __fmul_rn(f, src[im + 1 - i_lo][jj]));
-        }
-      }
-      v[c] = acc;
+  for (int c = 0; c < 4; ++c) {
+    const int jj = cx + c;
+    const bool colok = jj < jn;
+    const float f = colok ? s_frac[jj] : 0.f;
+    const float a = __fsub_rn(1.0f, f);
+    const int im0 = q0 + r0 - sd.base + (colok ? s_dest[jj] : 0);  // main source row of the first output
+    float sv[5];
+#pragma unroll
+    for (int u = 0; u < 5; ++u) {
+      const int im = im0 + u;
+      sv[u] = (colok && im >= 0 && im < sd.rows) ? src[im - i_lo][jj] : 0.f;
     }
-    if (j0 + cx < sd.pitch) {
-      *reinterpret_cast<float4*>(out + static_cast<size_t>(q) * sd.pitch + j0 + cx) =
-          make_float4(v[0], v[1], v[2], v[3]);
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      const int im = im0 + u;
+      float acc = 0.0f;
+      if (colok) {
+        if (im >= 0 && im < sd.rows) acc = __fadd_rn(acc, __fmul_rn(a, sv[u]));
+        if (im + 1 >= 0 && im + 1 < sd.rows) acc = __fadd_rn(acc, __fmul_rn(f, sv[u + 1]));
+      }
+      v[u][c] = acc;
+    }
+  }
+  if (j0 + cx < sd.pitch) {
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      const int q = q0 + r0 + u;
+      if (q < sd.skw_rows) {
+        const size_t o = static_cast<size_t>(q) * sd.pitch + j0 + cx;
+        *reinterpret_cast<float4*>(out + o) = make_float4(v[u][0], v[u][1], v[u][2], v[u][3]);
+        *reinterpret_cast<int4*>(cvz + o) = make_int4(0, 0, 0, 0);
+      }
     }
   }
 }
