@@ -500,6 +500,39 @@ void run_sectors(sks_context* ctx, const float* d_dem, int dimy, int dimx, doubl
   }
 }
 
+// Cell scan of a device DEM (dem_check_kernel) with one small D2H: throws
+// the reference's invalid_argument for the first non-finite cell, then
+// validates the config (validate(Dem) before validate(RunConfig),
+// engine.cpp:68-81); returns true when the FP32 filter's preconditions do
+// not hold (every POV then takes the exact FP64 path).
+bool device_check(sks_context* ctx, const float* d_dem, int dimy, int dimx, const sks_run_config* cfg,
+                  cudaStream_t st) {
+  const size_t n = static_cast<size_t>(dimy) * dimx;
+  ctx->check.ensure(2 * sizeof(unsigned long long), ctx->device);
+  if (ctx->h_check == nullptr) {
+    cuda_check(cudaHostAlloc(reinterpret_cast<void**>(&ctx->h_check), 2 * sizeof(unsigned long long),
+                             cudaHostAllocDefault),
+               "pinned check");
+  }
+  cuda_check(cudaMemsetAsync(ctx->check.p, 0xff, sizeof(unsigned long long), st), "memset check");
+  cuda_check(cudaMemsetAsync(static_cast<char*>(ctx->check.p) + 8, 0, sizeof(unsigned long long), st),
+             "memset check");
+  cuda_check(launch_dem_check(d_dem, static_cast<long long>(n), ctx->check.as<unsigned long long>(), st),
+             "launch dem check");
+  ++ctx->launches;
+  cuda_check(cudaMemcpyAsync(ctx->h_check, ctx->check.p, 2 * sizeof(unsigned long long),
+                             cudaMemcpyDeviceToHost, st),
+             "D2H check");
+  cuda_check(cudaStreamSynchronize(st), "sync check");
+  if (ctx->h_check[0] != ~0ull) {
+    throw std::invalid_argument(nonfinite_message(static_cast<long long>(ctx->h_check[0]), dimx));
+  }
+  const std::string err = validate_config(cfg->ns, cfg->h0, cfg->max_distance);
+  if (!err.empty()) throw std::invalid_argument(err);
+  const double plo = std::ldexp(1.0, -40), phi = std::ldexp(1.0, 40);
+  return ctx->h_check[1] != 0 || (cfg->h0 != 0.0 && (cfg->h0 < plo || cfg->h0 > phi));
+}
+
 void total_host(sks_context* ctx, const float* dem, int dimy, int dimx, double cellsize,
                 const sks_run_config* cfg, int raw, double* out, sks_stats* stats) {
   auto t0 = std::chrono::steady_clock::now();
@@ -516,31 +549,8 @@ void total_host(sks_context* ctx, const float* dem, int dimy, int dimx, double c
   cudaStream_t st = ctx->own_stream;
   ctx->dem.ensure(n * sizeof(float), ctx->device);
   ctx->map.ensure(n * sizeof(double), ctx->device);
-  ctx->check.ensure(2 * sizeof(unsigned long long), ctx->device);
-  if (ctx->h_check == nullptr) {
-    cuda_check(cudaHostAlloc(reinterpret_cast<void**>(&ctx->h_check), 2 * sizeof(unsigned long long),
-                             cudaHostAllocDefault),
-               "pinned check");
-  }
   cuda_check(cudaMemcpyAsync(ctx->dem.p, dem, n * sizeof(float), cudaMemcpyHostToDevice, st), "H2D dem");
-  cuda_check(cudaMemsetAsync(ctx->check.p, 0xff, sizeof(unsigned long long), st), "memset check");
-  cuda_check(cudaMemsetAsync(static_cast<char*>(ctx->check.p) + 8, 0, sizeof(unsigned long long), st),
-             "memset check");
-  cuda_check(launch_dem_check(ctx->dem.as<float>(), static_cast<long long>(n),
-                              ctx->check.as<unsigned long long>(), st),
-             "launch dem check");
-  ++ctx->launches;
-  cuda_check(cudaMemcpyAsync(ctx->h_check, ctx->check.p, 2 * sizeof(unsigned long long),
-                             cudaMemcpyDeviceToHost, st),
-             "D2H check");
-  cuda_check(cudaStreamSynchronize(st), "sync check");
-  if (ctx->h_check[0] != ~0ull) {
-    throw std::invalid_argument(nonfinite_message(static_cast<long long>(ctx->h_check[0]), dimx));
-  }
-  err = validate_config(cfg->ns, cfg->h0, cfg->max_distance);
-  if (!err.empty()) throw std::invalid_argument(err);
-  const double plo = std::ldexp(1.0, -40), phi = std::ldexp(1.0, 40);
-  const bool exact = ctx->h_check[1] != 0 || (cfg->h0 != 0.0 && (cfg->h0 < plo || cfg->h0 > phi));
+  const bool exact = device_check(ctx, ctx->dem.as<float>(), dimy, dimx, cfg, st);
   cuda_check(cudaMemsetAsync(ctx->map.p, 0, n * sizeof(double), st), "memset map");
   std::vector<int> all(cfg->ns / 2);
   std::iota(all.begin(), all.end(), 0);
@@ -700,14 +710,16 @@ sks_status sks_context_run_sectors(sks_context* ctx, const float* d_dem, int dim
                                    int n_sectors, double* d_map, void* stream, sks_stats* stats) {
   return guarded([&] {
     if (!ctx || !cfg || !d_dem || !d_map) throw std::invalid_argument("null argument");
-    if (cfg->ns < 2 || cfg->ns % 2) throw std::invalid_argument("ns must be an even integer >= 2");
-    if (dimy < 2 || dimx < 2) throw std::invalid_argument("grid must be at least 2x2");
+    const std::string err = validate_grid_header(dimy, dimx, cellsize);
+    if (!err.empty()) throw std::invalid_argument(err);
     ctx->activate();
     std::lock_guard<std::mutex> lk(ctx->mu);
     std::vector<int> ks(sectors, sectors + n_sectors);
     sks_stats local{};
+    const bool exact = device_check(ctx, d_dem, dimy, dimx, cfg, static_cast<cudaStream_t>(stream));
+    local.kernel_launches += 1;  // dem_check
     run_sectors(ctx, d_dem, dimy, dimx, cellsize, cfg, ks, d_map, static_cast<cudaStream_t>(stream),
-                stats ? &local : nullptr, false);
+                stats ? &local : nullptr, exact);
     if (stats) *stats = local;
   });
 }

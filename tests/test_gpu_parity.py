@@ -319,6 +319,43 @@ def test_total_viewshed_raw_bitexact(ora, shape, kind, ns, maxd):
     assert np.array_equal(b64(ours), b64(ref))
 
 
+@pytest.mark.parametrize("scale", [3.0e12, 2.0e-13])
+def test_exact_path_outside_filter_range(ora, scale):
+    """Elevations outside the FP32 filter's proven range [2^-40, 2^40]
+     switch every POV to the FP64 path: still bit-exact,
+    through the host entry point and through the device-pointer entry point
+    (Context.run_sectors, the multi-GPU building block)."""
+    import torch
+
+    base = sk.make_synthetic(sk.SyntheticKind.Fractal, 30, 26, 10.0, 5).values
+    vals = np.ascontiguousarray(base * np.float32(scale), np.float32)
+    dem = sk.Dem(vals, 10.0)
+    cfg = sk.RunConfig(ns=16, h0=0.0, units=sk.Units.SquareMeters)
+    ref = ora.total_viewshed(vals, 10.0, 16, 0.0, raw=True)
+    ours = sk.total_viewshed_raw(dem, cfg)
+    assert np.array_equal(b64(ours), b64(ref))
+    ctx = sk.Context(0)
+    d_dem = torch.from_numpy(vals).cuda()
+    d_map = torch.zeros(vals.shape, dtype=torch.float64, device="cuda")
+    ctx.run_sectors(d_dem.data_ptr(), *vals.shape, 10.0, cfg, list(range(8)), d_map.data_ptr(),
+                    stream=torch.cuda.current_stream().cuda_stream)
+    torch.cuda.synchronize()
+    assert np.array_equal(b64(d_map.cpu().numpy()), b64(ref))
+
+
+def test_device_entry_rejects_non_finite():
+    import torch
+
+    vals = sk.make_synthetic(sk.SyntheticKind.Fractal, 20, 20, 10.0, 5).values.copy()
+    vals[7, 11] = np.nan
+    ctx = sk.Context(0)
+    d_dem = torch.from_numpy(vals).cuda()
+    d_map = torch.zeros(vals.shape, dtype=torch.float64, device="cuda")
+    with pytest.raises(ValueError, match=r"non-finite elevation at cell \(7, 11\)"):
+        ctx.run_sectors(d_dem.data_ptr(), 20, 20, 10.0, sk.RunConfig(ns=8), [0, 1], d_map.data_ptr(),
+                        stream=torch.cuda.current_stream().cuda_stream)
+
+
 def test_total_viewshed_units_and_scale(ora):
     dem = sk.make_synthetic(sk.SyntheticKind.SmoothedNoise, 16, 16, 10.0, 1)
     for units in (sk.Units.SquareMeters, sk.Units.SquareKilometers):
