@@ -59,7 +59,11 @@ constexpr int kW = SKS_FINE_W;  // fine window (targets): 8 or 16
 #ifndef SKS_NEAR_NOTEST
 #define SKS_NEAR_NOTEST 64
 #endif
-constexpr int kH = 64;     // coarse window (targets); also the flush period
+#ifndef SKS_COARSE_W
+#define SKS_COARSE_W 64
+#endif
+constexpr int kH = SKS_COARSE_W;  // coarse window (targets)
+static_assert(kTaskPovs % kH == 0, "task starts must be aligned to coarse windows");
 constexpr int kOff = 128;  // table index offset (dd >= -kOff + 1 addressable)
 constexpr int kThreads = 768;  // 24 warps: 80 registers, no spills (1024 spills at 64)
 constexpr int kMaxSlots = 8;
@@ -79,9 +83,9 @@ struct Layout2 {
   int slots;  // offset of slot 0
   __host__ __device__ Layout2(int lmax, int ncopies) {
     nc = ncopies;
-    lb = ((lmax + 64 + 63) / 64) * 64;
+    lb = ((lmax + kH + kH - 1) / kH) * kH;
     nw16 = lb / kW;
-    nw64 = lb / 64;
+    nw64 = lb / kH;
     T = ((kOff + lb + 16 + 31) / 32) * 32;
     slot = 2 * lb + 4 * nw16 + 4 * nw64;
     ctl = kMaxSlots * kCtlInts;
@@ -364,7 +368,7 @@ __device__ void run_task(const ScanArgs& a, const Layout2& lay, const Slot& sl, 
   const int ktest = ymin + SKS_NEAR_NOTEST;
   while (k0 <= klast) {
     if (!kVis && k0 >= ktest && k0 + kH - 1 <= kmain) {
-      const float2 em = lds64(w64a + (static_cast<unsigned>(k0) >> 3));
+      const float2 em = lds64(w64a + 8u * (static_cast<unsigned>(k0) / kH));
       if (window_hidden<kHl>(P, em, tb, k0, kH)) {
         k0 += kH;
         nskip += kH;
