@@ -191,6 +191,17 @@ sks_status sks_context_run_sectors(sks_context* ctx, const float* d_dem,
                                    const int* sectors, int n_sectors,
                                    double* d_map, void* stream,
                                    sks_stats* stats);
+/* Row-block sharding: all ns/2 sectors, but only part
+   `part` of `nparts` of every sector's skewed rows — contiguous blocks of
+   equal exact scan work — accumulated into d_map. The nparts maps sum (e.g.
+   one NCCL reduce) to the total raw map; per-cell summation order differs
+   from the single-GPU order (relative differences ~1e-16). Replaces the
+   sector pool of total_viewshed_raw (engine.cpp:109-220) across GPUs. */
+sks_status sks_context_run_rows(sks_context* ctx, const float* d_dem, int dimy,
+                                int dimx, double cellsize,
+                                const sks_run_config* cfg, int part, int nparts,
+                                double* d_map, void* stream, sks_stats* stats);
+
 /* d_map[i] *= area_scale_factor(ns, cellsize, units) on `stream`. */
 sks_status sks_context_scale(sks_context* ctx, double* d_map, long long n,
                              int ns, double cellsize, int units,

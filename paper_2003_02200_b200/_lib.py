@@ -98,6 +98,8 @@ SIGNATURES = {
     "sks_context_destroy": (None, [_vp]),
     "sks_context_run_sectors": (C.c_int, [_vp, _vp, C.c_int, C.c_int, C.c_double, C.POINTER(RunConfigC),
                                           _i32p, C.c_int, _vp, _vp, C.POINTER(StatsC)]),
+    "sks_context_run_rows": (C.c_int, [_vp, _vp, C.c_int, C.c_int, C.c_double, C.POINTER(RunConfigC),
+                                       C.c_int, C.c_int, _vp, _vp, C.POINTER(StatsC)]),
     "sks_context_scale": (C.c_int, [_vp, _vp, C.c_longlong, C.c_int, C.c_double, C.c_int, _vp]),
     "sks_context_total_viewshed": (C.c_int, [_vp, _vp, C.c_int, C.c_int, C.c_double,
                                              C.POINTER(RunConfigC), C.c_int, _vp, C.POINTER(StatsC)]),

@@ -162,6 +162,8 @@ std::unique_ptr<Batch> make_batch(const std::vector<SectorPlanH>& plans,
     d.max_dd = p.max_dd;
     d.col_off = col_off;
     d.row_off = row_off;
+    d.q_lo = p.q_lo;
+    d.q_hi = p.q_hi < 0 ? p.skw_rows : p.q_hi;
     std::copy(p.map, p.map + 6, d.map);
     std::copy(p.inv, p.inv + 6, d.inv);
     d.correction = p.correction;
@@ -176,12 +178,12 @@ std::unique_ptr<Batch> make_batch(const std::vector<SectorPlanH>& plans,
       const RowRange& r = p.ranges[q];
       b->ranges.push_back(make_int2(r.first, r.last));
       const int L = r.last - r.first;
-      if (L >= 2 && p.max_dd > 0) {
+      if (L >= 2 && p.max_dd > 0 && q >= d.q_lo && q < d.q_hi) {
         b->items.push_back(ScanItem{static_cast<int>(s), q});
         b->lmax = std::max(b->lmax, L);
+        b->target_evals += row_target_evals(L, p.max_dd);
       }
     }
-    b->target_evals += p.target_evals;
     max_cols = std::max(max_cols, p.cols);
     max_rows = std::max(max_rows, p.skw_rows);
     b->sdev.push_back(d);
@@ -202,7 +204,15 @@ std::unique_ptr<Batch> make_batch(const std::vector<SectorPlanH>& plans,
     b->fix_cap += 2u * static_cast<unsigned>(r.y - r.x);
   }
   b->tiles_x = (max_cols + relocate_tile_cols() - 1) / relocate_tile_cols();
-  b->tiles_total = b->tiles_x * ((max_rows + relocate_tile_rows() - 1) / relocate_tile_rows());
+  // tile rows from each sector's first owned tile row to its last owned row
+  int tq_max = 0;
+  for (const SectorDev& d : b->sdev) {
+    const int tr = relocate_tile_rows();
+    const int hi = std::max(d.q_hi, d.q_lo + 1);
+    tq_max = std::max(tq_max, (hi + tr - 1) / tr - d.q_lo / tr);
+  }
+  (void)max_rows;
+  b->tiles_total = b->tiles_x * tq_max;
   if (b->fix_cap == 0) b->fix_cap = 1;
   // upload metadata once
   auto up = [&](DevBuf& buf, const void* src, size_t bytes) {
@@ -252,10 +262,10 @@ struct sks_context {
   int sms = 0;
   std::mutex mu;
   // plan cache
-  std::map<std::tuple<int, int, int, double, double, std::vector<int>>, std::unique_ptr<Plans>>
+  std::map<std::tuple<int, int, int, double, double, std::vector<int>, int, int>, std::unique_ptr<Plans>>
       cache;
   // work buffers
-  DevBuf sdem, cv, cvb, queue, fixcnt, wm16, counters, dem, map, vis, check;
+  DevBuf sdem, cv, cvb, queue, fixcnt, fixoff, wm16, counters, dem, map, vis, check;
   unsigned long long* h_check = nullptr;  // pinned: device DEM scan result
   cudaEvent_t ev[8] = {};
   long long launches = 0;
@@ -263,13 +273,16 @@ struct sks_context {
   void activate() const { cuda_check(cudaSetDevice(device), "cudaSetDevice"); }
 
   Plans& plans_for(int dimy, int dimx, int ns, double cellsize, double max_distance,
-                   const std::vector<int>& sectors) {
-    auto key = std::make_tuple(dimy, dimx, ns, cellsize, max_distance, sectors);
+                   const std::vector<int>& sectors, int part = 0, int nparts = 1) {
+    auto key = std::make_tuple(dimy, dimx, ns, cellsize, max_distance, sectors, part, nparts);
     auto it = cache.find(key);
     if (it != cache.end()) return *it->second;
     if (cache.size() > 16) cache.clear();
     auto P = std::make_unique<Plans>();
-    for (int k : sectors) P->plans.push_back(plan_sector(k, ns, dimy, dimx, cellsize, max_distance));
+    for (int k : sectors) {
+      P->plans.push_back(plan_sector(k, ns, dimy, dimx, cellsize, max_distance));
+      if (nparts > 1) set_row_block(P->plans.back(), part, nparts);
+    }
     make_batches(*P, device);
     Plans& ref = *P;
     cache.emplace(key, std::move(P));
@@ -296,6 +309,7 @@ struct sks_context {
     if (split_bwd) cvb.ensure(static_cast<size_t>(b.pool_elems) * sizeof(int), device);
     queue.ensure(static_cast<size_t>(b.fix_cap) * sizeof(unsigned), device);
     fixcnt.ensure(std::max<size_t>(b.items.size(), 1) * sizeof(unsigned), device);
+    fixoff.ensure((b.items.size() + 1) * sizeof(unsigned), device);
     wm16.ensure(static_cast<size_t>(b.pool_elems / 16 + 1) * sizeof(float), device);
     counters.ensure(kCounterBytes, device);
   }
@@ -357,8 +371,8 @@ struct sks_context {
 
   void fixup_batch(const ScanArgs& a, cudaStream_t st) {
     if (a.n_items == 0) return;
-    cuda_check(launch_fixup(a, st), "launch fixup");
-    launches += 1;
+    cuda_check(launch_fixup(a, fixoff.as<unsigned>(), st), "launch fixup");
+    launches += 2;
   }
 
   ~sks_context() {
@@ -421,13 +435,13 @@ double elapsed(cudaEvent_t a, cudaEvent_t b) {
 // Core: run the given sectors on device data. Accumulates into d_map.
 void run_sectors(sks_context* ctx, const float* d_dem, int dimy, int dimx, double cellsize,
                  const sks_run_config* cfg, std::vector<int> sectors, double* d_map,
-                 cudaStream_t st, sks_stats* stats, bool force_exact) {
+                 cudaStream_t st, sks_stats* stats, bool force_exact, int part = 0, int nparts = 1) {
   std::sort(sectors.begin(), sectors.end());
   sectors.erase(std::unique(sectors.begin(), sectors.end()), sectors.end());
   for (int k : sectors) {
     if (k < 0 || k >= cfg->ns / 2) throw std::out_of_range("sector index out of range");
   }
-  Plans& P = ctx->plans_for(dimy, dimx, cfg->ns, cellsize, cfg->max_distance, sectors);
+  Plans& P = ctx->plans_for(dimy, dimx, cfg->ns, cellsize, cfg->max_distance, sectors, part, nparts);
   const long long launches0 = ctx->launches;
   double t_skew = 0, t_scan = 0, t_fix = 0, t_unskew = 0;
   long long flagged = 0, evals = 0, skipped = 0;
@@ -720,6 +734,28 @@ sks_status sks_context_run_sectors(sks_context* ctx, const float* d_dem, int dim
     local.kernel_launches += 1;  // dem_check
     run_sectors(ctx, d_dem, dimy, dimx, cellsize, cfg, ks, d_map, static_cast<cudaStream_t>(stream),
                 stats ? &local : nullptr, exact);
+    if (stats) *stats = local;
+  });
+}
+
+sks_status sks_context_run_rows(sks_context* ctx, const float* d_dem, int dimy, int dimx,
+                                double cellsize, const sks_run_config* cfg, int part, int nparts,
+                                double* d_map, void* stream, sks_stats* stats) {
+  return guarded([&] {
+    if (!ctx || !cfg || !d_dem || !d_map) throw std::invalid_argument("null argument");
+    if (nparts < 1 || part < 0 || part >= nparts) throw std::out_of_range("row part out of range");
+    const std::string err = validate_grid_header(dimy, dimx, cellsize);
+    if (!err.empty()) throw std::invalid_argument(err);
+    ctx->activate();
+    std::lock_guard<std::mutex> lk(ctx->mu);
+    if (cfg->ns < 2 || cfg->ns % 2) throw std::invalid_argument("ns must be an even integer >= 2");
+    std::vector<int> all(cfg->ns / 2);
+    std::iota(all.begin(), all.end(), 0);
+    sks_stats local{};
+    const bool exact = device_check(ctx, d_dem, dimy, dimx, cfg, static_cast<cudaStream_t>(stream));
+    local.kernel_launches += 1;  // dem_check
+    run_sectors(ctx, d_dem, dimy, dimx, cellsize, cfg, all, d_map, static_cast<cudaStream_t>(stream),
+                stats ? &local : nullptr, exact, part, nparts);
     if (stats) *stats = local;
   });
 }

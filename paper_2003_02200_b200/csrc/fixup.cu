@@ -13,12 +13,13 @@
 // therefore the reference's.
 //
 // Mapping. The queue is segmented per skewed row (one exact-bound segment
-// per scan item, filled by the scan kernels). A warp claims 32 consecutive
-// rows at a time (longest rows first, global counter) and spreads all their
-// queued POVs over its lanes, one POV per lane (a row alone has ~5-25 on
-// fractal terrain). Rows are read through L1/L2 and each lane skips hidden
-// 16-target windows with the row's window maxima (written by the scan's row
-// loader), so occupancy is not limited by shared memory.
+// per scan item, filled by the scan kernels). A one-CTA prefix over the
+// per-row counts turns the segments into one flat list of queued POVs (in
+// row order, longest rows first) and every thread takes POVs from it: work
+// is spread over all lanes however the flags cluster (whole runs or the
+// row blocks of one GPU of several). Rows are read through L1/L2 and each
+// POV skips hidden 16-position blocks with the row's window maxima (written
+// by the scan's row loader).
 #include <cuda_runtime.h>
 
 #include <cfloat>
@@ -77,6 +78,58 @@ __device__ __forceinline__ bool exact_step(ExactState& S, const float* row, int 
 // path in groups of 4 (predicated updates only); a group containing a band
 // target is rolled back and re-run target by target with the exact
 // resolution, as is the remainder (< 4).
+// Block form: the block's (up to 16) elevations are loaded together first
+// (ev[i] = row[x + sg*(da+i)]), so a lane waits for one L2 round trip per
+// block instead of one per group of 4.
+__device__ __forceinline__ void eval_block(ExactState& S, const float* row, const float* ivt, int x,
+                                           int sg, int da, int db) {
+  float ev[16];
+#pragma unroll
+  for (int i = 0; i < 16; ++i) ev[i] = da + i <= db ? __ldg(row + x + sg * (da + i)) : 0.f;
+#pragma unroll
+  for (int g = 0; g < 4; ++g) {
+    const int dd = da + 4 * g;
+    if (dd + 3 > db) {
+      // remainder (< 4 targets): one by one
+#pragma unroll
+      for (int i = 0; i < 4; ++i) {
+        if (dd + i <= db) exact_step(S, row, x, sg, dd + i, ev[4 * g + i], ivt[dd + i]);
+      }
+      break;
+    }
+    float t[4];
+#pragma unroll
+    for (int i = 0; i < 4; ++i) t[i] = __fmul_rn(__fadd_rn(__fsub_rn(ev[4 * g + i], S.hf), -S.hl), ivt[dd + i]);
+    const float hi0 = S.hi, lo0 = S.lo;
+    const int cv0 = S.cv, r0 = S.r;
+    bool band = false, rec = false;
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+      const bool pa = t[i] > S.hi;
+      const bool pg = t[i] >= S.lo;
+      band |= pg & !pa;
+      rec |= pa;
+      if (pa) {
+        const float at = fabsf(t[i]);
+        S.hi = __fmaf_rn(at, kBand, t[i]);
+        S.lo = __fmaf_rn(at, -kBand, t[i]);
+        S.cv += 2 * (dd + i) + 1;
+        S.r = dd + i;
+      }
+    }
+    if (band) {
+      S.hi = hi0;
+      S.lo = lo0;
+      S.cv = cv0;
+      S.r = r0;
+#pragma unroll 1
+      for (int i = 0; i < 4; ++i) exact_step(S, row, x, sg, dd + i, ev[4 * g + i], ivt[dd + i]);
+    } else if (rec) {
+      S.Mvalid = false;
+    }
+  }
+}
+
 __device__ __forceinline__ void eval_range(ExactState& S, const float* row, const float* ivt, int x,
                                            int sg, int da, int db) {
   int dd = da;
@@ -167,91 +220,110 @@ __device__ int exact_pov(const float* row, const float* wm, const float* ivt, in
   // position blocks in scan order
   const int pfirst = x + sg, plast = x + sg * D;
   const int w0 = pfirst >> 4, w1 = plast >> 4;
+  float wmv = __ldg(wm + w0);  // window maximum of the current block, loaded one block ahead
   for (int w = w0;; w += sg) {
     const int da = max(1, sg > 0 ? 16 * w - x : x - (16 * w + 15));
     const int db = min(D, sg > 0 ? 16 * w + 15 - x : x - 16 * w);
-    const float N = __fadd_rn(__fsub_rn(wm[w], S.hf), -S.hl);
+    const float wnext = w != w1 ? __ldg(wm + w + sg) : 0.f;
+    const float N = __fadd_rn(__fsub_rn(wmv, S.hf), -S.hl);
     if (!(__fmul_rn(N, ivt[da]) < S.lo && __fmul_rn(N, ivt[db]) < S.lo)) {
-      eval_range(S, row, ivt, x, sg, da, db);
+      eval_block(S, row, ivt, x, sg, da, db);
     }
     if (w == w1) break;
+    wmv = wnext;
   }
   return S.cv;
 }
 
-// Persistent warps: each claims 32 consecutive rows (scan items, longest
-// first), prefix-sums their queued POV counts and gives every lane one
-// queued POV at a time. Rows are read through L1/L2 from the sDEM pool; the
-// fl(1/d) table sits in shared memory.
-__global__ void __launch_bounds__(kWarps * 32) fixup_kernel(ScanArgs a, int tab_len) {
+// Exclusive prefix of the queued POVs per scan item (one CTA): off[it] =
+// sum over items < it of fix_cnt * group; off[n_items] = total.
+__global__ void __launch_bounds__(1024) fixup_prefix_kernel(ScanArgs a, unsigned* off) {
+  __shared__ unsigned warp_sums[32];
+  const int n = a.n_items;
+  const int per = (n + blockDim.x - 1) / blockDim.x;
+  const int b0 = threadIdx.x * per, b1 = min(n, b0 + per);
+  const unsigned grp = static_cast<unsigned>(a.fix_group);
+  unsigned local = 0;
+  for (int i = b0; i < b1; ++i) local += a.fix_cnt[i] * grp;
+  // block exclusive scan of the per-thread sums
+  const int lane = threadIdx.x & 31, wp = threadIdx.x >> 5;
+  unsigned incl = local;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const unsigned u = __shfl_up_sync(0xffffffffu, incl, o);
+    if (lane >= o) incl += u;
+  }
+  if (lane == 31) warp_sums[wp] = incl;
+  __syncthreads();
+  if (wp == 0) {
+    unsigned ws = warp_sums[lane];
+    unsigned wi = ws;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const unsigned u = __shfl_up_sync(0xffffffffu, wi, o);
+      if (lane >= o) wi += u;
+    }
+    warp_sums[lane] = wi - ws;
+  }
+  __syncthreads();
+  unsigned run = warp_sums[wp] + incl - local;
+  for (int i = b0; i < b1; ++i) {
+    off[i] = run;
+    run += a.fix_cnt[i] * grp;
+  }
+  if (threadIdx.x == blockDim.x - 1) off[n] = run;
+}
+
+// One thread per queued POV (flat list over all rows, in row order, so
+// neighbouring threads share rows): the POV's row is found by a binary search
+// of the prefix, then the POV is re-run exactly (exact_pov). Rows are read
+// through L1/L2; the fl(1/d) table sits in shared memory.
+__global__ void __launch_bounds__(kWarps * 32) fixup_kernel(ScanArgs a, int tab_len, const unsigned* off) {
   extern __shared__ __align__(16) float ivt[];  // fl(1/d), d = 0 .. tab_len - 1
-  __shared__ unsigned pref[kWarps][32];          // inclusive prefix of POVs over the warp's rows
-  __shared__ unsigned next[kWarps];              // next POV of the warp's batch
-  const int lane = threadIdx.x & 31;
-  const int wp = threadIdx.x >> 5;
   for (int d = threadIdx.x; d < tab_len; d += blockDim.x) ivt[d] = __frcp_rn(static_cast<float>(d));
   __syncthreads();
   const unsigned grp = static_cast<unsigned>(a.fix_group);
-  for (;;) {
-    int it0 = 0;
-    if (lane == 0) it0 = static_cast<int>(atomicAdd(a.fix_item_counter, 32u));
-    it0 = __shfl_sync(0xffffffffu, it0, 0);
-    if (it0 >= a.n_items) break;
-    const unsigned c = it0 + lane < a.n_items ? a.fix_cnt[it0 + lane] * grp : 0u;
-    unsigned incl = c;
-#pragma unroll
-    for (int o = 1; o < 32; o <<= 1) {
-      const unsigned u = __shfl_up_sync(0xffffffffu, incl, o);
-      if (lane >= o) incl += u;
+  const unsigned total = off[a.n_items];
+  const unsigned stride = gridDim.x * blockDim.x;
+  for (unsigned w = blockIdx.x * blockDim.x + threadIdx.x; w < total; w += stride) {
+    // item: the last it with off[it] <= w
+    int lo = 0, hi = a.n_items;  // off[lo] <= w < off[hi]
+    while (hi - lo > 1) {
+      const int mid = (lo + hi) >> 1;
+      if (__ldg(off + mid) <= w) lo = mid; else hi = mid;
     }
-    const unsigned total = __shfl_sync(0xffffffffu, incl, 31);
-    if (total == 0) continue;
-    pref[wp][lane] = incl;
-    if (lane == 0) next[wp] = 0;
-    __syncwarp();
-    // lanes pull POVs one at a time until the batch is drained, so lanes
-    // with short scans do not idle behind long ones
-    for (;;) {
-      const unsigned w = atomicAdd(&next[wp], 1u);
-      if (w >= total) break;
-      int j = 0;  // row of POV w: first prefix entry above w
-#pragma unroll
-      for (int step = 16; step >= 1; step >>= 1) {
-        if (pref[wp][j + step - 1] <= w) j += step;
-      }
-      const unsigned wj = w - (j > 0 ? pref[wp][j - 1] : 0u);
-      const int it = it0 + j;
-      const ScanItem item = a.items[it];
-      const SectorDev& sd = a.b.sectors[item.s];
-      const int2 rg = a.b.ranges[sd.row_off + item.q];
-      const int first = rg.x;
-      const int L = rg.y - rg.x;
-      const long long rowoff = sd.sdem_off + static_cast<long long>(item.q) * sd.pitch;
-      const float* row = a.b.sdem + rowoff + first;
-      const unsigned ent = a.fix_queue[a.fix_off[it] + wj / grp];
-      const int dir = static_cast<int>(ent >> 31);
-      const int y = static_cast<int>((ent & 0x7fffffffu) * grp + wj % grp);
-      if (y >= L) continue;
-      const int x = dir ? (L - 1 - y) : y;
-      const int D = min(sd.max_dd, dir ? x : (L - 1 - x));
-      const bool dbg = a.dbg_j0 >= 0 && item.s == 0 && item.q == 0 && first + x == a.dbg_j0;
-      const double h = dbg ? a.dbg_h : __dadd_rn(static_cast<double>(row[x]), a.h0);
-      uint8_t* vis = dbg ? (dir ? a.dbg_vis_bwd : a.dbg_vis_fwd) : nullptr;
-      const float* wm = a.wm16 != nullptr ? a.wm16 + rowoff / 16 : nullptr;
-      const int cv = exact_pov(row, wm, ivt, x, dir ? -1 : 1, D, h, a.force_exact != 0, vis);
-      if (cv != 0) {
-        int* dst = ((dir && a.b.cv_bwd) ? a.b.cv_bwd : a.b.cv) + rowoff + first;
-        atomicAdd(dst + x, cv);
-      }
+    const int it = lo;
+    const unsigned wj = w - __ldg(off + it);
+    const ScanItem item = a.items[it];
+    const SectorDev& sd = a.b.sectors[item.s];
+    const int2 rg = a.b.ranges[sd.row_off + item.q];
+    const int first = rg.x;
+    const int L = rg.y - rg.x;
+    const long long rowoff = sd.sdem_off + static_cast<long long>(item.q) * sd.pitch;
+    const float* row = a.b.sdem + rowoff + first;
+    const unsigned ent = a.fix_queue[a.fix_off[it] + wj / grp];
+    const int dir = static_cast<int>(ent >> 31);
+    const int y = static_cast<int>((ent & 0x7fffffffu) * grp + wj % grp);
+    if (y >= L) continue;
+    const int x = dir ? (L - 1 - y) : y;
+    const int D = min(sd.max_dd, dir ? x : (L - 1 - x));
+    const bool dbg = a.dbg_j0 >= 0 && item.s == 0 && item.q == 0 && first + x == a.dbg_j0;
+    const double h = dbg ? a.dbg_h : __dadd_rn(static_cast<double>(row[x]), a.h0);
+    uint8_t* vis = dbg ? (dir ? a.dbg_vis_bwd : a.dbg_vis_fwd) : nullptr;
+    const float* wm = a.wm16 != nullptr ? a.wm16 + rowoff / 16 : nullptr;
+    const int cv = exact_pov(row, wm, ivt, x, dir ? -1 : 1, D, h, a.force_exact != 0, vis);
+    if (cv != 0) {
+      int* dst = ((dir && a.b.cv_bwd) ? a.b.cv_bwd : a.b.cv) + rowoff + first;
+      atomicAdd(dst + x, cv);
     }
-    __syncwarp();
   }
 }
 
 }  // namespace
 
-int launch_fixup(const ScanArgs& a, void* stream) {
+int launch_fixup(const ScanArgs& a, unsigned* off, void* stream) {
   if (a.n_items == 0) return 0;
+  fixup_prefix_kernel<<<1, 1024, 0, static_cast<cudaStream_t>(stream)>>>(a, off);
   int dev = 0;
   cudaGetDevice(&dev);
   int sms = 0;
@@ -266,7 +338,7 @@ int launch_fixup(const ScanArgs& a, void* stream) {
   e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fixup_kernel, kWarps * 32, smem);
   if (e != cudaSuccess) return static_cast<int>(e);
   fixup_kernel<<<sms * (per_sm > 0 ? per_sm : 1), kWarps * 32, smem, static_cast<cudaStream_t>(stream)>>>(
-      a, tab_len);
+      a, tab_len, off);
   return static_cast<int>(cudaGetLastError());
 }
 

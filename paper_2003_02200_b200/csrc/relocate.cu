@@ -36,11 +36,13 @@ relocate_kernel(const float* __restrict__ dem, BatchDev b, int tiles_x) {
 
   const SectorDev sd = b.sectors[blockIdx.y];
   const int tile = blockIdx.x;
-  const int tq = tile / tiles_x;
-  const int tj = tile - tq * tiles_x;
+  // tile rows are counted from the first tile row holding an owned row
+  const int tq = tile / tiles_x + sd.q_lo / kTQ;
+  const int tj = tile - (tile / tiles_x) * tiles_x;
   const int q0 = tq * kTQ;
   const int j0 = tj * kTJ;
   if (q0 >= sd.skw_rows || j0 >= sd.cols) return;
+  if (q0 + kTQ <= sd.q_lo || q0 >= sd.q_hi) return;  // no row of this run's block (row sharding)
   const int jn = min(kTJ, sd.cols - j0);
   const int* dest = b.dest + sd.col_off;
   const float* fracf = b.fracf + sd.col_off;

@@ -25,7 +25,7 @@ struct SectorDev {
   int max_dd;
   int col_off;   // into dest / fracf / fracd
   int row_off;   // into ranges
-  int pad0;
+  int q_lo, q_hi;  // skewed rows this run owns (row-block sharding; all: 0, skw_rows)
   int map[6];    // pre (i, j) -> DEM (si, sj)
   int inv[6];    // DEM (si, sj) -> pre (i, j)
   double correction;  // 1 + tan^2
@@ -93,7 +93,7 @@ size_t scan_smem_bytes(int lmax, bool shifted);
 int scan_block_threads(int lmax);
 int launch_scan(const ScanArgs& a, int grid, void* stream);
 int scan_occupancy(int lmax, int* grid_out);
-int launch_fixup(const ScanArgs& a, void* stream);  // fixup.cu
+int launch_fixup(const ScanArgs& a, unsigned* off, void* stream);  // fixup.cu (off: n_items + 1)
 int scan2_slots(int lmax);  // 0: rows too long for the target-lockstep kernel
 size_t scan2_smem_bytes(int lmax, int nslots);
 int launch_scan2(const ScanArgs& a, int nslots, void* stream);

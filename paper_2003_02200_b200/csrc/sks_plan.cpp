@@ -95,6 +95,40 @@ void fill_tables(SectorPlanH& p) {
 
 }  // namespace
 
+void set_row_block(SectorPlanH& p, int part, int nparts) {
+  if (nparts <= 1) {
+    p.q_lo = 0;
+    p.q_hi = p.skw_rows;
+    return;
+  }
+  // Row cost model: the exact scan work L(L-1) (capped) plus a constant per
+  // 64-POV task, whose first 64-target window is always evaluated in full
+  // (fitted from per-block times of the 2000^2 bench: ~60k target-equivalents):
+  // short rows cost far more per target than the work alone says.
+  constexpr long long kTaskCost = 60000;
+  auto row_cost = [&](int q) {
+    const long long L = p.ranges[q].last - p.ranges[q].first;
+    if (L < 2 || p.max_dd <= 0) return 0LL;
+    return row_target_evals(L, p.max_dd) + 2 * ((L + 63) / 64) * kTaskCost;
+  };
+  long long total = 0;
+  for (int q = 0; q < p.skw_rows; ++q) total += row_cost(q);
+  // block b starts at the first row whose preceding cost reaches b/nparts of
+  // the total (exact integer comparison: cum * nparts >= b * total)
+  auto start = [&](int b) {
+    if (b <= 0) return 0;
+    if (b >= nparts) return p.skw_rows;
+    long long cum = 0;
+    for (int q = 0; q < p.skw_rows; ++q) {
+      if (cum * nparts >= static_cast<long long>(b) * total) return q;
+      cum += row_cost(q);
+    }
+    return p.skw_rows;
+  };
+  p.q_lo = start(part);
+  p.q_hi = start(part + 1);
+}
+
 std::vector<RowRange> row_ranges(int rows, int cols, int base,
                                  const std::vector<int>& dest,
                                  const std::vector<float>& fracf) {

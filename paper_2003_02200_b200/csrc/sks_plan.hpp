@@ -45,7 +45,13 @@ struct SectorPlanH {
   std::vector<double> fracd;   // frac, unskew_accumulate's weights
   std::vector<RowRange> ranges;  // per skewed row, [first, last)
   long long target_evals = 0;    // exact scan work of the sector
+  int q_lo = 0, q_hi = -1;       // owned skewed rows [q_lo, q_hi); q_hi < 0: all
 };
+
+// Row-block sharding: the skewed rows of a sector split into
+// nparts contiguous blocks of equal exact scan work; block `part` of the
+// plan's rows. Sets p.q_lo / p.q_hi.
+void set_row_block(SectorPlanH& p, int part, int nparts);
 
 // skew.cpp:16-19
 int base_offset(int src_rows, int cols, double shear_tan);

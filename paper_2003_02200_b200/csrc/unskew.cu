@@ -110,14 +110,26 @@ __global__ void __launch_bounds__(256) unskew_tiled_kernel(BatchDev b, double* _
     const int d_lo = __ldg(dest + j_lo), d_hi = __ldg(dest + j_hi);
     const int p_lo = sd.base + i_lo - d_hi - 1;  // includes the p-1 rows
     const int np = sd.base + i_hi - d_lo - p_lo + 1;
+    // row-block sharding: rows outside [q_lo, q_hi) belong to another run
+    // (their cv contributes 0 here; the runs' maps sum to the total)
+    const int q_lo = sd.q_lo, q_hi = sd.q_hi;
+    if (max(p_lo, q_lo) >= min(p_lo + np, q_hi)) continue;  // nothing owned here (uniform across the CTA)
+    const bool whole = q_lo <= p_lo && q_hi >= p_lo + np;   // always so on one GPU
     __syncthreads();  // previous sector's smem reads are done
     if (threadIdx.x < nj) {
       sdest[threadIdx.x] = __ldg(dest + j_lo + threadIdx.x);
       sfrac[threadIdx.x] = __ldg(b.fracd + sd.col_off + j_lo + threadIdx.x);
     }
     const int* cvb = b.cv + sd.sdem_off + static_cast<long long>(p_lo) * sd.pitch + j_lo;
-    for (int r = ty; r < np; r += 8) {
-      if (tx < nj) scv[r][tx] = __ldg(cvb + static_cast<long long>(r) * sd.pitch + tx);
+    if (whole) {
+      for (int r = ty; r < np; r += 8) {
+        if (tx < nj) scv[r][tx] = __ldg(cvb + static_cast<long long>(r) * sd.pitch + tx);
+      }
+    } else {
+      for (int r = ty; r < np; r += 8) {
+        const int p = p_lo + r;
+        if (tx < nj) scv[r][tx] = (p >= q_lo && p < q_hi) ? __ldg(cvb + static_cast<long long>(r) * sd.pitch + tx) : 0;
+      }
     }
     __syncthreads();
 #pragma unroll

@@ -1,13 +1,23 @@
-"""Sector sharding over GPUs with one reduce of the viewshed maps.
+"""Multi-GPU total viewshed with one reduce of the viewshed maps.
 
 Replaces the reference's single-process sector pool (engine.cpp:115-176) and
 the paper's host-side multi-GPU reduction (Alg. 10): one process per
-GPU (torch.distributed, NCCL over NVLink), sectors assigned statically by
-longest-processing-time on their exact scan work (sks_partition_sectors),
-each rank accumulating its sectors in ascending k into a private FP64 map on
-its GPU, then a single ``reduce(SUM)`` of the maps to rank 0. That reduce is
-the path's only exchange step; the DEM itself is copied host->device on every
-rank (it is the caller's input).
+GPU (torch.distributed, NCCL over NVLink), each rank accumulating its share
+into a private FP64 map on its GPU, then a single ``reduce(SUM)`` of the maps
+to rank 0. That reduce is the path's only exchange step; the DEM itself is
+copied host->device on every rank (it is the caller's input).
+
+Two ways to share the work:
+
+* ``mode="rows"`` (default): every rank runs all sectors but only its block
+  of every sector's skewed rows (contiguous blocks of equal exact scan work,
+  ``sks_context_run_rows``). Measured per-sector costs at 2000^2 vary 4x
+  and correlate weakly with the exact work model (the hidden-window skip
+  depends on terrain and angle), so whole-sector assignment balances poorly
+  (LPT on the work model: 68% at 8 GPUs); a block of every sector averages
+  the terrain out (SURVEY §8e's sub-sector work items).
+* ``mode="sectors"``: whole sectors by LPT on the exact work
+  (``sks_partition_sectors``), the paper's scheme.
 
 ``compute`` lets CPU tests (gloo, world_size 2) exercise exactly this
 sharding/reduce logic with the oracle standing in for the GPU pipeline; the
@@ -30,10 +40,11 @@ def my_sectors(ns: int, dimy: int, dimx: int, world: int, rank: int, cellsize: f
 
 def total_viewshed_distributed(dem: np.ndarray, cellsize: float, cfg: RunConfig, raw: bool = False,
                                compute: Optional[Callable[[Sequence[int]], np.ndarray]] = None,
-                               context=None, stream=None, stats: Optional[dict] = None):
+                               context=None, stream=None, stats: Optional[dict] = None, mode: str = "rows"):
     """Total viewshed of ``dem`` sharded over the default process group.
 
     Returns the (scaled unless ``raw``) map on rank 0 and None elsewhere.
+    ``compute`` (CPU tests) replaces the GPU pipeline for sector sharding.
     """
     import torch
     import torch.distributed as dist
@@ -56,11 +67,15 @@ def total_viewshed_distributed(dem: np.ndarray, cellsize: float, cfg: RunConfig,
     st = stream or torch.cuda.current_stream(dev)
     d_dem = torch.from_numpy(np.ascontiguousarray(dem, np.float32)).to(dev, non_blocking=True)
     d_map = torch.zeros((dimy, dimx), dtype=torch.float64, device=dev)
-    es = ctx.run_sectors(d_dem.data_ptr(), dimy, dimx, cellsize, cfg, mine, d_map.data_ptr(),
-                         stream=st.cuda_stream, want_stats=stats is not None)
+    if mode == "rows":
+        es = ctx.run_rows(d_dem.data_ptr(), dimy, dimx, cellsize, cfg, rank, world, d_map.data_ptr(),
+                          stream=st.cuda_stream, want_stats=stats is not None)
+    else:
+        es = ctx.run_sectors(d_dem.data_ptr(), dimy, dimx, cellsize, cfg, mine, d_map.data_ptr(),
+                             stream=st.cuda_stream, want_stats=stats is not None)
     if stats is not None:
         stats["rank_stats"] = es
-        stats["sectors"] = mine
+        stats["sectors"] = mine if mode != "rows" else f"rows {rank}/{world} of every sector"
     dist.reduce(d_map, dst=0, op=dist.ReduceOp.SUM)
     if rank != 0:
         return None

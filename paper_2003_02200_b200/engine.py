@@ -397,6 +397,16 @@ class Context:
                                           d_map, stream, C.byref(st) if want_stats else None))
         return EngineStats.from_c(st) if want_stats else None
 
+    def run_rows(self, d_dem: int, dimy: int, dimx: int, cellsize: float, cfg: RunConfig, part: int,
+                 nparts: int, d_map: int, stream: int = 0, want_stats: bool = False):
+        """All sectors, row block `part` of `nparts` of every sector (row-block
+        sharding across GPUs; the nparts maps sum to the total raw map)."""
+        c = cfg.to_c()
+        st = _lib.StatsC()
+        check(lib.sks_context_run_rows(self._h, d_dem, dimy, dimx, cellsize, C.byref(c), part, nparts, d_map,
+                                       stream, C.byref(st) if want_stats else None))
+        return EngineStats.from_c(st) if want_stats else None
+
     def scale(self, d_map: int, n: int, ns: int, cellsize: float, units: int, stream: int = 0):
         check(lib.sks_context_scale(self._h, d_map, n, ns, cellsize, units, stream))
 

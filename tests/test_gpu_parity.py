@@ -356,6 +356,52 @@ def test_device_entry_rejects_non_finite():
                         stream=torch.cuda.current_stream().cuda_stream)
 
 
+@pytest.mark.parametrize("nparts", [1, 2, 3, 8])
+def test_row_block_parts_sum_to_total(ora, nparts):
+    """Row-block sharding (the multi-GPU split): the nparts partial maps of
+    Context.run_rows sum to the reference's total_viewshed_raw (per-cell sum
+    order differs, so within 1e-12 relative; one part is bit-exact)."""
+    import torch
+
+    vals = sk.make_synthetic(sk.SyntheticKind.Fractal, 72, 60, 10.0, 9).values
+    cfg = sk.RunConfig(ns=24, h0=1.5, units=sk.Units.SquareMeters)
+    ref = ora.total_viewshed(vals, 10.0, 24, 1.5, raw=True)
+    ctx = sk.Context(0)
+    d_dem = torch.from_numpy(vals).cuda()
+    total = np.zeros(vals.shape, np.float64)
+    st = torch.cuda.current_stream().cuda_stream
+    for part in range(nparts):
+        d_map = torch.zeros(vals.shape, dtype=torch.float64, device="cuda")
+        ctx.run_rows(d_dem.data_ptr(), *vals.shape, 10.0, cfg, part, nparts, d_map.data_ptr(), stream=st)
+        torch.cuda.synchronize()
+        total += d_map.cpu().numpy()
+    if nparts == 1:
+        assert np.array_equal(b64(total), b64(ref))
+    else:
+        np.testing.assert_allclose(total, ref, rtol=1e-12, atol=0)
+
+
+def test_row_blocks_balance_exact_work():
+    """Every target of every sector is owned by exactly one part."""
+    import torch
+
+    vals = sk.make_synthetic(sk.SyntheticKind.Fractal, 300, 300, 10.0, 9).values
+    cfg = sk.RunConfig(ns=36, h0=1.5)
+    ctx = sk.Context(0)
+    d_dem = torch.from_numpy(vals).cuda()
+    d_map = torch.zeros(vals.shape, dtype=torch.float64, device="cuda")
+    st = torch.cuda.current_stream().cuda_stream
+    work = []
+    for part in range(4):
+        es = ctx.run_rows(d_dem.data_ptr(), 300, 300, 10.0, cfg, part, 4, d_map.data_ptr(), stream=st,
+                          want_stats=True)
+        work.append(es.target_evals)
+    assert sum(work) == sk.total_target_evals(36, 300, 300, 10.0, None)
+    # blocks balance exact work plus a per-task term (short rows cost more
+    # per target), so the exact work alone is only roughly equal
+    assert min(work) > 0 and max(work) / (sum(work) / 4) < 1.4, work
+
+
 def test_total_viewshed_units_and_scale(ora):
     dem = sk.make_synthetic(sk.SyntheticKind.SmoothedNoise, 16, 16, 10.0, 1)
     for units in (sk.Units.SquareMeters, sk.Units.SquareKilometers):
