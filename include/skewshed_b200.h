@@ -30,7 +30,8 @@ typedef enum {
   SKS_OUT_OF_RANGE = 2,     /* std::out_of_range */
   SKS_CUDA_ERROR = 3,
   SKS_NCCL_ERROR = 4,
-  SKS_INTERNAL = 5 /* std::runtime_error */
+  SKS_INTERNAL = 5, /* std::runtime_error */
+  SKS_FORMAT_ERROR = 6 /* GridFormatError (ascii_grid.hpp:15-18) */
 } sks_status;
 
 enum { SKS_UNITS_M2 = 0, SKS_UNITS_KM2 = 1 };
@@ -211,6 +212,41 @@ sks_status sks_context_total_viewshed(sks_context* ctx, const float* dem,
                                       int dimy, int dimx, double cellsize,
                                       const sks_run_config* cfg, int raw,
                                       double* out, sks_stats* stats);
+
+/* ---- ESRI ASCII grid I/O: the DEM load / map output entry points
+   (ascii_grid.hpp:15-31). Host code; the body is parsed and written by all
+   host threads. ---------------------------------------------------------- */
+typedef struct {
+  int nrows, ncols;
+  double xllcorner, yllcorner, cellsize;
+  int has_nodata; /* NODATA_value present */
+  float nodata;
+} sks_grid_header;
+
+typedef struct sks_ascii_grid sks_ascii_grid;
+
+/* read_ascii_grid(path) (ascii_grid.cpp:198-204): SKS_FORMAT_ERROR with the
+   reference's "source:line:col: ..." message on bad input. */
+sks_status sks_ascii_grid_read(const char* path, sks_ascii_grid** out);
+/* read_ascii_grid(istream, source_name) (ascii_grid.cpp:110-196) on an
+   in-memory text of len bytes. */
+sks_status sks_ascii_grid_parse(const char* text, size_t len, const char* source_name,
+                                sks_ascii_grid** out);
+sks_status sks_ascii_grid_header(const sks_ascii_grid* grid, sks_grid_header* out);
+/* copies the nrows*ncols cell values (float32, north row first) */
+sks_status sks_ascii_grid_values(const sks_ascii_grid* grid, float* out);
+void sks_ascii_grid_free(sks_ascii_grid* grid);
+
+/* write_ascii_grid(Dem, path) (ascii_grid.cpp:225-245); header fields from
+   hdr (nodata written when has_nodata). */
+sks_status sks_write_ascii_grid_dem(const char* path, const float* values,
+                                    const sks_grid_header* hdr);
+/* write_ascii_grid(VsGrid, out_units, cellsize, origin, path)
+   (ascii_grid.cpp:247-272): values in units_in, written in units_out. */
+sks_status sks_write_ascii_grid_vs(const char* path, const double* values, int nrows,
+                                   int ncols, int units_in, int units_out,
+                                   double cellsize, double xllcorner,
+                                   double yllcorner);
 
 #ifdef __cplusplus
 }

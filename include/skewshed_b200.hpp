@@ -15,12 +15,16 @@
 
 #include <cmath>
 #include <cstdint>
+#include <filesystem>
 #include <functional>
+#include <istream>
+#include <iterator>
 #include <numbers>
 #include <optional>
 #include <span>
 #include <stdexcept>
 #include <string>
+#include <string_view>
 #include <utility>
 #include <vector>
 
@@ -28,10 +32,16 @@
 
 namespace skewshed_b200 {
 
+// ascii_grid.hpp:15-18
+class GridFormatError : public std::runtime_error {
+  using std::runtime_error::runtime_error;
+};
+
 inline void check(sks_status s) {
   if (s == SKS_OK) return;
   std::string msg = sks_last_error();
   if (s == SKS_INVALID_ARGUMENT) throw std::invalid_argument(msg);
+  if (s == SKS_FORMAT_ERROR) throw GridFormatError(msg);
   if (s == SKS_OUT_OF_RANGE) throw std::out_of_range(msg);
   throw std::runtime_error(msg);
 }
@@ -72,10 +82,18 @@ enum class ScanDir { Forward = SKS_SCAN_FORWARD, Backward = SKS_SCAN_BACKWARD };
 enum class AxisOp { Transpose = 0, FlipCols = 1, FlipRows = 2 };
 inline constexpr int kNoDistanceCap = SKS_NO_DISTANCE_CAP;
 
+// dem.hpp:13-17
+struct GridOrigin {
+  double easting = 0.0;
+  double northing = 0.0;
+  std::string zone;
+};
+
 struct Dem {
   Grid<float> values;
   double cellsize = 1.0;
   std::optional<float> nodata;
+  GridOrigin origin;
   int dimy() const { return values.rows(); }
   int dimx() const { return values.cols(); }
 };
@@ -269,6 +287,55 @@ inline void unskew_accumulate(const Grid<double>& skw_vs, const SectorPlan& plan
   }
   check(sks_unskew_accumulate(skw_vs.data().data(), skw_vs.rows(), skw_vs.cols(), plan.sector_index,
                               plan.ns, plan.src_rows, plan.src_cols, device, out.data().data()));
+}
+
+// ---- ESRI ASCII grid I/O (ascii_grid.hpp:20-31) ----
+
+namespace detail {
+inline Dem take_ascii_grid(sks_ascii_grid* g) {
+  sks_grid_header h{};
+  sks_status s = sks_ascii_grid_header(g, &h);
+  Dem dem;
+  if (s == SKS_OK) {
+    dem.values.reset(h.nrows, h.ncols);
+    s = sks_ascii_grid_values(g, dem.values.data().data());
+  }
+  sks_ascii_grid_free(g);
+  check(s);
+  dem.cellsize = h.cellsize;
+  dem.origin.easting = h.xllcorner;
+  dem.origin.northing = h.yllcorner;
+  if (h.has_nodata) dem.nodata = h.nodata;
+  return dem;
+}
+}  // namespace detail
+
+inline Dem read_ascii_grid(const std::filesystem::path& path) {
+  sks_ascii_grid* g = nullptr;
+  check(sks_ascii_grid_read(path.string().c_str(), &g));
+  return detail::take_ascii_grid(g);
+}
+
+inline Dem read_ascii_grid(std::istream& in, std::string_view source_name) {
+  const std::string text((std::istreambuf_iterator<char>(in)), std::istreambuf_iterator<char>());
+  const std::string src(source_name);
+  sks_ascii_grid* g = nullptr;
+  check(sks_ascii_grid_parse(text.data(), text.size(), src.c_str(), &g));
+  return detail::take_ascii_grid(g);
+}
+
+inline void write_ascii_grid(const Dem& dem, const std::filesystem::path& path) {
+  const sks_grid_header h{dem.dimy(), dem.dimx(), dem.origin.easting, dem.origin.northing,
+                          dem.cellsize, dem.nodata ? 1 : 0, dem.nodata.value_or(0.0f)};
+  check(sks_write_ascii_grid_dem(path.string().c_str(), dem.values.data().data(), &h));
+}
+
+inline void write_ascii_grid(const VsGrid& grid, Units out_units, double cellsize,
+                             const GridOrigin& origin, const std::filesystem::path& path) {
+  check(sks_write_ascii_grid_vs(path.string().c_str(), grid.values.data().data(), grid.values.rows(),
+                                grid.values.cols(), static_cast<int>(grid.units),
+                                static_cast<int>(out_units), cellsize, origin.easting,
+                                origin.northing));
 }
 
 }  // namespace skewshed_b200

@@ -20,6 +20,9 @@
 #include <thread>
 #include <vector>
 
+#include <sstream>
+
+#include "skewshed/ascii_grid.hpp"
 #include "skewshed/dem.hpp"
 #include "skewshed/engine.hpp"
 #include "skewshed/oracle.hpp"
@@ -349,6 +352,68 @@ int ref_sample_scan(const float* dem, int dimy, int dimx, int ns, double h0,
                        .count();
     *target_evals_out = static_cast<double>(evals.load());
   });
+}
+
+// read_ascii_grid(istream, source_name) (ascii_grid.cpp:110-196). Returns 0,
+// 3 for GridFormatError (message in ref_last_error) or 4 for another error.
+int ref_parse_ascii_grid(const char* text, size_t len, const char* source, int* nrows, int* ncols,
+                         double* hdr /* xll, yll, cellsize */, int* has_nodata, float* nodata,
+                         float* values, long long cap) {
+  try {
+    std::istringstream in(std::string(text, len));
+    Dem dem = read_ascii_grid(in, source);
+    *nrows = dem.dimy();
+    *ncols = dem.dimx();
+    hdr[0] = dem.origin.easting;
+    hdr[1] = dem.origin.northing;
+    hdr[2] = dem.cellsize;
+    *has_nodata = dem.nodata.has_value() ? 1 : 0;
+    *nodata = dem.nodata.value_or(0.0f);
+    const long long n = static_cast<long long>(dem.dimy()) * dem.dimx();
+    if (values && n <= cap) std::memcpy(values, dem.values.data().data(), sizeof(float) * n);
+    return 0;
+  } catch (const GridFormatError& e) {
+    g_err = e.what();
+    return 3;
+  } catch (const std::exception& e) {
+    g_err = e.what();
+    return 4;
+  }
+}
+
+// write_ascii_grid(Dem, path) (ascii_grid.cpp:225-245)
+int ref_write_ascii_grid_dem(const char* path, const float* v, int nrows, int ncols, double xll, double yll,
+                             double cellsize, int has_nodata, float nodata) {
+  try {
+    Dem dem = make_dem(v, nrows, ncols, cellsize);
+    dem.origin.easting = xll;
+    dem.origin.northing = yll;
+    if (has_nodata) dem.nodata = nodata;
+    write_ascii_grid(dem, path);
+    return 0;
+  } catch (const std::exception& e) {
+    g_err = e.what();
+    return 4;
+  }
+}
+
+// write_ascii_grid(VsGrid, out_units, cellsize, origin, path) (ascii_grid.cpp:247-272)
+int ref_write_ascii_grid_vs(const char* path, const double* v, int nrows, int ncols, int units_in, int units_out,
+                            double cellsize, double xll, double yll) {
+  try {
+    VsGrid vs;
+    vs.units = units_in ? Units::SquareKilometers : Units::SquareMeters;
+    vs.values.reset(nrows, ncols, 0.0);
+    std::memcpy(vs.values.data().data(), v, sizeof(double) * static_cast<size_t>(nrows) * ncols);
+    GridOrigin o;
+    o.easting = xll;
+    o.northing = yll;
+    write_ascii_grid(vs, units_out ? Units::SquareKilometers : Units::SquareMeters, cellsize, o, path);
+    return 0;
+  } catch (const std::exception& e) {
+    g_err = e.what();
+    return 4;
+  }
 }
 
 }  // extern "C"

@@ -5,7 +5,8 @@ hand-written sm_100a kernels inside libskewshed_b200.so, reached through its C
 ABI (include/skewshed_b200.h). This package is the host-side mirror of the
 reference's C++ API (proj/include/skewshed/*.hpp) plus the multi-GPU sharding.
 """
-from .engine import (AxisOp, Context, Dem, EngineStats, RunConfig, ScanDir, SectorPlan, SectorResult,
+from .engine import (AxisOp, Context, Dem, EngineStats, GridFormatError, GridOrigin, parse_ascii_grid,
+                     read_ascii_grid, write_ascii_grid, RunConfig, ScanDir, SectorPlan, SectorResult,
                      SkwGrid, SyntheticKind, Units, VsGrid, accumulate_into, area_scale, area_scale_factor,
                      build_sector_sdem, build_skw, convert_units, device_count, distance_cap_cells,
                      kNoDistanceCap, linear_viewshed_row, make_synthetic, partition_sectors, plan_sector,
@@ -14,7 +15,8 @@ from .engine import (AxisOp, Context, Dem, EngineStats, RunConfig, ScanDir, Sect
                      unskew_accumulate, validate)
 
 __all__ = [
-    "AxisOp", "Context", "Dem", "EngineStats", "RunConfig", "ScanDir", "SectorPlan", "SectorResult",
+    "AxisOp", "Context", "Dem", "EngineStats", "GridFormatError", "GridOrigin", "parse_ascii_grid",
+    "read_ascii_grid", "write_ascii_grid", "RunConfig", "ScanDir", "SectorPlan", "SectorResult",
     "SkwGrid", "SyntheticKind", "Units", "VsGrid", "accumulate_into", "area_scale", "area_scale_factor",
     "build_sector_sdem", "build_skw", "convert_units", "device_count", "distance_cap_cells",
     "kNoDistanceCap", "linear_viewshed_row", "make_synthetic", "partition_sectors", "plan_sector",

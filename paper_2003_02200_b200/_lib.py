@@ -30,6 +30,7 @@ SKS_OUT_OF_RANGE = 2
 SKS_CUDA_ERROR = 3
 SKS_NCCL_ERROR = 4
 SKS_INTERNAL = 5
+SKS_FORMAT_ERROR = 6
 NO_CAP = 2147483647
 
 
@@ -67,6 +68,11 @@ _ip = C.POINTER(C.c_int)
 _dp = C.POINTER(C.c_double)
 
 # Every symbol declared in include/skewshed_b200.h, with its signature.
+class GridHeaderC(C.Structure):
+    _fields_ = [("nrows", C.c_int), ("ncols", C.c_int), ("xllcorner", C.c_double), ("yllcorner", C.c_double),
+                ("cellsize", C.c_double), ("has_nodata", C.c_int), ("nodata", C.c_float)]
+
+
 SIGNATURES = {
     "sks_last_error": (C.c_char_p, []),
     "sks_version": (C.c_char_p, []),
@@ -98,6 +104,14 @@ SIGNATURES = {
     "sks_context_destroy": (None, [_vp]),
     "sks_context_run_sectors": (C.c_int, [_vp, _vp, C.c_int, C.c_int, C.c_double, C.POINTER(RunConfigC),
                                           _i32p, C.c_int, _vp, _vp, C.POINTER(StatsC)]),
+    "sks_ascii_grid_read": (C.c_int, [C.c_char_p, C.POINTER(_vp)]),
+    "sks_ascii_grid_parse": (C.c_int, [C.c_char_p, C.c_size_t, C.c_char_p, C.POINTER(_vp)]),
+    "sks_ascii_grid_header": (C.c_int, [_vp, C.POINTER(GridHeaderC)]),
+    "sks_ascii_grid_values": (C.c_int, [_vp, _vp]),
+    "sks_ascii_grid_free": (None, [_vp]),
+    "sks_write_ascii_grid_dem": (C.c_int, [C.c_char_p, _vp, C.POINTER(GridHeaderC)]),
+    "sks_write_ascii_grid_vs": (C.c_int, [C.c_char_p, _vp, C.c_int, C.c_int, C.c_int, C.c_int, C.c_double,
+                                          C.c_double, C.c_double]),
     "sks_context_run_rows": (C.c_int, [_vp, _vp, C.c_int, C.c_int, C.c_double, C.POINTER(RunConfigC),
                                        C.c_int, C.c_int, _vp, _vp, C.POINTER(StatsC)]),
     "sks_context_scale": (C.c_int, [_vp, _vp, C.c_longlong, C.c_int, C.c_double, C.c_int, _vp]),
@@ -115,6 +129,10 @@ def last_error() -> str:
     return lib.sks_last_error().decode()
 
 
+class GridFormatError(RuntimeError):
+    """ascii_grid.hpp:15-18: malformed grid text (message carries source:line:col)."""
+
+
 def check(status: int) -> None:
     """Maps sks_status to the reference's exception types."""
     if status == SKS_OK:
@@ -124,6 +142,8 @@ def check(status: int) -> None:
         raise ValueError(msg)
     if status == SKS_OUT_OF_RANGE:
         raise IndexError(msg)
+    if status == SKS_FORMAT_ERROR:
+        raise GridFormatError(msg)
     raise RuntimeError(msg)
 
 

@@ -27,6 +27,7 @@
 
 #include "../../include/skewshed_b200.h"
 #include "sks_device.cuh"
+#include "sks_io.hpp"
 #include "sks_plan.hpp"
 
 namespace sks {
@@ -60,6 +61,9 @@ sks_status guarded(Fn&& fn) {
   } catch (const std::out_of_range& e) {
     g_error = e.what();
     return SKS_OUT_OF_RANGE;
+  } catch (const GridFormatError& e) {
+    g_error = e.what();
+    return SKS_FORMAT_ERROR;
   } catch (const CudaError& e) {
     g_error = e.what();
     return SKS_CUDA_ERROR;
@@ -1043,6 +1047,68 @@ sks_status sks_unskew_accumulate(const double* skw_vs, int skw_rows, int cols, i
                "launch unskew");
     cuda_check(cudaMemcpyAsync(out, dmap.p, nm * sizeof(double), cudaMemcpyDeviceToHost, st), "D2H");
     cuda_check(cudaStreamSynchronize(st), "sync");
+  });
+}
+
+// ---- ESRI ASCII grid I/O (sks_io.cpp) ----------------------------------
+
+struct sks_ascii_grid {
+  AsciiGrid g;
+};
+
+sks_status sks_ascii_grid_read(const char* path, sks_ascii_grid** out) {
+  return guarded([&] {
+    if (!path || !out) throw std::invalid_argument("null argument");
+    *out = nullptr;
+    auto h = std::make_unique<sks_ascii_grid>();
+    h->g = read_ascii_grid_file(path);
+    *out = h.release();
+  });
+}
+
+sks_status sks_ascii_grid_parse(const char* text, size_t len, const char* source_name,
+                                sks_ascii_grid** out) {
+  return guarded([&] {
+    if ((!text && len) || !out) throw std::invalid_argument("null argument");
+    *out = nullptr;
+    auto h = std::make_unique<sks_ascii_grid>();
+    h->g = parse_ascii_grid(text ? text : "", len, source_name ? source_name : "<input>");
+    *out = h.release();
+  });
+}
+
+sks_status sks_ascii_grid_header(const sks_ascii_grid* grid, sks_grid_header* out) {
+  return guarded([&] {
+    if (!grid || !out) throw std::invalid_argument("null argument");
+    const AsciiGrid& g = grid->g;
+    *out = sks_grid_header{g.nrows, g.ncols, g.xllcorner, g.yllcorner, g.cellsize, g.has_nodata ? 1 : 0, g.nodata};
+  });
+}
+
+sks_status sks_ascii_grid_values(const sks_ascii_grid* grid, float* out) {
+  return guarded([&] {
+    if (!grid || !out) throw std::invalid_argument("null argument");
+    std::copy(grid->g.values.begin(), grid->g.values.end(), out);
+  });
+}
+
+void sks_ascii_grid_free(sks_ascii_grid* grid) { delete grid; }
+
+sks_status sks_write_ascii_grid_dem(const char* path, const float* values, const sks_grid_header* hdr) {
+  return guarded([&] {
+    if (!path || !values || !hdr) throw std::invalid_argument("null argument");
+    write_ascii_grid_dem(path, values, hdr->nrows, hdr->ncols, hdr->xllcorner, hdr->yllcorner, hdr->cellsize,
+                         hdr->has_nodata ? &hdr->nodata : nullptr);
+  });
+}
+
+sks_status sks_write_ascii_grid_vs(const char* path, const double* values, int nrows, int ncols, int units_in,
+                                   int units_out, double cellsize, double xllcorner, double yllcorner) {
+  return guarded([&] {
+    if (!path || !values) throw std::invalid_argument("null argument");
+    // convert_units (dem.cpp:24-34)
+    const double factor = units_in == units_out ? 1.0 : (units_out == SKS_UNITS_KM2 ? 1e-6 : 1e6);
+    write_ascii_grid_vs(path, values, nrows, ncols, factor, xllcorner, yllcorner, cellsize);
   });
 }
 

@@ -1,0 +1,37 @@
+// ESRI ASCII grid I/O (host C++): reference ascii_grid.hpp:15-31.
+#pragma once
+
+#include <stdexcept>
+#include <string>
+#include <vector>
+
+namespace sks {
+
+// read_ascii_grid's failure type (ascii_grid.hpp:15-18): message with the
+// offending source:line:col.
+class GridFormatError : public std::runtime_error {
+  using std::runtime_error::runtime_error;
+};
+
+struct AsciiGrid {
+  int nrows = 0, ncols = 0;
+  double xllcorner = 0.0, yllcorner = 0.0, cellsize = 1.0;
+  bool has_nodata = false;
+  float nodata = 0.f;
+  std::vector<float> values;  // nrows * ncols, north row first
+};
+
+// read_ascii_grid(istream, source_name) / read_ascii_grid(path)
+AsciiGrid parse_ascii_grid(const char* buf, size_t n, const std::string& source);
+AsciiGrid read_ascii_grid_file(const std::string& path);
+
+// write_ascii_grid(Dem, path): header "%.10g", cells "%.9g", optional NODATA_value
+void write_ascii_grid_dem(const std::string& path, const float* values, int nrows, int ncols, double xll,
+                          double yll, double cellsize, const float* nodata);
+// write_ascii_grid(VsGrid, units, cellsize, origin, path): cells "%.10g" of
+// value * factor (factor 1 when the units already match, else
+// convert_units' 1e-6 / 1e6, dem.cpp:24-34)
+void write_ascii_grid_vs(const std::string& path, const double* values, int nrows, int ncols, double factor,
+                         double xll, double yll, double cellsize);
+
+}  // namespace sks

@@ -72,11 +72,19 @@ class RunConfig:
 
 
 @dataclass
+class GridOrigin:
+    """dem.hpp:13-17: lower-left corner of the grid (ESRI xll/yllcorner)."""
+    easting: float = 0.0
+    northing: float = 0.0
+
+
+@dataclass
 class Dem:
     """dem.hpp:26-37: float32 elevations, row 0 = north, col 0 = west."""
     values: np.ndarray
     cellsize: float = 1.0
     nodata: Optional[float] = None
+    origin: GridOrigin = field(default_factory=GridOrigin)
 
     def __post_init__(self):
         self.values = np.ascontiguousarray(self.values, dtype=np.float32)
@@ -429,3 +437,53 @@ class Context:
 
 def device_count() -> int:
     return int(lib.sks_device_count())
+
+
+# ---- ESRI ASCII grid I/O (ascii_grid.hpp:15-31) ----------------------------
+
+GridFormatError = _lib.GridFormatError
+
+
+def _grid_from_handle(h) -> Dem:
+    try:
+        hdr = _lib.GridHeaderC()
+        check(lib.sks_ascii_grid_header(h, C.byref(hdr)))
+        vals = np.empty((hdr.nrows, hdr.ncols), np.float32)
+        check(lib.sks_ascii_grid_values(h, vals.ctypes.data))
+    finally:
+        lib.sks_ascii_grid_free(h)
+    return Dem(vals, hdr.cellsize, float(hdr.nodata) if hdr.has_nodata else None,
+               GridOrigin(hdr.xllcorner, hdr.yllcorner))
+
+
+def read_ascii_grid(path) -> Dem:
+    """read_ascii_grid(path) (ascii_grid.cpp:198-204); GridFormatError on bad input."""
+    h = C.c_void_p()
+    check(lib.sks_ascii_grid_read(str(path).encode(), C.byref(h)))
+    return _grid_from_handle(h)
+
+
+def parse_ascii_grid(text, source_name: str = "<input>") -> Dem:
+    """read_ascii_grid(istream, source_name) (ascii_grid.cpp:110-196) on text/bytes."""
+    data = text.encode() if isinstance(text, str) else bytes(text)
+    h = C.c_void_p()
+    check(lib.sks_ascii_grid_parse(data, len(data), source_name.encode(), C.byref(h)))
+    return _grid_from_handle(h)
+
+
+def write_ascii_grid(grid, path, units: Optional["Units"] = None, cellsize: Optional[float] = None,
+                     origin: Optional[GridOrigin] = None) -> None:
+    """write_ascii_grid for a Dem (ascii_grid.cpp:225-245) or a VsGrid in
+    `units` with the source DEM's cellsize and origin (:247-272)."""
+    if isinstance(grid, Dem):
+        hdr = _lib.GridHeaderC(grid.dimy(), grid.dimx(), grid.origin.easting, grid.origin.northing,
+                               grid.cellsize, 1 if grid.nodata is not None else 0,
+                               float(grid.nodata) if grid.nodata is not None else 0.0)
+        check(lib.sks_write_ascii_grid_dem(str(path).encode(), grid.values.ctypes.data, C.byref(hdr)))
+        return
+    vals = np.ascontiguousarray(grid.values, np.float64)
+    o = origin or GridOrigin()
+    out_units = grid.units if units is None else units
+    check(lib.sks_write_ascii_grid_vs(str(path).encode(), vals.ctypes.data, vals.shape[0], vals.shape[1],
+                                      int(grid.units), int(out_units), float(cellsize if cellsize else 1.0),
+                                      o.easting, o.northing))

@@ -77,3 +77,39 @@ def test_cpp_facade_header_compiles(tmp_path):
     r = subprocess.run(["g++", "-std=c++20", "-fsyntax-only", "-I", os.path.join(ROOT, "include"), str(src)],
                        capture_output=True, text=True)
     assert r.returncode == 0, r.stderr
+
+
+def test_cpp_facade_ascii_grid_round_trip(tmp_path):
+    """The C++ facade's read/write_ascii_grid (ascii_grid.hpp:20-31) linked
+    against the shipped library: host-only entry points, no GPU needed."""
+    src = tmp_path / "t.cpp"
+    src.write_text(r'''
+#include "skewshed_b200.hpp"
+#include <cstdio>
+#include <sstream>
+namespace sk = skewshed_b200;
+int main(int, char** argv) {
+  std::istringstream in("ncols 3\nnrows 2\nxllcorner 5\nyllcorner 6\ncellsize 2.5\nNODATA_value -1\n1 2 3\n4 -1 6\n");
+  sk::Dem d = sk::read_ascii_grid(in, "mem");
+  if (d.dimy() != 2 || d.dimx() != 3 || d.values(1, 2) != 6.0f || !d.nodata || *d.nodata != -1.0f) return 1;
+  if (d.origin.easting != 5.0 || d.origin.northing != 6.0 || d.cellsize != 2.5) return 2;
+  sk::write_ascii_grid(d, argv[1]);
+  sk::Dem e = sk::read_ascii_grid(argv[1]);
+  if (!(e.values == d.values) || e.origin.northing != 6.0) return 3;
+  std::istringstream bad("ncols 2\nnrows 2\nxllcorner 0\nyllcorner 0\ncellsize 1\n1 2\n3 q\n");
+  try { sk::read_ascii_grid(bad, "bad"); return 4; }
+  catch (const sk::GridFormatError& ex) { std::puts(ex.what()); }
+  sk::VsGrid vs{sk::Grid<double>(2, 3, 1.5e6), sk::Units::SquareMeters};
+  sk::write_ascii_grid(vs, sk::Units::SquareKilometers, 2.5, d.origin, argv[2]);
+  return 0;
+}
+''')
+    exe = tmp_path / "t"
+    libdir = os.path.join(ROOT, "paper_2003_02200_b200")
+    r = subprocess.run(["g++", "-std=c++20", "-I", os.path.join(ROOT, "include"), str(src), "-o", str(exe),
+                        "-L", libdir, "-lskewshed_b200", f"-Wl,-rpath,{libdir}"], capture_output=True, text=True)
+    assert r.returncode == 0, r.stderr
+    r = subprocess.run([str(exe), str(tmp_path / "d.asc"), str(tmp_path / "v.asc")], capture_output=True, text=True)
+    assert r.returncode == 0, (r.returncode, r.stderr)
+    assert r.stdout.strip() == "bad:7:3: expected a number for cell value, got 'q'"
+    assert (tmp_path / "v.asc").read_text().splitlines()[-1] == "1.5 1.5 1.5"
