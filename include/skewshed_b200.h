@@ -248,6 +248,48 @@ sks_status sks_write_ascii_grid_vs(const char* path, const double* values, int n
                                    double cellsize, double xllcorner,
                                    double yllcorner);
 
+/* ---- Rotational-sweep viewshed on the GPU: the reference's independent
+   oracle (oracle.hpp:10-68) — rays rasterised per azimuth in unskewed grid
+   space, Euclidean distances, no relocation. Bit-identical to oracle.cpp
+   (the per-azimuth ray tables are computed on the host with the same glibc
+   calls). max_distance: metres, 0 = unlimited. Areas in m^2. --------------- */
+enum { SKS_REFERENCE_CELL_GUARD = 65536 }; /* kReferenceCellGuard (oracle.hpp:62) */
+
+/* singular_viewshed(dem, i0, j0, h0, ns, max_distance) (oracle.cpp:108-129):
+   SKS_OUT_OF_RANGE for an observer outside the grid, SKS_INVALID_ARGUMENT
+   for a bad ns. */
+sks_status sks_singular_viewshed(const float* dem, int dimy, int dimx, double cellsize, int i, int j,
+                                 double h0, int ns, double max_distance, int device, double* area);
+
+/* multi_viewshed(dem, povs, h0, ns, max_distance) (oracle.cpp:131-141):
+   povs = npovs (i, j) pairs. Any of pov_area (npovs), grid (dimy*dimx,
+   nonzero only at observers, summed in list order) and total_area may be
+   null. */
+sks_status sks_multi_viewshed(const float* dem, int dimy, int dimx, double cellsize, const int* povs,
+                              int npovs, double h0, int ns, double max_distance, int device,
+                              double* pov_area, double* grid, double* total_area);
+
+/* total_viewshed_reference(dem, cfg, force) (oracle.cpp:143-194): the
+   singular viewshed of every cell in cfg->units; grids above
+   SKS_REFERENCE_CELL_GUARD cells are refused (SKS_INTERNAL, the reference's
+   runtime_error) unless force. nodata may be null. */
+sks_status sks_total_viewshed_reference(const float* dem, int dimy, int dimx, double cellsize,
+                                        const float* nodata, const sks_run_config* cfg, int force,
+                                        double* out);
+
+/* select_axis_point_set (oracle.cpp:62-71): *count cells of the ray, the
+   first min(cap, *count) written to ij as (i, j) pairs. Host only. */
+sks_status sks_axis_point_set(int dimy, int dimx, int i0, int j0, double azimuth_deg, int* ij, int cap,
+                              int* count);
+
+/* random_povs(dem, count, seed) (cli.cpp:207-221): count (i, j) pairs. */
+sks_status sks_random_povs(int dimy, int dimx, int count, uint32_t seed, int* ij);
+
+/* write_heatmap(grid, path, palette) (heatmap.cpp:11-56): binary PGM / PPM of
+   the min-max normalised map. Host code. */
+enum { SKS_PALETTE_GRAY = 0, SKS_PALETTE_BLUE_RED = 1 };
+sks_status sks_write_heatmap(const char* path, const double* values, int rows, int cols, int palette);
+
 #ifdef __cplusplus
 }
 #endif

@@ -16,6 +16,7 @@
 #include <cstdint>
 #include <cstring>
 #include <exception>
+#include <optional>
 #include <string>
 #include <thread>
 #include <vector>
@@ -25,6 +26,7 @@
 #include "skewshed/ascii_grid.hpp"
 #include "skewshed/dem.hpp"
 #include "skewshed/engine.hpp"
+#include "skewshed/heatmap.hpp"
 #include "skewshed/oracle.hpp"
 #include "skewshed/scan.hpp"
 #include "skewshed/skew.hpp"
@@ -414,6 +416,71 @@ int ref_write_ascii_grid_vs(const char* path, const double* v, int nrows, int nc
     g_err = e.what();
     return 4;
   }
+}
+
+// oracle.cpp:108-129 singular_viewshed (max_distance 0 = unset)
+int ref_singular_viewshed(const float* dem, int dimy, int dimx, double cellsize, int i, int j, double h0,
+                          int ns, double max_distance, double* area) {
+  return guarded([&] {
+    Dem d = make_dem(dem, dimy, dimx, cellsize);
+    std::optional<double> md;
+    if (max_distance != 0.0) md = max_distance;
+    *area = oracle::singular_viewshed(d, i, j, h0, ns, md);
+  });
+}
+
+// oracle.cpp:131-141 multi_viewshed: grid (dimy*dimx) and total
+int ref_multi_viewshed(const float* dem, int dimy, int dimx, double cellsize, const int* povs, int npovs,
+                       double h0, int ns, double max_distance, double* grid, double* total) {
+  return guarded([&] {
+    Dem d = make_dem(dem, dimy, dimx, cellsize);
+    std::vector<oracle::GridPoint> p(static_cast<size_t>(npovs));
+    for (int t = 0; t < npovs; ++t) p[t] = {povs[2 * t], povs[2 * t + 1]};
+    std::optional<double> md;
+    if (max_distance != 0.0) md = max_distance;
+    oracle::MultiViewshed mv = oracle::multi_viewshed(d, p, h0, ns, md);
+    std::memcpy(grid, mv.grid.values.data().data(), sizeof(double) * mv.grid.values.size());
+    *total = mv.total_area;
+  });
+}
+
+// oracle.cpp:143-194 total_viewshed_reference with the caller's units/force/
+// nodata (error paths included)
+int ref_total_viewshed_reference(const float* dem, int dimy, int dimx, double cellsize, const float* nodata,
+                                 int ns, double h0, double max_distance, int units, int force, double* out) {
+  return guarded([&] {
+    Dem d = make_dem(dem, dimy, dimx, cellsize);
+    if (nodata) d.nodata = *nodata;
+    RunConfig cfg = make_cfg(ns, h0, 1, 0.0, units);
+    if (max_distance != 0.0) cfg.max_distance = max_distance;
+    cfg.workers = std::max(1u, std::thread::hardware_concurrency());
+    VsGrid g = oracle::total_viewshed_reference(d, cfg, force != 0);
+    std::memcpy(out, g.values.data().data(), sizeof(double) * g.values.size());
+  });
+}
+
+// oracle.cpp:62-71 select_axis_point_set
+int ref_axis_point_set(int dimy, int dimx, int i0, int j0, double azimuth_deg, int* ij, int cap, int* count) {
+  return guarded([&] {
+    Dem d;
+    d.values.reset(dimy, dimx, 0.0f);
+    auto pts = oracle::select_axis_point_set(d, i0, j0, azimuth_deg);
+    *count = static_cast<int>(pts.size());
+    for (int t = 0; t < std::min(cap, *count); ++t) {
+      ij[2 * t] = pts[t].i;
+      ij[2 * t + 1] = pts[t].j;
+    }
+  });
+}
+
+// heatmap.cpp:11-56 write_heatmap
+int ref_write_heatmap(const char* path, const double* v, int rows, int cols, int palette) {
+  return guarded([&] {
+    VsGrid g;
+    g.values.reset(rows, cols, 0.0);
+    if (g.values.size()) std::memcpy(g.values.data().data(), v, sizeof(double) * g.values.size());
+    write_heatmap(g, path, palette ? Palette::BlueRed : Palette::Gray);
+  });
 }
 
 }  // extern "C"

@@ -5,7 +5,7 @@ hand-written sm_100a kernels inside libskewshed_b200.so, reached through its C
 ABI (include/skewshed_b200.h). This package is the host-side mirror of the
 reference's C++ API (proj/include/skewshed/*.hpp) plus the multi-GPU sharding.
 """
-from .engine import (AxisOp, Context, Dem, EngineStats, GridFormatError, GridOrigin, parse_ascii_grid,
+from .engine import (AxisOp, Palette, write_heatmap, Context, Dem, EngineStats, GridFormatError, GridOrigin, parse_ascii_grid,
                      read_ascii_grid, write_ascii_grid, RunConfig, ScanDir, SectorPlan, SectorResult,
                      SkwGrid, SyntheticKind, Units, VsGrid, accumulate_into, area_scale, area_scale_factor,
                      build_sector_sdem, build_skw, convert_units, device_count, distance_cap_cells,
@@ -13,9 +13,10 @@ from .engine import (AxisOp, Context, Dem, EngineStats, GridFormatError, GridOri
                      reduce_ordered, row_ranges, sector_sweep, sector_target_evals, sector_viewshed,
                      shear_params, total_target_evals, total_viewshed, total_viewshed_raw,
                      unskew_accumulate, validate)
+from . import sweep  # noqa: E402  (rotational-sweep oracle API, oracle.hpp)
 
 __all__ = [
-    "AxisOp", "Context", "Dem", "EngineStats", "GridFormatError", "GridOrigin", "parse_ascii_grid",
+    "AxisOp", "Palette", "write_heatmap", "sweep", "Context", "Dem", "EngineStats", "GridFormatError", "GridOrigin", "parse_ascii_grid",
     "read_ascii_grid", "write_ascii_grid", "RunConfig", "ScanDir", "SectorPlan", "SectorResult",
     "SkwGrid", "SyntheticKind", "Units", "VsGrid", "accumulate_into", "area_scale", "area_scale_factor",
     "build_sector_sdem", "build_skw", "convert_units", "device_count", "distance_cap_cells",

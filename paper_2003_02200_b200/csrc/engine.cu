@@ -18,6 +18,7 @@
 #include <map>
 #include <memory>
 #include <mutex>
+#include <numbers>
 #include <numeric>
 #include <sstream>
 #include <stdexcept>
@@ -29,6 +30,7 @@
 #include "sks_device.cuh"
 #include "sks_io.hpp"
 #include "sks_plan.hpp"
+#include "sks_sweep.hpp"
 
 namespace sks {
 
@@ -1109,6 +1111,170 @@ sks_status sks_write_ascii_grid_vs(const char* path, const double* values, int n
     // convert_units (dem.cpp:24-34)
     const double factor = units_in == units_out ? 1.0 : (units_out == SKS_UNITS_KM2 ? 1e-6 : 1e6);
     write_ascii_grid_vs(path, values, nrows, ncols, factor, xllcorner, yllcorner, cellsize);
+  });
+}
+
+}  // extern "C"
+
+// ---- rotational-sweep reference on the GPU (oracle.cpp:74-194) -----------
+
+namespace {
+
+void require_inside(int dimy, int dimx, int i, int j) {  // oracle.cpp:14-21
+  if (i < 0 || i >= dimy || j < 0 || j >= dimx) {
+    std::ostringstream os;
+    os << "observer (" << i << ", " << j << ") outside grid " << dimy << "x" << dimx;
+    throw std::out_of_range(os.str());
+  }
+}
+
+// singular_viewshed (oracle.cpp:108-129) of npov observers — povs (i, j
+// pairs) or, when null, the linear cell indices [0, npov) — times
+// unit_factor, into out[npov] (host). Observers run in batches whose
+// per-azimuth sums fit in ~1 GiB.
+void sweep_areas(sks_context* ctx, const float* dem, int dimy, int dimx, double cellsize, const int* povs,
+                 long long npov, double h0, int ns, double max_distance, double unit_factor, double* out) {
+  if (npov <= 0) return;
+  const double max_cells = max_distance != 0.0 ? max_distance / cellsize : INFINITY;
+  const SweepTable tab = build_sweep_table(ns, dimy, dimx, max_cells);
+  static_assert(sizeof(SweepStep) == sizeof(SweepStepDev), "table layout");
+  ctx->activate();
+  std::lock_guard<std::mutex> lk(ctx->mu);
+  cudaStream_t st = ctx->own_stream;
+  const size_t n = static_cast<size_t>(dimy) * dimx;
+  DevBuf d_tab, d_len, d_povs, d_buf, d_out;
+  ctx->dem.ensure(n * sizeof(float), ctx->device);
+  d_tab.ensure(tab.steps.size() * sizeof(SweepStep), ctx->device);
+  d_len.ensure(tab.len.size() * sizeof(int), ctx->device);
+  d_out.ensure(static_cast<size_t>(npov) * sizeof(double), ctx->device);
+  const long long batch = std::max(1LL, std::min(npov, (1LL << 27) / tab.ndir));
+  d_buf.ensure(static_cast<size_t>(batch) * tab.ndir * sizeof(double), ctx->device);
+  cuda_check(cudaMemcpyAsync(ctx->dem.p, dem, n * sizeof(float), cudaMemcpyHostToDevice, st), "H2D dem");
+  cuda_check(cudaMemcpyAsync(d_tab.p, tab.steps.data(), tab.steps.size() * sizeof(SweepStep),
+                             cudaMemcpyHostToDevice, st),
+             "H2D sweep table");
+  cuda_check(cudaMemcpyAsync(d_len.p, tab.len.data(), tab.len.size() * sizeof(int), cudaMemcpyHostToDevice, st),
+             "H2D sweep lengths");
+  if (povs) {
+    d_povs.ensure(static_cast<size_t>(npov) * sizeof(int2), ctx->device);
+    cuda_check(cudaMemcpyAsync(d_povs.p, povs, static_cast<size_t>(npov) * sizeof(int2), cudaMemcpyHostToDevice, st),
+               "H2D povs");
+  }
+  const double pi_over_ns = std::numbers::pi / ns;
+  for (long long b0 = 0; b0 < npov; b0 += batch) {
+    const int nb = static_cast<int>(std::min(batch, npov - b0));
+    cuda_check(launch_sweep(ctx->dem.as<float>(), dimy, dimx, d_tab.as<SweepStepDev>(), d_len.as<int>(),
+                            tab.stride, tab.ndir, povs ? d_povs.as<int2>() + b0 : nullptr, b0, nb, h0,
+                            d_buf.as<double>(), st),
+               "launch sweep");
+    cuda_check(launch_sweep_sum(d_buf.as<double>(), tab.ndir, nb, pi_over_ns, cellsize, unit_factor,
+                                d_out.as<double>(), b0, st),
+               "launch sweep sum");
+    ctx->launches += 2;
+  }
+  cuda_check(cudaMemcpyAsync(out, d_out.p, static_cast<size_t>(npov) * sizeof(double), cudaMemcpyDeviceToHost, st),
+             "D2H areas");
+  cuda_check(cudaStreamSynchronize(st), "sync sweep");
+}
+
+void require_sector_count(int ns) {  // oracle.cpp:110-112
+  if (ns < 2 || ns % 2 != 0) throw std::invalid_argument("sector count must be an even integer >= 2");
+}
+
+}  // namespace
+
+extern "C" {
+
+sks_status sks_singular_viewshed(const float* dem, int dimy, int dimx, double cellsize, int i, int j, double h0,
+                                 int ns, double max_distance, int device, double* area) {
+  return guarded([&] {
+    if (!dem || !area) throw std::invalid_argument("null argument");
+    require_inside(dimy, dimx, i, j);
+    require_sector_count(ns);
+    const int p[2] = {i, j};
+    sweep_areas(default_context(device), dem, dimy, dimx, cellsize, p, 1, h0, ns, max_distance, 1.0, area);
+  });
+}
+
+sks_status sks_multi_viewshed(const float* dem, int dimy, int dimx, double cellsize, const int* povs, int npovs,
+                              double h0, int ns, double max_distance, int device, double* pov_area,
+                              double* grid, double* total_area) {
+  return guarded([&] {
+    if (!dem || (npovs > 0 && !povs)) throw std::invalid_argument("null argument");
+    // the reference validates inside the per-observer loop (oracle.cpp:131-141):
+    // the first observer's position, then ns, then the remaining observers
+    for (int t = 0; t < npovs; ++t) {
+      require_inside(dimy, dimx, povs[2 * t], povs[2 * t + 1]);
+      if (t == 0) require_sector_count(ns);
+    }
+    std::vector<double> area(static_cast<size_t>(std::max(npovs, 0)));
+    sweep_areas(default_context(device), dem, dimy, dimx, cellsize, povs, npovs, h0, ns, max_distance, 1.0,
+                area.data());
+    if (grid) std::fill(grid, grid + static_cast<size_t>(dimy) * dimx, 0.0);
+    double total = 0.0;
+    for (int t = 0; t < npovs; ++t) {  // list order (oracle.cpp:137-139)
+      if (grid) grid[static_cast<size_t>(povs[2 * t]) * dimx + povs[2 * t + 1]] += area[t];
+      total += area[t];
+    }
+    if (pov_area) std::copy(area.begin(), area.end(), pov_area);
+    if (total_area) *total_area = total;
+  });
+}
+
+sks_status sks_total_viewshed_reference(const float* dem, int dimy, int dimx, double cellsize,
+                                        const float* nodata, const sks_run_config* cfg, int force,
+                                        double* out) {
+  return guarded([&] {
+    if (!dem || !cfg || !out) throw std::invalid_argument("null argument");
+    // validate(Dem), validate(RunConfig) (oracle.cpp:145-153)
+    std::string err = validate_grid_header(dimy, dimx, cellsize);
+    if (!err.empty()) throw std::invalid_argument(err);
+    const size_t n = static_cast<size_t>(dimy) * dimx;
+    for (size_t c = 0; c < n; ++c) {
+      if (nodata && dem[c] == *nodata) continue;
+      if (!std::isfinite(dem[c])) throw std::invalid_argument(nonfinite_message(static_cast<long long>(c), dimx));
+    }
+    err = validate_config(cfg->ns, cfg->h0, cfg->max_distance);
+    if (!err.empty()) throw std::invalid_argument(err);
+    const long long cells = static_cast<long long>(dimy) * dimx;
+    if (cells > SKS_REFERENCE_CELL_GUARD && !force) {  // oracle.cpp:154-163
+      std::ostringstream os;
+      os << "reference total viewshed on " << dimy << "x" << dimx << " (" << cells
+         << " cells) refused: the sweep costs on the order of ns * N^(3/2) elevation tests and grids above "
+         << SKS_REFERENCE_CELL_GUARD << " cells take a long time; pass force to run anyway";
+      throw std::runtime_error(os.str());
+    }
+    sweep_areas(default_context(cfg->device), dem, dimy, dimx, cellsize, nullptr, cells, cfg->h0, cfg->ns,
+                cfg->max_distance, cfg->units == SKS_UNITS_KM2 ? 1e-6 : 1.0, out);
+  });
+}
+
+sks_status sks_axis_point_set(int dimy, int dimx, int i0, int j0, double azimuth_deg, int* ij, int cap,
+                              int* count) {
+  return guarded([&] {
+    if (!count) throw std::invalid_argument("null argument");
+    require_inside(dimy, dimx, i0, j0);
+    const std::vector<SweepStep> pts = axis_points(dimy, dimx, i0, j0, azimuth_deg);
+    *count = static_cast<int>(pts.size());
+    for (int t = 0; t < std::min(cap, *count) && ij; ++t) {
+      ij[2 * t] = pts[t].di;
+      ij[2 * t + 1] = pts[t].dj;
+    }
+  });
+}
+
+sks_status sks_random_povs(int dimy, int dimx, int count, uint32_t seed, int* ij) {
+  return guarded([&] {
+    if (count > 0 && !ij) throw std::invalid_argument("null argument");
+    random_povs(dimy, dimx, count, seed, ij);
+  });
+}
+
+sks_status sks_write_heatmap(const char* path, const double* values, int rows, int cols, int palette) {
+  return guarded([&] {
+    if (!path || (!values && static_cast<long long>(rows) * cols > 0)) throw std::invalid_argument("null argument");
+    if (palette != SKS_PALETTE_GRAY && palette != SKS_PALETTE_BLUE_RED) throw std::invalid_argument("unknown palette");
+    write_heatmap(path, values, rows, cols, palette);
   });
 }
 

@@ -106,4 +106,15 @@ int launch_dem_check(const float* dem, long long n, unsigned long long* res, voi
 int launch_cv_to_vs(const int* cvf, const int* cvb, double* out,
                     long long n, double correction, void* stream);
 
+// rotational sweep (sweep.cu); same layout as the host SweepStep
+struct SweepStepDev {
+  int di, dj;
+  double dist;
+};
+int launch_sweep(const float* dem, int rows, int cols, const SweepStepDev* tab, const int* len,
+                 int stride, int ndir, const int2* povs, long long pov0, int npov, double h0,
+                 double* buf, void* stream);
+int launch_sweep_sum(const double* buf, int ndir, int npov, double pi_over_ns, double cellsize,
+                     double unit_factor, double* out, long long out_off, void* stream);
+
 }  // namespace sks

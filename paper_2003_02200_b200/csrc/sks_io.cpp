@@ -356,4 +356,75 @@ void write_ascii_grid_vs(const std::string& path, const double* values, int nrow
   if (std::fclose(f) != 0) throw std::runtime_error("failed while writing '" + path + "'");
 }
 
+void write_heatmap(const std::string& path, const double* values, int rows, int cols, int palette) {
+  const size_t n = static_cast<size_t>(std::max(rows, 0)) * static_cast<size_t>(std::max(cols, 0));
+  if (n == 0) throw std::invalid_argument("cannot render an empty grid");
+  // min/max with the non-finite check, split over host threads; lo starts at
+  // the first cell exactly as the reference's (heatmap.cpp:18-27)
+  const unsigned T = std::max(1u, std::min<unsigned>(std::thread::hardware_concurrency(),
+                                                     static_cast<unsigned>((n + 65535) / 65536)));
+  std::vector<double> los(T, values[0]), his(T, values[0]);
+  std::vector<char> bad(T, 0);
+  {
+    std::vector<std::thread> th;
+    for (unsigned t = 0; t < T; ++t) {
+      th.emplace_back([&, t] {
+        const size_t a = n * t / T, z = n * (t + 1) / T;
+        double lo = values[0], hi = values[0];
+        for (size_t c = a; c < z; ++c) {
+          const double x = values[c];
+          if (!std::isfinite(x)) {
+            bad[t] = 1;
+            return;
+          }
+          lo = std::min(lo, x);
+          hi = std::max(hi, x);
+        }
+        los[t] = lo;
+        his[t] = hi;
+      });
+    }
+    for (auto& x : th) x.join();
+  }
+  for (unsigned t = 0; t < T; ++t) {
+    if (bad[t]) throw std::invalid_argument("cannot render a grid with non-finite values");
+  }
+  double lo = values[0], hi = values[0];
+  for (unsigned t = 0; t < T; ++t) {
+    lo = std::min(lo, los[t]);
+    hi = std::max(hi, his[t]);
+  }
+  const double range = hi - lo;
+  const bool gray = palette == 0;
+  std::string bytes = std::string(gray ? "P5\n" : "P6\n") + std::to_string(cols) + " " + std::to_string(rows) +
+                      "\n255\n";
+  const size_t head = bytes.size(), px = gray ? 1 : 3;
+  bytes.resize(head + n * px);
+  {
+    std::vector<std::thread> th;
+    for (unsigned t = 0; t < T; ++t) {
+      th.emplace_back([&, t] {
+        const size_t a = n * t / T, z = n * (t + 1) / T;
+        for (size_t c = a; c < z; ++c) {
+          const double u = range > 0.0 ? (values[c] - lo) / range : 0.0;
+          const auto level = static_cast<unsigned char>(std::lround(u * 255.0));  // heatmap.cpp:35-36
+          char* o = bytes.data() + head + c * px;
+          if (gray) {
+            o[0] = static_cast<char>(level);
+          } else {
+            o[0] = static_cast<char>(level);        // red
+            o[1] = 0;                               // green
+            o[2] = static_cast<char>(255 - level);  // blue
+          }
+        }
+      });
+    }
+    for (auto& x : th) x.join();
+  }
+  FILE* f = std::fopen(path.c_str(), "wb");
+  if (!f) throw std::runtime_error("cannot open '" + path + "' for writing");
+  const bool ok = std::fwrite(bytes.data(), 1, bytes.size(), f) == bytes.size();
+  if (std::fclose(f) != 0 || !ok) throw std::runtime_error("failed while writing '" + path + "'");
+}
+
 }  // namespace sks

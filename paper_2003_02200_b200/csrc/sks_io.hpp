@@ -34,4 +34,8 @@ void write_ascii_grid_dem(const std::string& path, const float* values, int nrow
 void write_ascii_grid_vs(const std::string& path, const double* values, int nrows, int ncols, double factor,
                          double xll, double yll, double cellsize);
 
+// write_heatmap (heatmap.cpp:11-56): min-max normalised 8-bit raster, binary
+// PGM (palette 0, Gray) or PPM (palette 1, BlueRed).
+void write_heatmap(const std::string& path, const double* values, int rows, int cols, int palette);
+
 }  // namespace sks

@@ -1,0 +1,111 @@
+// GPU rotational-sweep viewshed: the reference's independent oracle
+// (oracle.cpp:74-194 — linear_scan, singular_viewshed, multi_viewshed,
+// total_viewshed_reference) re-laid for B200.
+//
+// sweep_dirs_kernel: one thread per (observer, azimuth). The block's 128
+// threads are 128 consecutive observers of the same azimuth, so at every
+// step the warp reads one table entry (a broadcast) and 32 neighbouring
+// cells of one DEM row segment (coalesced). The recurrence is the
+// reference's FP64 one verbatim (oracle.cpp:84-98, the build's --fmad=false
+// keeps dist*dist - open*open unfused like the reference's
+// -ffp-contract=off), so each per-azimuth ring sum is bit-identical.
+// sweep_sum_kernel then adds the ns per-azimuth sums of each observer in the
+// reference's order (forward, backward, k ascending; oracle.cpp:122-126) and
+// applies (pi/ns)*cellsize^2 (oracle.cpp:128).
+//
+// Roofline: FP64-issue bound (one IEEE double divide per ray cell); DEM reads
+// hit L1/L2 (the rays of a warp share rows).
+#include <cuda_runtime.h>
+
+#include <cmath>
+
+#include "sks_device.cuh"
+
+namespace sks {
+
+namespace {
+
+constexpr int kSweepThreads = 128;
+
+__global__ void __launch_bounds__(kSweepThreads)
+sweep_dirs_kernel(const float* __restrict__ dem, int rows, int cols, const SweepStepDev* __restrict__ tab,
+                  const int* __restrict__ len, int stride, int ndir, const int2* __restrict__ povs,
+                  long long pov0, int npov, double h0, double* __restrict__ buf) {
+  const int t = blockIdx.x * kSweepThreads + threadIdx.x;
+  if (t >= npov) return;
+  int i0, j0;
+  if (povs != nullptr) {
+    const int2 p = povs[t];
+    i0 = p.x;
+    j0 = p.y;
+  } else {
+    const long long p = pov0 + t;
+    i0 = static_cast<int>(p / cols);
+    j0 = static_cast<int>(p % cols);
+  }
+  // pov_h = dem(i0, j0) + h0 (oracle.cpp:116)
+  const double h = static_cast<double>(dem[static_cast<long long>(i0) * cols + j0]) + h0;
+  for (int d = blockIdx.y; d < ndir; d += gridDim.y) {
+    const SweepStepDev* s = tab + static_cast<long long>(d) * stride;
+    const int L = len[d];
+    double cv = 0.0, max_theta = -INFINITY, open_d = 0.0, last_d = 0.0;
+    bool visible = false;
+    for (int n = 0; n < L; ++n) {
+      const SweepStepDev st = s[n];
+      const int i = i0 + st.di, j = j0 + st.dj;
+      if (static_cast<unsigned>(i) >= static_cast<unsigned>(rows) ||
+          static_cast<unsigned>(j) >= static_cast<unsigned>(cols)) {
+        break;  // the ray left the grid (oracle.cpp:40,52)
+      }
+      const double theta = (static_cast<double>(__ldg(dem + static_cast<long long>(i) * cols + j)) - h) / st.dist;
+      const bool above = theta > max_theta;
+      if (above && !visible) {
+        open_d = st.dist;
+      } else if (!above && visible) {
+        cv += st.dist * st.dist - open_d * open_d;
+      }
+      visible = above;
+      if (above) max_theta = theta;
+      last_d = st.dist;
+    }
+    if (visible) {  // close at the last cell + 1 (oracle.cpp:101-105)
+      const double close_d = last_d + 1.0;
+      cv += close_d * close_d - open_d * open_d;
+    }
+    buf[static_cast<long long>(d) * npov + t] = cv;
+  }
+}
+
+__global__ void sweep_sum_kernel(const double* __restrict__ buf, int ndir, int npov, double pi_over_ns,
+                                 double cellsize, double unit_factor, double* __restrict__ out,
+                                 long long out_stride_off) {
+  const int t = blockIdx.x * blockDim.x + threadIdx.x;
+  if (t >= npov) return;
+  double cv = 0.0;
+  for (int d = 0; d < ndir; ++d) cv += buf[static_cast<long long>(d) * npov + t];
+  double area = cv * pi_over_ns * cellsize * cellsize;  // oracle.cpp:128
+  if (unit_factor != 1.0) area = area * unit_factor;  // convert_units (dem.cpp:24-34)
+  out[out_stride_off + t] = area;
+}
+
+}  // namespace
+
+int launch_sweep(const float* dem, int rows, int cols, const SweepStepDev* tab, const int* len, int stride,
+                 int ndir, const int2* povs, long long pov0, int npov, double h0, double* buf,
+                 void* stream) {
+  if (npov <= 0) return 0;
+  const dim3 grid((npov + kSweepThreads - 1) / kSweepThreads, ndir < 65535 ? ndir : 65535);
+  sweep_dirs_kernel<<<grid, kSweepThreads, 0, static_cast<cudaStream_t>(stream)>>>(
+      dem, rows, cols, tab, len, stride, ndir, povs, pov0, npov, h0, buf);
+  return static_cast<int>(cudaGetLastError());
+}
+
+int launch_sweep_sum(const double* buf, int ndir, int npov, double pi_over_ns, double cellsize,
+                     double unit_factor, double* out, long long out_off, void* stream) {
+  if (npov <= 0) return 0;
+  sweep_sum_kernel<<<(npov + 255) / 256, 256, 0, static_cast<cudaStream_t>(stream)>>>(
+      buf, ndir, npov, pi_over_ns, cellsize, unit_factor, out, out_off);
+  return static_cast<int>(cudaGetLastError());
+}
+
+}  // namespace sks

@@ -487,3 +487,17 @@ def write_ascii_grid(grid, path, units: Optional["Units"] = None, cellsize: Opti
     check(lib.sks_write_ascii_grid_vs(str(path).encode(), vals.ctypes.data, vals.shape[0], vals.shape[1],
                                       int(grid.units), int(out_units), float(cellsize if cellsize else 1.0),
                                       o.easting, o.northing))
+
+
+class Palette(enum.IntEnum):
+    """heatmap.hpp:9"""
+    Gray = 0
+    BlueRed = 1
+
+
+def write_heatmap(grid: VsGrid, path, palette: Palette = Palette.Gray) -> None:
+    """write_heatmap (heatmap.cpp:11-56): binary PGM (Gray) or PPM (BlueRed)
+    of the min-max normalised map."""
+    vals = np.ascontiguousarray(grid.values if isinstance(grid, VsGrid) else grid, np.float64)
+    rows, cols = (vals.shape + (0, 0))[:2] if vals.ndim == 2 else (0, 0)
+    check(lib.sks_write_heatmap(str(path).encode(), vals.ctypes.data, rows, cols, int(palette)))

@@ -100,6 +100,55 @@ class Ref:
                                         _i32p, C.c_int, C.c_int, C.c_int, C.c_int, C.POINTER(C.c_double),
                                         C.POINTER(C.c_double)]
 
+        lib.ref_singular_viewshed.argtypes = [_f32p, C.c_int, C.c_int, C.c_double, C.c_int, C.c_int, C.c_double,
+                                              C.c_int, C.c_double, C.POINTER(C.c_double)]
+        lib.ref_multi_viewshed.argtypes = [_f32p, C.c_int, C.c_int, C.c_double, C.c_void_p, C.c_int, C.c_double,
+                                           C.c_int, C.c_double, _f64p, C.POINTER(C.c_double)]
+        lib.ref_total_viewshed_reference.argtypes = [_f32p, C.c_int, C.c_int, C.c_double, C.c_void_p, C.c_int,
+                                                     C.c_double, C.c_double, C.c_int, C.c_int, _f64p]
+        lib.ref_axis_point_set.argtypes = [C.c_int, C.c_int, C.c_int, C.c_int, C.c_double, C.c_void_p, C.c_int,
+                                           C.POINTER(C.c_int)]
+        lib.ref_write_heatmap.argtypes = [C.c_char_p, C.c_void_p, C.c_int, C.c_int, C.c_int]
+
+    # ---- rotational sweep (oracle.cpp) / heatmap (heatmap.cpp) ----
+    def singular_viewshed(self, dem, i, j, h0, ns, max_distance=None, cellsize=10.0):
+        out = C.c_double()
+        d = np.ascontiguousarray(dem, np.float32)
+        self._check(self.lib.ref_singular_viewshed(d, d.shape[0], d.shape[1], cellsize, i, j, h0, ns,
+                                                   max_distance or 0.0, C.byref(out)))
+        return out.value
+
+    def multi_viewshed(self, dem, povs, h0, ns, max_distance=None, cellsize=10.0):
+        d = np.ascontiguousarray(dem, np.float32)
+        ij = np.ascontiguousarray(povs, np.int32).reshape(-1, 2)
+        grid = np.empty(d.shape, np.float64)
+        tot = C.c_double()
+        self._check(self.lib.ref_multi_viewshed(d, d.shape[0], d.shape[1], cellsize, ij.ctypes.data, ij.shape[0],
+                                                h0, ns, max_distance or 0.0, grid, C.byref(tot)))
+        return grid, tot.value
+
+    def total_viewshed_reference(self, dem, ns, h0, max_distance=None, units=0, force=True, cellsize=10.0,
+                                 nodata=None):
+        d = np.ascontiguousarray(dem, np.float32)
+        out = np.empty(d.shape, np.float64)
+        nod = C.c_float(nodata) if nodata is not None else None
+        self._check(self.lib.ref_total_viewshed_reference(d, d.shape[0], d.shape[1], cellsize,
+                                                          C.byref(nod) if nod is not None else None, ns, h0,
+                                                          max_distance or 0.0, units, 1 if force else 0, out))
+        return out
+
+    def axis_point_set(self, dimy, dimx, i0, j0, az):
+        cnt = C.c_int()
+        ij = np.empty(2 * (dimy + dimx + 2), np.int32)
+        self._check(self.lib.ref_axis_point_set(dimy, dimx, i0, j0, az, ij.ctypes.data, dimy + dimx + 1,
+                                                C.byref(cnt)))
+        return [(int(ij[2 * t]), int(ij[2 * t + 1])) for t in range(cnt.value)]
+
+    def write_heatmap(self, path, values, palette):
+        v = np.ascontiguousarray(values, np.float64)
+        rows, cols = v.shape if v.ndim == 2 else (0, 0)
+        self._check(self.lib.ref_write_heatmap(str(path).encode(), v.ctypes.data, rows, cols, palette))
+
     def _check(self, rc):
         if rc != 0:
             msg = self.lib.ref_last_error().decode()
@@ -234,6 +283,26 @@ class Orc:
                                            C.c_int, C.c_int, C.c_int, C.c_int, _f64p]
         lib.orc_mt19937_nth.argtypes = [C.c_uint32, C.c_int]
         lib.orc_mt19937_nth.restype = C.c_uint32
+        lib.orc_singular_viewshed.argtypes = [_f32p, C.c_int, C.c_int, C.c_double, C.c_int, C.c_int, C.c_double,
+                                              C.c_int, C.c_double, C.POINTER(C.c_double)]
+        lib.orc_rotational_rows.argtypes = [_f32p, C.c_int, C.c_int, C.c_double, C.c_int, C.c_double, C.c_double,
+                                            C.c_int, C.c_int, C.c_int, _f64p]
+
+    def singular_viewshed(self, dem, i, j, h0, ns, max_distance=None, cellsize=10.0):
+        out = C.c_double()
+        d = np.ascontiguousarray(dem, np.float32)
+        self._check(self.lib.orc_singular_viewshed(d, d.shape[0], d.shape[1], cellsize, i, j, h0, ns,
+                                                   max_distance or 0.0, C.byref(out)))
+        return out.value
+
+    def rotational_rows(self, dem, ns, h0, max_distance=None, units=0, rows=None, cellsize=10.0):
+        """total_viewshed_reference restated, on rows [lo, hi) (NaN elsewhere)."""
+        d = np.ascontiguousarray(dem, np.float32)
+        out = np.full(d.shape, np.nan)
+        lo, hi = rows if rows else (0, d.shape[0])
+        self._check(self.lib.orc_rotational_rows(d, d.shape[0], d.shape[1], cellsize, ns, h0, max_distance or 0.0,
+                                                 units, lo, hi, out))
+        return out
 
     def _check(self, rc):
         if rc == 1:
