@@ -116,6 +116,7 @@ struct Batch {
   std::vector<ScanItem> items;
   long long pool_elems = 0;  // sdem / cv pool elements
   int lmax = 0;
+  bool fused = false;  // relocation fused into scan2's row loader
   unsigned fix_cap = 0;
   std::vector<unsigned> fix_off;  // per item: fixup queue segment offset
   int tiles_x = 0, tiles_total = 0;
@@ -137,6 +138,16 @@ int scan2_slots_for(int lmax) {
     return s != nullptr && std::atoi(s) == 1;
   }();
   return off ? 0 : scan2_slots(lmax);
+}
+
+// Relocation fused into scan2's row loader: opt-in with
+// SKS_FUSED=1, read when a batch is built. Measured on config 2 it removes
+// the 1.1 ms relocation launch but the loader warp's dependent DEM gathers
+// add 1.45 ms to the scan, so the default stays the
+// standalone relocation kernel.
+bool fused_relocation() {
+  const char* s = std::getenv("SKS_FUSED");
+  return s != nullptr && std::atoi(s) != 0;
 }
 
 long long batch_budget_bytes() {
@@ -173,6 +184,7 @@ std::unique_ptr<Batch> make_batch(const std::vector<SectorPlanH>& plans,
     std::copy(p.map, p.map + 6, d.map);
     std::copy(p.inv, p.inv + 6, d.inv);
     d.correction = p.correction;
+    d.shear_tan = p.shear_tan;
     d.sdem_off = off;
     off += static_cast<long long>(p.skw_rows) * d.pitch;
     col_off += p.cols;
@@ -184,10 +196,14 @@ std::unique_ptr<Batch> make_batch(const std::vector<SectorPlanH>& plans,
       const RowRange& r = p.ranges[q];
       b->ranges.push_back(make_int2(r.first, r.last));
       const int L = r.last - r.first;
-      if (L >= 2 && p.max_dd > 0 && q >= d.q_lo && q < d.q_hi) {
+      if (L >= 1 && q >= d.q_lo && q < d.q_hi) {
+        // rows with no target (L = 1 or a zero cap) only matter to the fused
+        // loader, which zeroes their cv range; dropped below otherwise
         b->items.push_back(ScanItem{static_cast<int>(s), q});
-        b->lmax = std::max(b->lmax, L);
-        b->target_evals += row_target_evals(L, p.max_dd);
+        if (L >= 2 && p.max_dd > 0) {
+          b->lmax = std::max(b->lmax, L);
+          b->target_evals += row_target_evals(L, p.max_dd);
+        }
       }
     }
     max_cols = std::max(max_cols, p.cols);
@@ -195,6 +211,13 @@ std::unique_ptr<Batch> make_batch(const std::vector<SectorPlanH>& plans,
     b->sdev.push_back(d);
   }
   b->pool_elems = off;
+  b->fused = fused_relocation() && scan2_slots_for(b->lmax) > 0;
+  if (!b->fused) {
+    std::erase_if(b->items, [&](const ScanItem& it) {
+      const int2 r = b->ranges[b->sdev[it.s].row_off + it.q];
+      return r.y - r.x < 2 || b->sdev[it.s].max_dd <= 0;
+    });
+  }
   // longest rows first (load balance of the persistent scan)
   std::stable_sort(b->items.begin(), b->items.end(), [&](const ScanItem& x, const ScanItem& y) {
     const int2 rx = b->ranges[b->sdev[x.s].row_off + x.q];
@@ -455,11 +478,15 @@ void run_sectors(sks_context* ctx, const float* d_dem, int dimy, int dimx, doubl
     Batch& b = *bp;
     ctx->ensure_pools(b, false);
     BatchDev bd = ctx->batch_dev(b, false);
+    const bool fused = b.fused;  // relocation inside scan2's row loader
+    if (fused) bd.dem = d_dem;
     ScanArgs a = ctx->scan_args(b, bd, cfg->h0);
     a.force_exact = force_exact ? 1 : 0;
     if (stats) cuda_check(cudaEventRecord(ctx->ev[0], st), "event");
-    cuda_check(launch_relocate_grid(d_dem, bd, b.tiles_x, b.tiles_total, st), "launch relocate");
-    ++ctx->launches;
+    if (!fused) {
+      cuda_check(launch_relocate_grid(d_dem, bd, b.tiles_x, b.tiles_total, st), "launch relocate");
+      ++ctx->launches;
+    }
     if (stats) cuda_check(cudaEventRecord(ctx->ev[1], st), "event");
     ctx->scan_batch(b, a, st, false, false);
     if (stats) cuda_check(cudaEventRecord(ctx->ev[2], st), "event");

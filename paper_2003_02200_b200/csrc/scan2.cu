@@ -129,7 +129,17 @@ __device__ __forceinline__ Slot slot_ptrs(float* base, const Layout2& lay) {
 
 // Loads the next row (longest first) into slot `sl`; one warp. Returns false
 // and marks the slot dead when the work list is exhausted.
+#ifdef SKS_EXP_LOADCLK
+__device__ void load_slot_(const ScanArgs& a, int* ctl, float* base, const Layout2& lay, int lane);
 __device__ void load_slot(const ScanArgs& a, int* ctl, float* base, const Layout2& lay, int lane) {
+  const long long t0 = clock64();
+  load_slot_(a, ctl, base, lay, lane);
+  if (lane == 0 && a.skipped) atomicAdd(a.skipped, static_cast<unsigned long long>(clock64() - t0) << 20);
+}
+__device__ void load_slot_(const ScanArgs& a, int* ctl, float* base, const Layout2& lay, int lane) {
+#else
+__device__ void load_slot(const ScanArgs& a, int* ctl, float* base, const Layout2& lay, int lane) {
+#endif
   int it = 0;
   if (lane == 0) it = static_cast<int>(atomicAdd(a.item_counter, 1u));
   it = __shfl_sync(0xffffffffu, it, 0);
@@ -141,12 +151,74 @@ __device__ void load_slot(const ScanArgs& a, int* ctl, float* base, const Layout
   const SectorDev& sd = a.b.sectors[item.s];
   const int2 rg = a.b.ranges[sd.row_off + item.q];
   const int L = rg.y - rg.x;
-  const float* src = a.b.sdem + sd.sdem_off + static_cast<long long>(item.q) * sd.pitch + rg.x;
+  const long long row0 = sd.sdem_off + static_cast<long long>(item.q) * sd.pitch + rg.x;
   float* S = base;
   float* R = base + lay.lb;
   const float ninf = -INFINITY;
+  if (a.b.dem != nullptr) {
+    // Fused relocation: gather v(q, j) = (+0 + (1-f)*pre(i, j)) + f*pre(i+1, j),
+    // i = q - base + dest[j], exactly as relocate_kernel (skew.cpp:163-183),
+    // with pre(i, j) = dem(to_source(i, j)) (apply_pre_ops, skew.cpp:103-142).
+    // The row also goes to sdem (the fixup reads it) and its cv range is zeroed.
+    const int* m = sd.map;
+    float* gdst = a.b.sdem + row0;
+    int* cz = a.b.cv + row0;
+    int* czb = a.b.cv_bwd ? a.b.cv_bwd + row0 : nullptr;
+    const int qb = item.q - sd.base;
+    const int nsr = sd.rows;
+    // kU cells per lane in flight: the dest/frac loads, then the dependent
+    // DEM gathers (L2 hits; strided for transposed sectors), then the stores
+    constexpr int kU = 4;
+    for (int xb = 0; xb < lay.lb; xb += 32 * kU) {
+      int im[kU];
+      float f[kU], v1[kU], v2[kU];
+#pragma unroll
+      for (int u = 0; u < kU; ++u) {
+        // shear_params (skew.cpp:97-101) in the same IEEE double ops: no
+        // dependent load before the gathers
+        const int x = xb + 32 * u + lane;
+        const double y = __dmul_rn(sd.shear_tan, static_cast<double>(rg.x + x));
+        const int dj = __double2int_rz(y);
+        f[u] = __double2float_rn(__dsub_rn(y, static_cast<double>(dj)));
+        im[u] = x < L ? qb + dj : -2;
+      }
+#pragma unroll
+      for (int u = 0; u < kU; ++u) {
+        const int j = rg.x + xb + 32 * u + lane;
+        const int i1 = im[u], i2 = im[u] + 1;
+        v1[u] = (i1 >= 0 && i1 < nsr)
+                    ? __ldg(a.b.dem + static_cast<long long>(m[0] * i1 + m[1] * j + m[2]) * sd.src_cols +
+                            (m[3] * i1 + m[4] * j + m[5]))
+                    : 0.0f;
+        v2[u] = (i2 >= 0 && i2 < nsr)
+                    ? __ldg(a.b.dem + static_cast<long long>(m[0] * i2 + m[1] * j + m[2]) * sd.src_cols +
+                            (m[3] * i2 + m[4] * j + m[5]))
+                    : 0.0f;
+      }
+#pragma unroll
+      for (int u = 0; u < kU; ++u) {
+        const int x = xb + 32 * u + lane;
+        if (x >= lay.lb) break;
+        float v = ninf;
+        if (x < L) {
+          float acc = 0.0f;
+          if (im[u] >= 0 && im[u] < nsr) acc = __fadd_rn(acc, __fmul_rn(__fsub_rn(1.0f, f[u]), v1[u]));
+          if (im[u] + 1 >= 0 && im[u] + 1 < nsr) acc = __fadd_rn(acc, __fmul_rn(f[u], v2[u]));
+#ifndef SKS_EXP_NOSTORE
+          gdst[x] = acc;
+          cz[x] = 0;
+          if (czb) czb[x] = 0;
+#endif
+          v = acc;
+        }
+        S[x] = v;
+      }
+    }
+  } else {
+    const float* src = a.b.sdem + row0;
 #pragma unroll 4
-  for (int x = lane; x < lay.lb; x += 32) S[x] = x < L ? __ldg(src + x) : ninf;
+    for (int x = lane; x < lay.lb; x += 32) S[x] = x < L ? __ldg(src + x) : ninf;
+  }
   __syncwarp();
   for (int x = lane; x < lay.lb; x += 32) R[x] = x < L ? S[L - 1 - x] : ninf;
   __syncwarp();
@@ -427,7 +499,7 @@ __device__ void run_task(const ScanArgs& a, const Layout2& lay, const Slot& sl, 
 }
 
 template <int kThr, int kNC>
-__global__ void __launch_bounds__(kThr, 1) scan2_kernel(ScanArgs a, int nslots, int lmax) {
+__global__ void __launch_bounds__(kThr, 1) scan2_kernel(const __grid_constant__ ScanArgs a, int nslots, int lmax) {
   extern __shared__ __align__(16) float smem[];
   const Layout2 lay(lmax, kNC);
   int* ctl_all = reinterpret_cast<int*>(smem);

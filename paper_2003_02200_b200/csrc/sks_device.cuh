@@ -29,6 +29,7 @@ struct SectorDev {
   int map[6];    // pre (i, j) -> DEM (si, sj)
   int inv[6];    // DEM (si, sj) -> pre (i, j)
   double correction;  // 1 + tan^2
+  double shear_tan;   // shear_params (skew.cpp:97-101) on device: the fused loader
   long long sdem_off;  // element offset of this sector in the sdem / cv pools
 };
 
@@ -48,6 +49,11 @@ struct BatchDev {
   float* sdem;
   int* cv;
   int* cv_bwd;  // debug: backward scan results kept apart (nullptr = cv)
+  // Fused relocation (scan2 only): the row loader builds each sDEM row from
+  // this DEM (writing it to sdem for the fixup and zeroing the row's cv
+  // range), and the unskew treats cv outside the row ranges as 0. nullptr:
+  // rows come from sdem written by relocate_kernel, which zeroes cv.
+  const float* dem;
 };
 
 struct ScanArgs {

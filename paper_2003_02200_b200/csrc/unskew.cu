@@ -149,6 +149,12 @@ __global__ void __launch_bounds__(256) unskew_tiled_kernel(BatchDev b, double* _
       double va = 0.0, vb = 0.0;
       if (a) va = __dmul_rn(static_cast<double>(scv[p - p_lo][jl]), sd.correction);
       if (!a || c) vb = __dmul_rn(static_cast<double>(scv[p - 1 - p_lo][jl]), sd.correction);
+      if (!a && !c && b.dem != nullptr) {
+        // the only read that may fall outside the row ranges (skwVS is 0
+        // there, scan.cpp:66); with fused relocation nothing zeroed it
+        const int2 rg = (p >= 1 && p - 1 < sd.skw_rows) ? __ldg(b.ranges + sd.row_off + p - 1) : make_int2(0, 0);
+        if (j < rg.x || j >= rg.y) vb = 0.0;
+      }
       double v;
       if (a && c) {
         v = __dadd_rn(__dmul_rn(omr, va), __dmul_rn(r, vb));

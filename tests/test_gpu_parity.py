@@ -381,6 +381,40 @@ def test_row_block_parts_sum_to_total(ora, nparts):
         np.testing.assert_allclose(total, ref, rtol=1e-12, atol=0)
 
 
+@pytest.mark.parametrize("shape,kind,ns,maxd", [
+    ((48, 40), sk.SyntheticKind.SmoothedNoise, 36, None),
+    ((40, 48), sk.SyntheticKind.Fractal, 36, None),
+    ((64, 64), sk.SyntheticKind.Fractal, 180, 150.0),
+    ((24, 40), sk.SyntheticKind.Ramp, 2, None),
+    ((2, 2), sk.SyntheticKind.SmoothedNoise, 8, None),
+    ((33, 35), sk.SyntheticKind.Cone, 90, 10.0),  # a distance cap of 1 cell at most
+])
+def test_fused_relocation_bitexact(ora, shape, kind, ns, maxd, monkeypatch):
+    """Relocation fused into scan2's row loader (SKS_FUSED=1, read when a
+    context builds its batches): rows gathered from the DEM in the loader,
+    the unskew reading only the ranges it wrote. Bit-exact like the default
+    path, on one part and (to 1e-12) on row-block parts."""
+    import torch
+
+    monkeypatch.setenv("SKS_FUSED", "1")
+    dem = sk.make_synthetic(kind, *shape, 10.0, 13)
+    cfg = sk.RunConfig(ns=ns, h0=1.5, max_distance=maxd, units=sk.Units.SquareMeters)
+    ref = ora.total_viewshed(dem.values, 10.0, ns, 1.5, max_distance=maxd or 0.0, raw=True)
+    ctx = sk.Context(0)
+    ours = ctx.total_viewshed(dem.values, 10.0, cfg, raw=True)
+    assert np.array_equal(b64(ours), b64(ref))
+    d_dem = torch.from_numpy(dem.values).cuda()
+    total = np.zeros(shape, np.float64)
+    for part in range(3):
+        d_map = torch.zeros(shape, dtype=torch.float64, device="cuda")
+        ctx.run_rows(d_dem.data_ptr(), *shape, 10.0, cfg, part, 3, d_map.data_ptr(),
+                     stream=torch.cuda.current_stream().cuda_stream)
+        torch.cuda.synchronize()
+        total += d_map.cpu().numpy()
+    np.testing.assert_allclose(total, ref, rtol=1e-12, atol=0)
+    ctx.close()
+
+
 def test_row_blocks_balance_exact_work():
     """Every target of every sector is owned by exactly one part."""
     import torch
