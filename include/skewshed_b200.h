@@ -237,6 +237,13 @@ sks_status sks_ascii_grid_header(const sks_ascii_grid* grid, sks_grid_header* ou
 sks_status sks_ascii_grid_values(const sks_ascii_grid* grid, float* out);
 void sks_ascii_grid_free(sks_ascii_grid* grid);
 
+/* Binary side format for large DEMs (no reference counterpart; SURVEY §8f
+   rank 3): ESRI float grid, `.hdr` text header + `.flt` float32 cells, north
+   row first, LSBFIRST or MSBFIRST. path names either file. Same handle as
+   the ASCII reader; SKS_FORMAT_ERROR on a bad header or a short/long file. */
+sks_status sks_float_grid_read(const char* path, sks_ascii_grid** out);
+sks_status sks_write_float_grid(const char* path, const float* values, const sks_grid_header* hdr);
+
 /* write_ascii_grid(Dem, path) (ascii_grid.cpp:225-245); header fields from
    hdr (nodata written when has_nodata). */
 sks_status sks_write_ascii_grid_dem(const char* path, const float* values,

@@ -324,6 +324,19 @@ inline Dem read_ascii_grid(std::istream& in, std::string_view source_name) {
   return detail::take_ascii_grid(g);
 }
 
+// Binary side format (ESRI .hdr + .flt float32), the fast load of large DEMs.
+inline Dem read_float_grid(const std::filesystem::path& path) {
+  sks_ascii_grid* g = nullptr;
+  check(sks_float_grid_read(path.string().c_str(), &g));
+  return detail::take_ascii_grid(g);
+}
+
+inline void write_float_grid(const Dem& dem, const std::filesystem::path& path) {
+  const sks_grid_header h{dem.dimy(), dem.dimx(), dem.origin.easting, dem.origin.northing,
+                          dem.cellsize, dem.nodata ? 1 : 0, dem.nodata.value_or(0.0f)};
+  check(sks_write_float_grid(path.string().c_str(), dem.values.data().data(), &h));
+}
+
 inline void write_ascii_grid(const Dem& dem, const std::filesystem::path& path) {
   const sks_grid_header h{dem.dimy(), dem.dimx(), dem.origin.easting, dem.origin.northing,
                           dem.cellsize, dem.nodata ? 1 : 0, dem.nodata.value_or(0.0f)};

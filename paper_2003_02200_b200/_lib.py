@@ -109,6 +109,8 @@ SIGNATURES = {
     "sks_ascii_grid_header": (C.c_int, [_vp, C.POINTER(GridHeaderC)]),
     "sks_ascii_grid_values": (C.c_int, [_vp, _vp]),
     "sks_ascii_grid_free": (None, [_vp]),
+    "sks_float_grid_read": (C.c_int, [C.c_char_p, C.POINTER(_vp)]),
+    "sks_write_float_grid": (C.c_int, [C.c_char_p, _vp, C.POINTER(GridHeaderC)]),
     "sks_write_ascii_grid_dem": (C.c_int, [C.c_char_p, _vp, C.POINTER(GridHeaderC)]),
     "sks_write_ascii_grid_vs": (C.c_int, [C.c_char_p, _vp, C.c_int, C.c_int, C.c_int, C.c_int, C.c_double,
                                           C.c_double, C.c_double]),

@@ -1123,6 +1123,24 @@ sks_status sks_ascii_grid_values(const sks_ascii_grid* grid, float* out) {
 
 void sks_ascii_grid_free(sks_ascii_grid* grid) { delete grid; }
 
+sks_status sks_float_grid_read(const char* path, sks_ascii_grid** out) {
+  return guarded([&] {
+    if (!path || !out) throw std::invalid_argument("null argument");
+    *out = nullptr;
+    auto h = std::make_unique<sks_ascii_grid>();
+    h->g = read_float_grid(path);
+    *out = h.release();
+  });
+}
+
+sks_status sks_write_float_grid(const char* path, const float* values, const sks_grid_header* hdr) {
+  return guarded([&] {
+    if (!path || !values || !hdr) throw std::invalid_argument("null argument");
+    write_float_grid(path, values, hdr->nrows, hdr->ncols, hdr->xllcorner, hdr->yllcorner, hdr->cellsize,
+                     hdr->has_nodata ? &hdr->nodata : nullptr);
+  });
+}
+
 sks_status sks_write_ascii_grid_dem(const char* path, const float* values, const sks_grid_header* hdr) {
   return guarded([&] {
     if (!path || !values || !hdr) throw std::invalid_argument("null argument");

@@ -20,6 +20,7 @@
 #include <cctype>
 #include <charconv>
 #include <cmath>
+#include <cstdint>
 #include <cstdio>
 #include <cstring>
 #include <stdexcept>
@@ -329,7 +330,9 @@ void write_ascii_grid_dem(const std::string& path, const float* values, int nrow
   try {
     if (std::fwrite(h.data(), 1, h.size(), f) != h.size()) throw std::runtime_error("failed while writing '" + path + "'");
     write_rows(f, nrows, ncols, [&](char* b, size_t n, int i, int j) {
-      return std::snprintf(b, n, "%.9g", static_cast<double>(values[static_cast<size_t>(i) * ncols + j]));
+      // to_chars(general, p) is specified as printf("%.pg") in the C locale
+      return static_cast<int>(std::to_chars(b, b + n, static_cast<double>(values[static_cast<size_t>(i) * ncols + j]),
+                                            std::chars_format::general, 9).ptr - b);
     }, path);
   } catch (...) {
     std::fclose(f);
@@ -347,13 +350,149 @@ void write_ascii_grid_vs(const std::string& path, const double* values, int nrow
     if (std::fwrite(h.data(), 1, h.size(), f) != h.size()) throw std::runtime_error("failed while writing '" + path + "'");
     write_rows(f, nrows, ncols, [&](char* b, size_t n, int i, int j) {
       const double v = values[static_cast<size_t>(i) * ncols + j];
-      return std::snprintf(b, n, "%.10g", factor == 1.0 ? v : v * factor);
+      return static_cast<int>(
+          std::to_chars(b, b + n, factor == 1.0 ? v : v * factor, std::chars_format::general, 10).ptr - b);
     }, path);
   } catch (...) {
     std::fclose(f);
     throw;
   }
   if (std::fclose(f) != 0) throw std::runtime_error("failed while writing '" + path + "'");
+}
+
+namespace {
+
+// "dem.flt" / "dem.hdr" / "dem" -> ("dem.hdr", "dem.flt")
+void float_grid_paths(const std::string& path, std::string* hdr, std::string* flt) {
+  std::string base = path;
+  const size_t dot = path.find_last_of('.');
+  const size_t slash = path.find_last_of('/');
+  if (dot != std::string::npos && (slash == std::string::npos || dot > slash)) {
+    const std::string ext = lower(path.data() + dot, path.data() + path.size());
+    if (ext == ".flt" || ext == ".hdr") base = path.substr(0, dot);
+  }
+  *hdr = base + ".hdr";
+  *flt = base + ".flt";
+}
+
+std::string slurp(const std::string& path) {
+  FILE* f = std::fopen(path.c_str(), "rb");
+  if (!f) throw GridFormatError("cannot open '" + path + "' for reading");
+  std::string s;
+  char b[1 << 16];
+  size_t k;
+  while ((k = std::fread(b, 1, sizeof(b), f)) > 0) s.append(b, k);
+  std::fclose(f);
+  return s;
+}
+
+}  // namespace
+
+AsciiGrid read_float_grid(const std::string& path) {
+  std::string hp, fp;
+  float_grid_paths(path, &hp, &fp);
+  const std::string h = slurp(hp);
+  AsciiGrid g;
+  bool have[5] = {false, false, false, false, false};
+  bool center[2] = {false, false};
+  bool msb = false;
+  Cursor cur{h.data(), h.size()};
+  size_t b = 0, e = 0;
+  while (cur.next(&b, &e)) {
+    const std::string key = lower(h.data() + b, h.data() + e);
+    const size_t kb = b, ke = e;
+    if (!cur.next(&b, &e)) fail_eof(hp, h.data(), h.size(), "missing value for header key '" + key + "'");
+    const char* vb = h.data() + b;
+    const char* ve = h.data() + e;
+    double d = 0.0;
+    long l = 0;
+    if (key == "ncols" || key == "nrows") {
+      if (!to_long(vb, ve, &l) || l < 1 || l > INT32_MAX) {
+        fail_at(hp, h.data(), b, "expected a positive integer for '" + key + "', got '" + std::string(vb, ve) + "'");
+      }
+      (key == "ncols" ? g.ncols : g.nrows) = static_cast<int>(l);
+      have[key == "ncols" ? 0 : 1] = true;
+    } else if (key == "byteorder") {
+      const std::string v = lower(vb, ve);
+      if (v == "msbfirst" || v == "m") {
+        msb = true;
+      } else if (v == "lsbfirst" || v == "i") {
+        msb = false;
+      } else {
+        fail_at(hp, h.data(), b, "byteorder must be LSBFIRST or MSBFIRST, got '" + std::string(vb, ve) + "'");
+      }
+    } else if (key == "xllcorner" || key == "xllcenter" || key == "yllcorner" || key == "yllcenter" ||
+               key == "cellsize" || key == "nodata_value") {
+      if (!to_double(vb, ve, &d)) {
+        fail_at(hp, h.data(), b, "expected a number for '" + key + "', got '" + std::string(vb, ve) + "'");
+      }
+      if (key[0] == 'x') {
+        g.xllcorner = d, have[2] = true, center[0] = key == "xllcenter";
+      } else if (key[0] == 'y') {
+        g.yllcorner = d, have[3] = true, center[1] = key == "yllcenter";
+      } else if (key == "cellsize") {
+        g.cellsize = d, have[4] = true;
+      } else {
+        g.has_nodata = true;
+        g.nodata = static_cast<float>(d);
+      }
+    } else {
+      fail_at(hp, h.data(), kb, "unknown header key '" + std::string(h.data() + kb, h.data() + ke) + "'");
+    }
+  }
+  static const char* names[5] = {"ncols", "nrows", "xllcorner", "yllcorner", "cellsize"};
+  for (int k = 0; k < 5; ++k) {
+    if (!have[k]) throw GridFormatError(hp + ": missing header key '" + names[k] + "'");
+  }
+  if (!(g.cellsize > 0.0) || !std::isfinite(g.cellsize)) {
+    throw GridFormatError(hp + ": cellsize must be a positive finite number, got " + fmt_g(g.cellsize));
+  }
+  // cell-centre origins move to the corner (half a cell)
+  if (center[0]) g.xllcorner -= 0.5 * g.cellsize;
+  if (center[1]) g.yllcorner -= 0.5 * g.cellsize;
+  const long long cells = static_cast<long long>(g.nrows) * g.ncols;
+  if (cells > kMaxCells) throw GridFormatError(hp + ": grid of " + std::to_string(cells) + " cells is too large");
+  FILE* f = std::fopen(fp.c_str(), "rb");
+  if (!f) throw GridFormatError("cannot open '" + fp + "' for reading");
+  g.values.resize(static_cast<size_t>(cells));
+  const size_t got = std::fread(g.values.data(), sizeof(float), g.values.size(), f);
+  const bool extra = std::fgetc(f) != EOF;
+  std::fclose(f);
+  if (got != g.values.size() || extra) {
+    throw GridFormatError(fp + ": expected " + std::to_string(cells * 4) + " bytes of float32 cells for " +
+                          std::to_string(g.nrows) + "x" + std::to_string(g.ncols) + (extra ? ", got more" : ", got fewer"));
+  }
+  if (msb) {
+    for (float& v : g.values) {
+      uint32_t u;
+      std::memcpy(&u, &v, 4);
+      u = __builtin_bswap32(u);
+      std::memcpy(&v, &u, 4);
+    }
+  }
+  return g;
+}
+
+void write_float_grid(const std::string& path, const float* values, int nrows, int ncols, double xll, double yll,
+                      double cellsize, const float* nodata) {
+  std::string hp, fp;
+  float_grid_paths(path, &hp, &fp);
+  std::string h = header_text(ncols, nrows, xll, yll, cellsize);
+  if (nodata) {
+    char b[64];
+    std::snprintf(b, sizeof(b), "%.9g", static_cast<double>(*nodata));
+    h += std::string("NODATA_value ") + b + "\n";
+  }
+  h += "byteorder LSBFIRST\n";
+  FILE* f = std::fopen(hp.c_str(), "wb");
+  if (!f) throw std::runtime_error("cannot open '" + hp + "' for writing");
+  const bool okh = std::fwrite(h.data(), 1, h.size(), f) == h.size();
+  if (std::fclose(f) != 0 || !okh) throw std::runtime_error("failed while writing '" + hp + "'");
+  f = std::fopen(fp.c_str(), "wb");
+  if (!f) throw std::runtime_error("cannot open '" + fp + "' for writing");
+  const size_t n = static_cast<size_t>(nrows) * static_cast<size_t>(ncols);
+  const bool ok = std::fwrite(values, sizeof(float), n, f) == n;
+  if (std::fclose(f) != 0 || !ok) throw std::runtime_error("failed while writing '" + fp + "'");
 }
 
 void write_heatmap(const std::string& path, const double* values, int rows, int cols, int palette) {

@@ -34,6 +34,15 @@ void write_ascii_grid_dem(const std::string& path, const float* values, int nrow
 void write_ascii_grid_vs(const std::string& path, const double* values, int nrows, int ncols, double factor,
                          double xll, double yll, double cellsize);
 
+// Binary side format for large DEMs: the ESRI float grid,
+// a `.hdr` text header (ncols, nrows, xllcorner|xllcenter,
+// yllcorner|yllcenter, cellsize, optional NODATA_value, byteorder
+// LSBFIRST|MSBFIRST) next to a `.flt` file of nrows*ncols IEEE float32, north
+// row first. `path` may name either file (or neither extension).
+AsciiGrid read_float_grid(const std::string& path);
+void write_float_grid(const std::string& path, const float* values, int nrows, int ncols, double xll,
+                      double yll, double cellsize, const float* nodata);
+
 // write_heatmap (heatmap.cpp:11-56): min-max normalised 8-bit raster, binary
 // PGM (palette 0, Gray) or PPM (palette 1, BlueRed).
 void write_heatmap(const std::string& path, const double* values, int rows, int cols, int palette);

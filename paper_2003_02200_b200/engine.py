@@ -471,6 +471,21 @@ def parse_ascii_grid(text, source_name: str = "<input>") -> Dem:
     return _grid_from_handle(h)
 
 
+def read_float_grid(path) -> Dem:
+    """Binary side format (ESRI .hdr + .flt float32): the fast DEM load for
+    large grids. GridFormatError on a bad header or file size."""
+    h = C.c_void_p()
+    check(lib.sks_float_grid_read(str(path).encode(), C.byref(h)))
+    return _grid_from_handle(h)
+
+
+def write_float_grid(dem: Dem, path) -> None:
+    """Writes dem as <base>.hdr + <base>.flt (LSBFIRST)."""
+    hdr = _lib.GridHeaderC(dem.dimy(), dem.dimx(), dem.origin.easting, dem.origin.northing, dem.cellsize,
+                           1 if dem.nodata is not None else 0, float(dem.nodata) if dem.nodata is not None else 0.0)
+    check(lib.sks_write_float_grid(str(path).encode(), dem.values.ctypes.data, C.byref(hdr)))
+
+
 def write_ascii_grid(grid, path, units: Optional["Units"] = None, cellsize: Optional[float] = None,
                      origin: Optional[GridOrigin] = None) -> None:
     """write_ascii_grid for a Dem (ascii_grid.cpp:225-245) or a VsGrid in

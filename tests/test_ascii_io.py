@@ -161,3 +161,65 @@ def test_file_entry_points_and_writers_match_reference_bytes(tmp_path):
         assert o2.read_bytes() == r2.read_bytes(), (uin, uout)
     with pytest.raises(sk.GridFormatError, match="cannot open"):
         sk.read_ascii_grid(tmp_path / "missing.asc")
+
+
+def test_writers_special_values_match_reference_bytes(tmp_path):
+    """to_chars(general) must print exactly like the reference's %.9g / %.10g:
+    signed zeros, subnormals, huge values, inf and nan."""
+    lib = _ref()
+    v = np.array([[0.0, -0.0, 1e-45, -3.4e38], [np.inf, -np.inf, np.nan, 123456789.0],
+                  [1.0 / 3.0, 2.5e-7, 1e15, -7.0]], np.float32)
+    ours, ref = tmp_path / "o.asc", tmp_path / "r.asc"
+    sk.write_ascii_grid(sk.Dem(v, 1.0), ours)
+    assert lib.ref_write_ascii_grid_dem(str(ref).encode(), v.ctypes.data, 3, 4, 0.0, 0.0, 1.0, 0, 0.0) == 0
+    assert ours.read_bytes() == ref.read_bytes()
+    d = np.array([[0.0, -0.0, 5e-324, 1.7976931348623157e308], [np.inf, -np.nan, 0.1, 1e21]], np.float64)
+    sk.write_ascii_grid(sk.VsGrid(d, sk.Units.SquareMeters), ours, cellsize=1.0)
+    assert lib.ref_write_ascii_grid_vs(str(ref).encode(), d.ctypes.data, 2, 4, 0, 0, 1.0, 0.0, 0.0) == 0
+    assert ours.read_bytes() == ref.read_bytes()
+
+
+# ---- binary side format (ESRI .hdr + .flt float32) -------------------------
+
+def test_float_grid_round_trip_and_equals_ascii(tmp_path):
+    dem = sk.make_synthetic(sk.SyntheticKind.Fractal, 41, 29, 10.0, 5)
+    v = dem.values.copy()
+    v[0, 0], v[1, 1], v[2, 2] = -0.0, np.float32(1e-45), -9999.0
+    dem = sk.Dem(v, 12.5, -9999.0, sk.GridOrigin(482500.25, 5634200.125))
+    sk.write_float_grid(dem, tmp_path / "d.flt")
+    assert (tmp_path / "d.hdr").exists()
+    for name in ("d.flt", "d.hdr", "d"):
+        back = sk.read_float_grid(tmp_path / name)
+        assert np.array_equal(back.values.view(np.uint32), v.view(np.uint32))
+        assert back.cellsize == 12.5 and back.nodata == -9999.0 and back.origin == dem.origin
+    sk.write_ascii_grid(dem, tmp_path / "d.asc")
+    asc = sk.read_ascii_grid(tmp_path / "d.asc")
+    assert np.array_equal(asc.values.view(np.uint32), sk.read_float_grid(tmp_path / "d").values.view(np.uint32))
+
+
+def test_float_grid_big_endian_and_cell_centres(tmp_path):
+    v = np.arange(12, dtype=np.float32).reshape(3, 4) * np.float32(1.5) - 4
+    (tmp_path / "b.hdr").write_text("NCOLS 4\nNROWS 3\nXLLCENTER 5\nYLLCENTER 7\nCELLSIZE 2\nBYTEORDER MSBFIRST\n")
+    (tmp_path / "b.flt").write_bytes(v.astype(">f4").tobytes())
+    g = sk.read_float_grid(tmp_path / "b.flt")
+    assert np.array_equal(g.values, v) and g.nodata is None
+    assert g.origin == sk.GridOrigin(4.0, 6.0)  # half a cell to the corner
+
+
+@pytest.mark.parametrize("hdr,flt_bytes,msg", [
+    ("ncols 4\nnrows 3\nxllcorner 0\nyllcorner 0\ncellsize 2\n", 40, "expected 48 bytes of float32 cells for 3x4, got fewer"),
+    ("ncols 4\nnrows 3\nxllcorner 0\nyllcorner 0\ncellsize 2\n", 52, "got more"),
+    ("ncols 4\nnrows 3\nxllcorner 0\nyllcorner 0\n", 48, "missing header key 'cellsize'"),
+    ("ncols 4\nnrows x\nxllcorner 0\nyllcorner 0\ncellsize 2\n", 48, "b.hdr:2:7: expected a positive integer for 'nrows'"),
+    ("ncols 4\nnrows 3\nxllcorner 0\nyllcorner 0\ncellsize 0\n", 48, "cellsize must be a positive finite number"),
+    ("ncols 4\nnrows 3\nxllcorner 0\nyllcorner 0\ncellsize 2\nbyteorder VAX\n", 48, "byteorder must be"),
+    ("ncols 4\nnrows 3\nxllcorner 0\nyllcorner 0\ncellsize 2\nlayout bil\n", 48, "b.hdr:6:1: unknown header key 'layout'"),
+    ("ncols 4\nnrows 3\nxllcorner 0\nyllcorner 0\ncellsize\n", 48, "missing value for header key 'cellsize'"),
+])
+def test_float_grid_errors(tmp_path, hdr, flt_bytes, msg):
+    (tmp_path / "b.hdr").write_text(hdr)
+    (tmp_path / "b.flt").write_bytes(b"\0" * flt_bytes)
+    with pytest.raises(sk.GridFormatError, match=msg):
+        sk.read_float_grid(tmp_path / "b")
+    with pytest.raises(sk.GridFormatError, match="cannot open"):
+        sk.read_float_grid(tmp_path / "nope.flt")
