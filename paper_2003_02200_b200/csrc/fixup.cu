@@ -92,8 +92,10 @@ __device__ __forceinline__ void eval_block(ExactState& S, const float* row, cons
     if (dd + 3 > db) {
       // remainder (< 4 targets): one by one
 #pragma unroll
+      // (elevations re-read through L1: ev stays in registers, statically indexed)
+#pragma unroll 1
       for (int i = 0; i < 4; ++i) {
-        if (dd + i <= db) exact_step(S, row, x, sg, dd + i, ev[4 * g + i], ivt[dd + i]);
+        if (dd + i <= db) exact_step(S, row, x, sg, dd + i, __ldg(row + x + sg * (dd + i)), ivt[dd + i]);
       }
       break;
     }
@@ -123,7 +125,7 @@ __device__ __forceinline__ void eval_block(ExactState& S, const float* row, cons
       S.cv = cv0;
       S.r = r0;
 #pragma unroll 1
-      for (int i = 0; i < 4; ++i) exact_step(S, row, x, sg, dd + i, ev[4 * g + i], ivt[dd + i]);
+      for (int i = 0; i < 4; ++i) exact_step(S, row, x, sg, dd + i, __ldg(row + x + sg * (dd + i)), ivt[dd + i]);
     } else if (rec) {
       S.Mvalid = false;
     }
@@ -217,20 +219,35 @@ __device__ int exact_pov(const float* row, const float* wm, const float* ivt, in
     return S.cv;
   }
   if (D < 1) return 0;
-  // position blocks in scan order
+  // position blocks in scan order, the window maxima of kWm blocks loaded
+  // together (one L2 round trip per kWm blocks); candidates are re-tested
+  // against lo as raised by the blocks evaluated since (it only rises)
   const int pfirst = x + sg, plast = x + sg * D;
   const int w0 = pfirst >> 4, w1 = plast >> 4;
-  float wmv = __ldg(wm + w0);  // window maximum of the current block, loaded one block ahead
-  for (int w = w0;; w += sg) {
-    const int da = max(1, sg > 0 ? 16 * w - x : x - (16 * w + 15));
-    const int db = min(D, sg > 0 ? 16 * w + 15 - x : x - 16 * w);
-    const float wnext = w != w1 ? __ldg(wm + w + sg) : 0.f;
-    const float N = __fadd_rn(__fsub_rn(wmv, S.hf), -S.hl);
-    if (!(__fmul_rn(N, ivt[da]) < S.lo && __fmul_rn(N, ivt[db]) < S.lo)) {
-      eval_block(S, row, ivt, x, sg, da, db);
+  const int nblk = (w1 - w0) * sg + 1;
+  constexpr int kWm = 8;
+  for (int b0 = 0; b0 < nblk; b0 += kWm) {
+    unsigned cand = 0;
+#pragma unroll
+    for (int u = 0; u < kWm; ++u) {
+      const int w = w0 + sg * (b0 + u);
+      const float wv = b0 + u < nblk ? __ldg(wm + w) : -INFINITY;
+      const int da = max(1, sg > 0 ? 16 * w - x : x - (16 * w + 15));
+      const int db = min(D, sg > 0 ? 16 * w + 15 - x : x - 16 * w);
+      const float N = __fadd_rn(__fsub_rn(wv, S.hf), -S.hl);
+      if (b0 + u < nblk && !(__fmul_rn(N, ivt[da]) < S.lo && __fmul_rn(N, ivt[db]) < S.lo)) cand |= 1u << u;
     }
-    if (w == w1) break;
-    wmv = wnext;
+    while (cand != 0) {
+      const int u = __ffs(cand) - 1;
+      cand &= cand - 1;
+      const int w = w0 + sg * (b0 + u);
+      const int da = max(1, sg > 0 ? 16 * w - x : x - (16 * w + 15));
+      const int db = min(D, sg > 0 ? 16 * w + 15 - x : x - 16 * w);
+      const float N = __fadd_rn(__fsub_rn(__ldg(wm + w), S.hf), -S.hl);  // L1 hit
+      if (!(__fmul_rn(N, ivt[da]) < S.lo && __fmul_rn(N, ivt[db]) < S.lo)) {
+        eval_block(S, row, ivt, x, sg, da, db);
+      }
+    }
   }
   return S.cv;
 }
