@@ -10,8 +10,10 @@
 // intrinsics in the reference's order, so the per-cell sum is bit-identical
 // to total_viewshed_raw when sectors are accumulated on one GPU.
 // HBM roofline: per sector ~8 B of cv gathered per cell (the cv block a tile
-// needs, staged by unskew_tiled_kernel) + 16 B of map RMW per cell per batch.
+// needs, staged by unskew_pipe_kernel) + 16 B of map RMW per cell per batch.
 #include <cuda_runtime.h>
+
+#include <cstdlib>
 
 #include "sks_device.cuh"
 
@@ -71,24 +73,41 @@ __global__ void __launch_bounds__(256) unskew_kernel(BatchDev b, const double* _
   map[idx] = acc;
 }
 
-// Tiled form of unskew_kernel<true> (same per-cell arithmetic, same
-// ascending-k order). A CTA owns a 32x32 tile of DEM cells (each thread 4
-// cells of one column); per sector it stages the block of cv rows the tile
-// gathers from (<= 66 rows x 32 columns, loaded along j, i.e. coalesced for
-// transposed sectors too) plus the tile's dest/frac columns in shared
-// memory, then every cell reads its two values from there.
 constexpr int kUT = 32;           // tile edge (cells)
-constexpr int kUR = 2 * kUT + 2;  // cv rows a tile can touch (shear <= 45 deg)
 
-__global__ void __launch_bounds__(256) unskew_tiled_kernel(BatchDev b, double* __restrict__ map,
-                                                           int dimy, int dimx) {
-  __shared__ int scv[kUR][kUT + 1];
-  __shared__ int sdest[kUT];
-  __shared__ double sfrac[kUT];
+// Tiled unskew (same per-cell arithmetic as unskew_kernel<true>, same
+// ascending-k order). A CTA owns a 32x32 tile of DEM cells (each thread 4
+// cells of one column) and walks the batch's sectors; the cv block is staged
+// by SOURCE row: T[ir][jl] =
+// cv(p = base + i - dest[j], j) for i = i_lo - 1 + ir, so a cell (i, j)
+// reads rows p and p-1 as T[i - i_lo + 1][jl] and T[i - i_lo][jl]: a warp
+// reads one T row (non-transposed sectors) or one T column (transposed;
+// stride 33) and never hits a bank twice, where indexing the staged block
+// by skewed row p serialises up to 32-way at 45 degrees. 33 x 32 staged
+// values per sector instead of up to 66 x 32; dest[j] is recomputed with
+// the reference's double ops (shear_params, skew.cpp:97-101), so the
+// staging addresses need no dependent load. Sector s+1 is copied with
+// cp.async into the second buffer while sector s is computed.
+constexpr int kTR = kUT + 1;  // staged source rows (the tile's rows + the row above)
+
+__device__ __forceinline__ void cp_async4(void* smem_dst, const void* gmem_src) {
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 4;\n" ::"r"(static_cast<unsigned>(__cvta_generic_to_shared(smem_dst))),
+               "l"(gmem_src));
+}
+
+__device__ __forceinline__ void cp_async8(void* smem_dst, const void* gmem_src) {
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 8;\n" ::"r"(static_cast<unsigned>(__cvta_generic_to_shared(smem_dst))),
+               "l"(gmem_src));
+}
+
+__global__ void __launch_bounds__(256) unskew_pipe_kernel(BatchDev b, double* __restrict__ map, int dimy, int dimx) {
+  __shared__ int scv[2][kTR][kUT + 1];
+  __shared__ int sdest[2][kUT];
+  __shared__ double sfrac[2][kUT];
   const int tx = threadIdx.x & 31;
   const int ty = threadIdx.x >> 5;  // 0..7
   const int y0 = blockIdx.y * kUT, x0 = blockIdx.x * kUT;
-  const int ye = min(dimy, y0 + kUT) - 1, xe = min(dimx, x0 + kUT) - 1;  // last cell of the tile
+  const int ye = min(dimy, y0 + kUT) - 1, xe = min(dimx, x0 + kUT) - 1;
   const int sj = x0 + tx;
   double acc[4];
 #pragma unroll
@@ -96,42 +115,53 @@ __global__ void __launch_bounds__(256) unskew_tiled_kernel(BatchDev b, double* _
     const int si = y0 + ty + 8 * u;
     acc[u] = (si < dimy && sj < dimx) ? map[static_cast<long long>(si) * dimx + sj] : 0.0;
   }
-  for (int s = 0; s < b.n_sectors; ++s) {
-    const SectorDev& sd = b.sectors[s];
-    const int* iv = sd.inv;
-    // pre_ops ranges of the tile: the affine maps are axis permutations/flips,
-    // so the extremes are at the corners
+  // the tile's pre_ops box of sector s (axis permutations/flips: corners)
+  auto box = [&](int s, int* i_lo, int* j_lo) {
+    const int* iv = b.sectors[s].inv;
     const int ia = iv[0] * y0 + iv[1] * x0 + iv[2], ib = iv[0] * ye + iv[1] * xe + iv[2];
     const int ja = iv[3] * y0 + iv[4] * x0 + iv[5], jb = iv[3] * ye + iv[4] * xe + iv[5];
-    const int i_lo = min(ia, ib), i_hi = max(ia, ib);
-    const int j_lo = min(ja, jb), j_hi = max(ja, jb);
-    const int nj = j_hi - j_lo + 1;
-    const int* dest = b.dest + sd.col_off;
-    const int d_lo = __ldg(dest + j_lo), d_hi = __ldg(dest + j_hi);
-    const int p_lo = sd.base + i_lo - d_hi - 1;  // includes the p-1 rows
-    const int np = sd.base + i_hi - d_lo - p_lo + 1;
-    // row-block sharding: rows outside [q_lo, q_hi) belong to another run
-    // (their cv contributes 0 here; the runs' maps sum to the total)
-    const int q_lo = sd.q_lo, q_hi = sd.q_hi;
-    if (max(p_lo, q_lo) >= min(p_lo + np, q_hi)) continue;  // nothing owned here (uniform across the CTA)
-    const bool whole = q_lo <= p_lo && q_hi >= p_lo + np;   // always so on one GPU
-    __syncthreads();  // previous sector's smem reads are done
+    *i_lo = min(ia, ib);
+    *j_lo = min(ja, jb);
+    return max(ja, jb) - *j_lo + 1;  // nj
+  };
+  auto stage = [&](int s, int bf) {
+    const SectorDev& sd = b.sectors[s];
+    int i_lo, j_lo;
+    const int nj = box(s, &i_lo, &j_lo);
     if (threadIdx.x < nj) {
-      sdest[threadIdx.x] = __ldg(dest + j_lo + threadIdx.x);
-      sfrac[threadIdx.x] = __ldg(b.fracd + sd.col_off + j_lo + threadIdx.x);
+      cp_async4(&sdest[bf][threadIdx.x], b.dest + sd.col_off + j_lo + threadIdx.x);
+      cp_async8(&sfrac[bf][threadIdx.x], b.fracd + sd.col_off + j_lo + threadIdx.x);
     }
-    const int* cvb = b.cv + sd.sdem_off + static_cast<long long>(p_lo) * sd.pitch + j_lo;
-    if (whole) {
-      for (int r = ty; r < np; r += 8) {
-        if (tx < nj) scv[r][tx] = __ldg(cvb + static_cast<long long>(r) * sd.pitch + tx);
+    if (tx < nj) {
+      const int j = j_lo + tx;
+      const int dj = __double2int_rz(__dmul_rn(sd.shear_tan, static_cast<double>(j)));
+      const int* col = b.cv + sd.sdem_off + j;
+      for (int ir = ty; ir < kTR; ir += 8) {
+        const int p = sd.base + (i_lo - 1 + ir) - dj;
+        if (p >= sd.q_lo && p < sd.q_hi && p >= 0 && p < sd.skw_rows) {
+          cp_async4(&scv[bf][ir][tx], col + static_cast<long long>(p) * sd.pitch);
+        } else {
+          scv[bf][ir][tx] = 0;  // outside the sector or another run's row
+        }
       }
+    }
+  };
+  stage(0, 0);
+  asm volatile("cp.async.commit_group;\n" ::);
+  for (int s = 0; s < b.n_sectors; ++s) {
+    const int bf = s & 1;
+    if (s + 1 < b.n_sectors) {
+      stage(s + 1, bf ^ 1);
+      asm volatile("cp.async.commit_group;\n" ::);
+      asm volatile("cp.async.wait_group 1;\n" ::);
     } else {
-      for (int r = ty; r < np; r += 8) {
-        const int p = p_lo + r;
-        if (tx < nj) scv[r][tx] = (p >= q_lo && p < q_hi) ? __ldg(cvb + static_cast<long long>(r) * sd.pitch + tx) : 0;
-      }
+      asm volatile("cp.async.wait_group 0;\n" ::);
     }
-    __syncthreads();
+    __syncthreads();  // sector s's buffer complete for every thread
+    const SectorDev& sd = b.sectors[s];
+    int i_lo, j_lo;
+    box(s, &i_lo, &j_lo);
+    const int* iv = sd.inv;
 #pragma unroll
     for (int u = 0; u < 4; ++u) {
       const int si = y0 + ty + 8 * u;
@@ -139,19 +169,18 @@ __global__ void __launch_bounds__(256) unskew_tiled_kernel(BatchDev b, double* _
       const int i = iv[0] * si + iv[1] * sj + iv[2];
       const int j = iv[3] * si + iv[4] * sj + iv[5];
       const int jl = j - j_lo;
-      const int p = sd.base + i - sdest[jl];
-      const double r = sfrac[jl];
+      const int ir = i - i_lo + 1;  // T row of p; p - 1 is T row ir - 1
+      const double r = sfrac[bf][jl];
       const double omr = __dsub_rn(1.0, r);
       const double w_p = (i + 1 < sd.rows) ? __dadd_rn(omr, r) : omr;
       const double w_m = (i >= 1) ? __dadd_rn(omr, r) : r;
       const bool a = full_d(w_p);
       const bool c = full_d(w_m);
       double va = 0.0, vb = 0.0;
-      if (a) va = __dmul_rn(static_cast<double>(scv[p - p_lo][jl]), sd.correction);
-      if (!a || c) vb = __dmul_rn(static_cast<double>(scv[p - 1 - p_lo][jl]), sd.correction);
+      if (a) va = __dmul_rn(static_cast<double>(scv[bf][ir][jl]), sd.correction);
+      if (!a || c) vb = __dmul_rn(static_cast<double>(scv[bf][ir - 1][jl]), sd.correction);
       if (!a && !c && b.dem != nullptr) {
-        // the only read that may fall outside the row ranges (skwVS is 0
-        // there, scan.cpp:66); with fused relocation nothing zeroed it
+        const int p = sd.base + i - sdest[bf][jl];
         const int2 rg = (p >= 1 && p - 1 < sd.skw_rows) ? __ldg(b.ranges + sd.row_off + p - 1) : make_int2(0, 0);
         if (j < rg.x || j >= rg.y) vb = 0.0;
       }
@@ -165,6 +194,7 @@ __global__ void __launch_bounds__(256) unskew_tiled_kernel(BatchDev b, double* _
       }
       acc[u] = __dadd_rn(acc[u], v);
     }
+    __syncthreads();  // buffer bf free before sector s+2 is staged into it
   }
 #pragma unroll
   for (int u = 0; u < 4; ++u) {
@@ -210,7 +240,7 @@ __global__ void cv_to_vs_kernel(const int* cvf, const int* cvb, double* out, lon
 int launch_unskew(const BatchDev& b, const float*, double* map, int dimy, int dimx,
                   void* stream) {
   dim3 grid((dimx + kUT - 1) / kUT, (dimy + kUT - 1) / kUT);
-  unskew_tiled_kernel<<<grid, 256, 0, static_cast<cudaStream_t>(stream)>>>(b, map, dimy, dimx);
+  unskew_pipe_kernel<<<grid, 256, 0, static_cast<cudaStream_t>(stream)>>>(b, map, dimy, dimx);
   return static_cast<int>(cudaGetLastError());
 }
 

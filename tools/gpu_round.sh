@@ -13,6 +13,6 @@ if [ "$2" != "skip_ref" ]; then
 fi
 timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file $OUT/launches.csv \
   python tools/prof_step.py --steps 1 > $OUT/launches.log 2>&1
-timeout 900 ncu --set full --clock-control none --import-source on -k regex:"scan2_kernel|relocate_kernel|fixup_kernel|unskew_tiled_kernel" -c 4 \
+timeout 900 ncu --set full --clock-control none --import-source on -k regex:"scan2_kernel|relocate_kernel|fixup_kernel|unskew_pipe_kernel" -c 4 \
   -o $OUT/full python tools/prof_step.py --steps 1 > $OUT/ncu_full.log 2>&1
 echo done
