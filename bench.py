@@ -230,7 +230,7 @@ def run_ours(args, world, rank, local):
     import torch
 
     import paper_2003_02200_b200 as sk
-    from paper_2003_02200_b200.distributed import my_sectors, total_viewshed_distributed
+    from paper_2003_02200_b200.distributed import RowBalancer, my_sectors, total_viewshed_distributed
 
     cfgid = args.config
     c = CONFIGS[cfgid]
@@ -245,12 +245,13 @@ def run_ours(args, world, rank, local):
     d_map = torch.zeros((n, n), dtype=torch.float64, device=dev)
     flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev)
     factor = sk.area_scale_factor(cfg, CELLSIZE)
+    balancer = RowBalancer(world)
 
     def step(want_stats):
         d_map.zero_()
         if world > 1:  # row-block sharding (distributed.py: balances terrain-dependent costs)
             st = ctx.run_rows(d_dem.data_ptr(), n, n, CELLSIZE, cfg, rank, world, d_map.data_ptr(),
-                              stream=stream.cuda_stream, want_stats=want_stats)
+                              stream=stream.cuda_stream, want_stats=want_stats, cuts=balancer.cuts)
         else:
             st = ctx.run_sectors(d_dem.data_ptr(), n, n, CELLSIZE, cfg, mine, d_map.data_ptr(),
                                  stream=stream.cuda_stream, want_stats=want_stats)
@@ -261,8 +262,22 @@ def run_ours(args, world, rank, local):
             ctx.scale(d_map.data_ptr(), n * n, ns, CELLSIZE, int(cfg.units), stream.cuda_stream)
         return st
 
+    rank_ms = []
     for _ in range(args.warmup):
-        step(False)
+        wst = step(world > 1)
+        if world > 1:
+            # warm-up doubles as the row-block rebalancing: every rank's kernel
+            # time for its blocks (the phase events, which exclude the host's
+            # plan building for new cuts), all-gathered, moves the cuts; they
+            # are frozen for the timed steps
+            import torch.distributed as dist
+            torch.cuda.synchronize()
+            busy = (wst.skew_seconds + wst.scan_seconds + wst.fixup_seconds + wst.unskew_seconds) * 1e3
+            mine_t = torch.tensor([busy], dtype=torch.float64, device=dev)
+            got = [torch.zeros_like(mine_t) for _ in range(world)]
+            dist.all_gather(got, mine_t)
+            rank_ms = [float(x.item()) for x in got]
+            balancer.update(rank_ms)
     torch.cuda.synchronize()
 
     sampler = ClockSampler(local)
@@ -316,7 +331,7 @@ def run_ours(args, world, rank, local):
         if world == 1:
             ctx.total_viewshed(pinned_dem.numpy(), CELLSIZE, cfg, out=pinned_out.numpy())
         else:
-            total_viewshed_distributed(pinned_dem.numpy(), CELLSIZE, cfg, context=ctx)
+            total_viewshed_distributed(pinned_dem.numpy(), CELLSIZE, cfg, context=ctx, cuts=balancer.cuts)
             torch.cuda.synchronize()
         t1 = time.perf_counter()
         if i >= args.warmup:
@@ -353,6 +368,10 @@ def run_ours(args, world, rank, local):
                    "l2": "flushed between timed steps (256 MiB device write, untimed)",
                    "parallelism": (f"row-block sharded x{world} (every sector), NCCL reduce of f64 maps" if world > 1
                                    else "single GPU, all sectors")},
+        "row_balance": ({"cuts": [round(float(x), 6) for x in balancer.cuts],
+                         "last_warmup_rank_ms": [round(x, 3) for x in rank_ms],
+                         "note": "row-block cuts moved from measured per-rank times during warm-up, then frozen"}
+                        if world > 1 else None),
         "roofline": {"kernel": "scan_kernel (FP32-issue bound)", "bound": "fp32",
                      "achieved": scan_achieved / 1e12, "peak": fp32_peak / 1e12, "unit": "TFLOP/s",
                      "frac": scan_achieved / fp32_peak, "traffic": traffic,

@@ -202,6 +202,15 @@ sks_status sks_context_run_rows(sks_context* ctx, const float* d_dem, int dimy,
                                 int dimx, double cellsize,
                                 const sks_run_config* cfg, int part, int nparts,
                                 double* d_map, void* stream, sks_stats* stats);
+/* The same with the row blocks placed by cuts (nparts + 1 non-decreasing
+   fractions of each sector's modelled cost, cuts[0] = 0, cuts[nparts] = 1;
+   NULL = equal shares): measured-time rebalancing across GPUs
+   (paper_2003_02200_b200/distributed.py RowBalancer). Every rank must pass
+   the same cuts. */
+sks_status sks_context_run_rows_cuts(sks_context* ctx, const float* d_dem, int dimy,
+                                     int dimx, double cellsize, const sks_run_config* cfg,
+                                     int part, int nparts, const double* cuts, double* d_map,
+                                     void* stream, sks_stats* stats);
 
 /* d_map[i] *= area_scale_factor(ns, cellsize, units) on `stream`. */
 sks_status sks_context_scale(sks_context* ctx, double* d_map, long long n,

@@ -116,6 +116,8 @@ SIGNATURES = {
                                           C.c_double, C.c_double]),
     "sks_context_run_rows": (C.c_int, [_vp, _vp, C.c_int, C.c_int, C.c_double, C.POINTER(RunConfigC),
                                        C.c_int, C.c_int, _vp, _vp, C.POINTER(StatsC)]),
+    "sks_context_run_rows_cuts": (C.c_int, [_vp, _vp, C.c_int, C.c_int, C.c_double, C.POINTER(RunConfigC),
+                                            C.c_int, C.c_int, _vp, _vp, _vp, C.POINTER(StatsC)]),
     "sks_singular_viewshed": (C.c_int, [_vp, C.c_int, C.c_int, C.c_double, C.c_int, C.c_int, C.c_double,
                                         C.c_int, C.c_double, C.c_int, _vp]),
     "sks_multi_viewshed": (C.c_int, [_vp, C.c_int, C.c_int, C.c_double, _vp, C.c_int, C.c_double, C.c_int,

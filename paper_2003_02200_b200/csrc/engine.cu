@@ -291,7 +291,8 @@ struct sks_context {
   int sms = 0;
   std::mutex mu;
   // plan cache
-  std::map<std::tuple<int, int, int, double, double, std::vector<int>, int, int>, std::unique_ptr<Plans>>
+  std::map<std::tuple<int, int, int, double, double, std::vector<int>, int, int, std::vector<double>>,
+           std::unique_ptr<Plans>>
       cache;
   // work buffers
   DevBuf sdem, cv, cvb, queue, fixcnt, fixoff, wm16, counters, dem, map, vis, check;
@@ -302,15 +303,16 @@ struct sks_context {
   void activate() const { cuda_check(cudaSetDevice(device), "cudaSetDevice"); }
 
   Plans& plans_for(int dimy, int dimx, int ns, double cellsize, double max_distance,
-                   const std::vector<int>& sectors, int part = 0, int nparts = 1) {
-    auto key = std::make_tuple(dimy, dimx, ns, cellsize, max_distance, sectors, part, nparts);
+                   const std::vector<int>& sectors, int part = 0, int nparts = 1,
+                   const std::vector<double>& cuts = {}) {
+    auto key = std::make_tuple(dimy, dimx, ns, cellsize, max_distance, sectors, part, nparts, cuts);
     auto it = cache.find(key);
     if (it != cache.end()) return *it->second;
     if (cache.size() > 16) cache.clear();
     auto P = std::make_unique<Plans>();
     for (int k : sectors) {
       P->plans.push_back(plan_sector(k, ns, dimy, dimx, cellsize, max_distance));
-      if (nparts > 1) set_row_block(P->plans.back(), part, nparts);
+      if (nparts > 1) set_row_block(P->plans.back(), part, nparts, cuts.empty() ? nullptr : cuts.data());
     }
     make_batches(*P, device);
     Plans& ref = *P;
@@ -464,13 +466,14 @@ double elapsed(cudaEvent_t a, cudaEvent_t b) {
 // Core: run the given sectors on device data. Accumulates into d_map.
 void run_sectors(sks_context* ctx, const float* d_dem, int dimy, int dimx, double cellsize,
                  const sks_run_config* cfg, std::vector<int> sectors, double* d_map,
-                 cudaStream_t st, sks_stats* stats, bool force_exact, int part = 0, int nparts = 1) {
+                 cudaStream_t st, sks_stats* stats, bool force_exact, int part = 0, int nparts = 1,
+                 const std::vector<double>& cuts = {}) {
   std::sort(sectors.begin(), sectors.end());
   sectors.erase(std::unique(sectors.begin(), sectors.end()), sectors.end());
   for (int k : sectors) {
     if (k < 0 || k >= cfg->ns / 2) throw std::out_of_range("sector index out of range");
   }
-  Plans& P = ctx->plans_for(dimy, dimx, cfg->ns, cellsize, cfg->max_distance, sectors, part, nparts);
+  Plans& P = ctx->plans_for(dimy, dimx, cfg->ns, cellsize, cfg->max_distance, sectors, part, nparts, cuts);
   const long long launches0 = ctx->launches;
   double t_skew = 0, t_scan = 0, t_fix = 0, t_unskew = 0;
   long long flagged = 0, evals = 0, skipped = 0;
@@ -774,9 +777,25 @@ sks_status sks_context_run_sectors(sks_context* ctx, const float* d_dem, int dim
 sks_status sks_context_run_rows(sks_context* ctx, const float* d_dem, int dimy, int dimx,
                                 double cellsize, const sks_run_config* cfg, int part, int nparts,
                                 double* d_map, void* stream, sks_stats* stats) {
+  return sks_context_run_rows_cuts(ctx, d_dem, dimy, dimx, cellsize, cfg, part, nparts, nullptr, d_map, stream,
+                                   stats);
+}
+
+sks_status sks_context_run_rows_cuts(sks_context* ctx, const float* d_dem, int dimy, int dimx,
+                                     double cellsize, const sks_run_config* cfg, int part, int nparts,
+                                     const double* cuts, double* d_map, void* stream, sks_stats* stats) {
   return guarded([&] {
     if (!ctx || !cfg || !d_dem || !d_map) throw std::invalid_argument("null argument");
     if (nparts < 1 || part < 0 || part >= nparts) throw std::out_of_range("row part out of range");
+    std::vector<double> cv;
+    if (cuts != nullptr && nparts > 1) {
+      cv.assign(cuts, cuts + nparts + 1);
+      for (int b = 0; b <= nparts; ++b) {
+        if (!(cv[b] >= 0.0 && cv[b] <= 1.0) || (b > 0 && cv[b] < cv[b - 1])) {
+          throw std::invalid_argument("row cuts must be non-decreasing fractions in [0, 1]");
+        }
+      }
+    }
     const std::string err = validate_grid_header(dimy, dimx, cellsize);
     if (!err.empty()) throw std::invalid_argument(err);
     ctx->activate();
@@ -788,7 +807,7 @@ sks_status sks_context_run_rows(sks_context* ctx, const float* d_dem, int dimy, 
     const bool exact = device_check(ctx, d_dem, dimy, dimx, cfg, static_cast<cudaStream_t>(stream));
     local.kernel_launches += 1;  // dem_check
     run_sectors(ctx, d_dem, dimy, dimx, cellsize, cfg, all, d_map, static_cast<cudaStream_t>(stream),
-                stats ? &local : nullptr, exact, part, nparts);
+                stats ? &local : nullptr, exact, part, nparts, cv);
     if (stats) *stats = local;
   });
 }

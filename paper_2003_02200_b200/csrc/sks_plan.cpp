@@ -95,7 +95,7 @@ void fill_tables(SectorPlanH& p) {
 
 }  // namespace
 
-void set_row_block(SectorPlanH& p, int part, int nparts) {
+void set_row_block(SectorPlanH& p, int part, int nparts, const double* cuts) {
   if (nparts <= 1) {
     p.q_lo = 0;
     p.q_hi = p.skw_rows;
@@ -120,7 +120,10 @@ void set_row_block(SectorPlanH& p, int part, int nparts) {
     if (b >= nparts) return p.skw_rows;
     long long cum = 0;
     for (int q = 0; q < p.skw_rows; ++q) {
-      if (cum * nparts >= static_cast<long long>(b) * total) return q;
+      if (cuts != nullptr ? static_cast<double>(cum) >= cuts[b] * static_cast<double>(total)
+                          : cum * nparts >= static_cast<long long>(b) * total) {
+        return q;
+      }
       cum += row_cost(q);
     }
     return p.skw_rows;

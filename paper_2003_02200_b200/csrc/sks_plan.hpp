@@ -51,7 +51,11 @@ struct SectorPlanH {
 // Row-block sharding: the skewed rows of a sector split into
 // nparts contiguous blocks of equal exact scan work; block `part` of the
 // plan's rows. Sets p.q_lo / p.q_hi.
-void set_row_block(SectorPlanH& p, int part, int nparts);
+// Row block `part` of `nparts` of the sector's skewed rows, balanced by the
+// row cost model; with cuts (nparts + 1 non-decreasing fractions, 0 .. 1)
+// block b holds the rows whose preceding cost lies in [cuts[b], cuts[b+1])
+// of the total (measured-time rebalancing, distributed.py).
+void set_row_block(SectorPlanH& p, int part, int nparts, const double* cuts = nullptr);
 
 // skew.cpp:16-19
 int base_offset(int src_rows, int cols, double shear_tan);

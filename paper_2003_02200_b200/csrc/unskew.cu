@@ -124,8 +124,21 @@ __global__ void __launch_bounds__(256) unskew_pipe_kernel(BatchDev b, double* __
     *j_lo = min(ja, jb);
     return max(ja, jb) - *j_lo + 1;  // nj
   };
+  // false when none of the skewed rows the tile reads belongs to this run
+  // (row-block sharding; uniform across the CTA)
+  auto owned = [&](int s) {
+    const SectorDev& sd = b.sectors[s];
+    if (sd.q_lo <= 0 && sd.q_hi >= sd.skw_rows) return true;
+    int i_lo, j_lo;
+    const int nj = box(s, &i_lo, &j_lo);
+    const int d_lo = __double2int_rz(__dmul_rn(sd.shear_tan, static_cast<double>(j_lo)));
+    const int d_hi = __double2int_rz(__dmul_rn(sd.shear_tan, static_cast<double>(j_lo + nj - 1)));
+    const int p_min = sd.base + i_lo - 1 - d_hi, p_max = sd.base + i_lo + kUT - 1 - d_lo;
+    return max(p_min, sd.q_lo) <= min(p_max, sd.q_hi - 1);
+  };
   auto stage = [&](int s, int bf) {
     const SectorDev& sd = b.sectors[s];
+    if (!owned(s)) return;
     int i_lo, j_lo;
     const int nj = box(s, &i_lo, &j_lo);
     if (threadIdx.x < nj) {
@@ -159,6 +172,10 @@ __global__ void __launch_bounds__(256) unskew_pipe_kernel(BatchDev b, double* __
     }
     __syncthreads();  // sector s's buffer complete for every thread
     const SectorDev& sd = b.sectors[s];
+    if (!owned(s)) {
+      __syncthreads();
+      continue;
+    }
     int i_lo, j_lo;
     box(s, &i_lo, &j_lo);
     const int* iv = sd.inv;

@@ -19,6 +19,9 @@ Two ways to share the work:
 * ``mode="sectors"``: whole sectors by LPT on the exact work
   (``sks_partition_sectors``), the paper's scheme.
 
+``RowBalancer`` moves the row-block boundaries from measured per-rank times
+(bench.py adapts during its warm-up steps and then freezes them).
+
 ``compute`` lets CPU tests (gloo, world_size 2) exercise exactly this
 sharding/reduce logic with the oracle standing in for the GPU pipeline; the
 product path (compute=None) always runs the CUDA kernels.
@@ -32,6 +35,41 @@ import numpy as np
 from .engine import RunConfig, Units, area_scale_factor, partition_sectors
 
 
+class RowBalancer:
+    """Measured-time rebalancing of the row blocks across ranks.
+
+    The static split gives every rank an equal share of each sector's
+    MODELLED row cost (sks_plan.cpp set_row_block); terrain makes the real
+    cost per share differ by ~10 % between blocks at 8 GPUs. After a run with
+    cuts c and per-rank times t, the time is modelled as piecewise linear in
+    the cost fraction (density t_r / (c[r+1] - c[r]) on block r) and the new
+    cuts put an equal share of the total time in every block. Every rank
+    feeds the same all-gathered times, so every rank computes the same cuts
+    (deterministic float64 arithmetic).
+    """
+
+    def __init__(self, world: int):
+        self.world = int(world)
+        self.cuts = np.linspace(0.0, 1.0, self.world + 1)
+
+    def update(self, times: Sequence[float]) -> np.ndarray:
+        t = np.asarray(times, np.float64)
+        if t.shape != (self.world,) or not np.all(np.isfinite(t)) or t.sum() <= 0.0:
+            return self.cuts
+        c = self.cuts
+        T = np.concatenate([[0.0], np.cumsum(t)])
+        new = [0.0]
+        for b in range(1, self.world):
+            target = b * T[-1] / self.world
+            r = int(np.searchsorted(T, target, side="right") - 1)
+            r = min(max(r, 0), self.world - 1)
+            frac = (target - T[r]) / t[r] if t[r] > 0.0 else 0.0
+            new.append(float(c[r] + min(max(frac, 0.0), 1.0) * (c[r + 1] - c[r])))
+        new.append(1.0)
+        self.cuts = np.maximum.accumulate(np.clip(np.asarray(new), 0.0, 1.0))
+        return self.cuts
+
+
 def my_sectors(ns: int, dimy: int, dimx: int, world: int, rank: int, cellsize: float = 1.0,
                max_distance: Optional[float] = None) -> list:
     owner = partition_sectors(ns, dimy, dimx, world, cellsize, max_distance)
@@ -40,7 +78,8 @@ def my_sectors(ns: int, dimy: int, dimx: int, world: int, rank: int, cellsize: f
 
 def total_viewshed_distributed(dem: np.ndarray, cellsize: float, cfg: RunConfig, raw: bool = False,
                                compute: Optional[Callable[[Sequence[int]], np.ndarray]] = None,
-                               context=None, stream=None, stats: Optional[dict] = None, mode: str = "rows"):
+                               context=None, stream=None, stats: Optional[dict] = None, mode: str = "rows",
+                               cuts=None):
     """Total viewshed of ``dem`` sharded over the default process group.
 
     Returns the (scaled unless ``raw``) map on rank 0 and None elsewhere.
@@ -69,7 +108,7 @@ def total_viewshed_distributed(dem: np.ndarray, cellsize: float, cfg: RunConfig,
     d_map = torch.zeros((dimy, dimx), dtype=torch.float64, device=dev)
     if mode == "rows":
         es = ctx.run_rows(d_dem.data_ptr(), dimy, dimx, cellsize, cfg, rank, world, d_map.data_ptr(),
-                          stream=st.cuda_stream, want_stats=stats is not None)
+                          stream=st.cuda_stream, want_stats=stats is not None, cuts=cuts)
     else:
         es = ctx.run_sectors(d_dem.data_ptr(), dimy, dimx, cellsize, cfg, mine, d_map.data_ptr(),
                              stream=st.cuda_stream, want_stats=stats is not None)

@@ -406,13 +406,21 @@ class Context:
         return EngineStats.from_c(st) if want_stats else None
 
     def run_rows(self, d_dem: int, dimy: int, dimx: int, cellsize: float, cfg: RunConfig, part: int,
-                 nparts: int, d_map: int, stream: int = 0, want_stats: bool = False):
+                 nparts: int, d_map: int, stream: int = 0, want_stats: bool = False, cuts=None):
         """All sectors, row block `part` of `nparts` of every sector (row-block
-        sharding across GPUs; the nparts maps sum to the total raw map)."""
+        sharding across GPUs; the nparts maps sum to the total raw map).
+        ``cuts`` (nparts + 1 non-decreasing fractions of the modelled cost,
+        identical on every rank) places the blocks; None = equal shares."""
         c = cfg.to_c()
         st = _lib.StatsC()
-        check(lib.sks_context_run_rows(self._h, d_dem, dimy, dimx, cellsize, C.byref(c), part, nparts, d_map,
-                                       stream, C.byref(st) if want_stats else None))
+        cp = None
+        if cuts is not None:
+            cuts_arr = np.ascontiguousarray(cuts, np.float64)
+            if cuts_arr.shape != (nparts + 1,):
+                raise ValueError(f"cuts must hold nparts + 1 = {nparts + 1} fractions")
+            cp = cuts_arr.ctypes.data
+        check(lib.sks_context_run_rows_cuts(self._h, d_dem, dimy, dimx, cellsize, C.byref(c), part, nparts, cp,
+                                            d_map, stream, C.byref(st) if want_stats else None))
         return EngineStats.from_c(st) if want_stats else None
 
     def scale(self, d_map: int, n: int, ns: int, cellsize: float, units: int, stream: int = 0):

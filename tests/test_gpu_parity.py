@@ -415,6 +415,32 @@ def test_fused_relocation_bitexact(ora, shape, kind, ns, maxd, monkeypatch):
     ctx.close()
 
 
+def test_row_block_cuts_sum_to_total(ora):
+    """Row blocks placed by explicit cuts (the measured-time rebalancing
+    path): any non-decreasing cuts partition every sector's rows, so the
+    parts still sum to the total; bad cuts are rejected."""
+    import torch
+
+    vals = sk.make_synthetic(sk.SyntheticKind.Fractal, 60, 72, 10.0, 4).values
+    cfg = sk.RunConfig(ns=24, h0=1.5, units=sk.Units.SquareMeters)
+    ref = ora.total_viewshed(vals, 10.0, 24, 1.5, raw=True)
+    ctx = sk.Context(0)
+    d_dem = torch.from_numpy(vals).cuda()
+    st = torch.cuda.current_stream().cuda_stream
+    for cuts in ([0.0, 0.1, 0.75, 1.0], [0.0, 0.0, 0.5, 1.0], [0.0, 0.3, 0.3, 1.0]):
+        total = np.zeros(vals.shape, np.float64)
+        for part in range(3):
+            d_map = torch.zeros(vals.shape, dtype=torch.float64, device="cuda")
+            ctx.run_rows(d_dem.data_ptr(), *vals.shape, 10.0, cfg, part, 3, d_map.data_ptr(), stream=st, cuts=cuts)
+            torch.cuda.synchronize()
+            total += d_map.cpu().numpy()
+        np.testing.assert_allclose(total, ref, rtol=1e-12, atol=0)
+    d_map = torch.zeros(vals.shape, dtype=torch.float64, device="cuda")
+    with pytest.raises(ValueError, match="non-decreasing"):
+        ctx.run_rows(d_dem.data_ptr(), *vals.shape, 10.0, cfg, 0, 3, d_map.data_ptr(), stream=st,
+                     cuts=[0.0, 0.6, 0.4, 1.0])
+
+
 def test_row_blocks_balance_exact_work():
     """Every target of every sector is owned by exactly one part."""
     import torch

@@ -19,12 +19,13 @@ import torch  # noqa: E402
 
 import bench  # noqa: E402
 import paper_2003_02200_b200 as sk  # noqa: E402
-from paper_2003_02200_b200.distributed import my_sectors  # noqa: E402
+from paper_2003_02200_b200.distributed import RowBalancer, my_sectors  # noqa: E402
 
 ap = argparse.ArgumentParser()
 ap.add_argument("--config", type=int, default=2)
 ap.add_argument("--mode", default="rows")
 ap.add_argument("--reps", type=int, default=3)
+ap.add_argument("--balance", type=int, default=3, help="rebalancing rounds (rows mode, as bench.py's warm-up)")
 a = ap.parse_args()
 c = bench.CONFIGS[a.config]
 n, ns, maxd = c["n"], c["ns"], c["max_distance"]
@@ -36,16 +37,48 @@ d_map = torch.zeros((n, n), dtype=torch.float64, device="cuda")
 st = torch.cuda.current_stream().cuda_stream
 
 
+CUTS = {}
+
+
 def run(world, rank):
     if a.mode == "rows":
-        ctx.run_rows(d_dem.data_ptr(), n, n, 10.0, cfg, rank, world, d_map.data_ptr(), stream=st)
+        ctx.run_rows(d_dem.data_ptr(), n, n, 10.0, cfg, rank, world, d_map.data_ptr(), stream=st,
+                     cuts=CUTS.get(world))
     else:
         ctx.run_sectors(d_dem.data_ptr(), n, n, 10.0, cfg, my_sectors(ns, n, n, world, rank, 10.0, maxd),
                         d_map.data_ptr(), stream=st)
 
 
-out = {"config": a.config, "mode": a.mode}
+def time_rank(world, rank, reps):
+    best = 1e30
+    for _ in range(reps):
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        torch.cuda.synchronize()
+        e0.record()
+        run(world, rank)
+        e1.record()
+        torch.cuda.synchronize()
+        best = min(best, e0.elapsed_time(e1))
+    return best
+
+
+out = {"config": a.config, "mode": a.mode, "balance_rounds": a.balance if a.mode == "rows" else 0}
 for world in (1, 2, 4, 8):
+    if a.mode == "rows" and world > 1 and a.balance > 0:
+        bal = RowBalancer(world)
+        hist = []
+        for _ in range(a.balance):  # bench.py's warm-up: measure (kernel phases), move the cuts
+            CUTS[world] = bal.cuts
+            t = []
+            for r in range(world):
+                es = ctx.run_rows(d_dem.data_ptr(), n, n, 10.0, cfg, r, world, d_map.data_ptr(), stream=st,
+                                  want_stats=True, cuts=bal.cuts)
+                t.append((es.skew_seconds + es.scan_seconds + es.fixup_seconds + es.unskew_seconds) * 1e3)
+            hist.append(round(max(t) / (sum(t) / world), 4))
+            bal.update(t)
+        CUTS[world] = bal.cuts
+        out[f"imbalance_history_{world}"] = hist
+        out[f"cuts_{world}"] = [round(float(x), 5) for x in bal.cuts]
     times = []
     for rank in range(world):
         run(world, rank)  # warm (plans, pools)
@@ -64,7 +97,7 @@ for world in (1, 2, 4, 8):
         phases = []
         for rank in range(world):
             es = ctx.run_rows(d_dem.data_ptr(), n, n, 10.0, cfg, rank, world, d_map.data_ptr(), stream=st,
-                              want_stats=True)
+                              want_stats=True, cuts=CUTS.get(world))
             phases.append({k: round(getattr(es, k) * 1e3, 3) for k in
                            ("skew_seconds", "scan_seconds", "fixup_seconds", "unskew_seconds")})
         out["phases_8"] = phases
