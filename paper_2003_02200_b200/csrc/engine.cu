@@ -331,6 +331,9 @@ struct sks_context {
     d.sdem = sdem.as<float>();
     d.cv = cv.as<int>();
     d.cv_bwd = split_bwd ? cvb.as<int>() : nullptr;
+    for (const SectorDev& sd : b.sdev) {
+      if (sd.q_lo > 0 || sd.q_hi < sd.skw_rows) d.row_blocks = 1;
+    }
     return d;
   }
 

@@ -54,6 +54,7 @@ struct BatchDev {
   // range), and the unskew treats cv outside the row ranges as 0. nullptr:
   // rows come from sdem written by relocate_kernel, which zeroes cv.
   const float* dem;
+  int row_blocks;  // some sector owns only a block of its rows (multi-GPU run_rows)
 };
 
 struct ScanArgs {

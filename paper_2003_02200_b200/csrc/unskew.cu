@@ -100,8 +100,11 @@ __device__ __forceinline__ void cp_async8(void* smem_dst, const void* gmem_src) 
                "l"(gmem_src));
 }
 
-__global__ void __launch_bounds__(256) unskew_pipe_kernel(BatchDev b, double* __restrict__ map, int dimy, int dimx) {
+template <bool kBlocks>  // row-block sharding: some tiles own no row of a sector
+__global__ void __launch_bounds__(256) unskew_pipe_kernel(BatchDev b, double* __restrict__ map, int dimy,
+                                                              int dimx) {
   __shared__ int scv[2][kTR][kUT + 1];
+  __shared__ int sown[2];  // sector staged in the buffer has owned rows in the tile
   __shared__ int sdest[2][kUT];
   __shared__ double sfrac[2][kUT];
   const int tx = threadIdx.x & 31;
@@ -127,6 +130,7 @@ __global__ void __launch_bounds__(256) unskew_pipe_kernel(BatchDev b, double* __
   // false when none of the skewed rows the tile reads belongs to this run
   // (row-block sharding; uniform across the CTA)
   auto owned = [&](int s) {
+    if (!kBlocks) return true;
     const SectorDev& sd = b.sectors[s];
     if (sd.q_lo <= 0 && sd.q_hi >= sd.skw_rows) return true;
     int i_lo, j_lo;
@@ -138,7 +142,9 @@ __global__ void __launch_bounds__(256) unskew_pipe_kernel(BatchDev b, double* __
   };
   auto stage = [&](int s, int bf) {
     const SectorDev& sd = b.sectors[s];
-    if (!owned(s)) return;
+    const bool own = owned(s);
+    if (kBlocks && threadIdx.x == 0) sown[bf] = own ? 1 : 0;
+    if (!own) return;
     int i_lo, j_lo;
     const int nj = box(s, &i_lo, &j_lo);
     if (threadIdx.x < nj) {
@@ -172,7 +178,7 @@ __global__ void __launch_bounds__(256) unskew_pipe_kernel(BatchDev b, double* __
     }
     __syncthreads();  // sector s's buffer complete for every thread
     const SectorDev& sd = b.sectors[s];
-    if (!owned(s)) {
+    if (kBlocks && sown[bf] == 0) {
       __syncthreads();
       continue;
     }
@@ -257,7 +263,11 @@ __global__ void cv_to_vs_kernel(const int* cvf, const int* cvb, double* out, lon
 int launch_unskew(const BatchDev& b, const float*, double* map, int dimy, int dimx,
                   void* stream) {
   dim3 grid((dimx + kUT - 1) / kUT, (dimy + kUT - 1) / kUT);
-  unskew_pipe_kernel<<<grid, 256, 0, static_cast<cudaStream_t>(stream)>>>(b, map, dimy, dimx);
+  if (b.row_blocks) {
+    unskew_pipe_kernel<true><<<grid, 256, 0, static_cast<cudaStream_t>(stream)>>>(b, map, dimy, dimx);
+  } else {
+    unskew_pipe_kernel<false><<<grid, 256, 0, static_cast<cudaStream_t>(stream)>>>(b, map, dimy, dimx);
+  }
   return static_cast<int>(cudaGetLastError());
 }
 
