@@ -343,7 +343,7 @@ struct sks_context {
     if (split_bwd) cvb.ensure(static_cast<size_t>(b.pool_elems) * sizeof(int), device);
     queue.ensure(static_cast<size_t>(b.fix_cap) * sizeof(unsigned), device);
     fixcnt.ensure(std::max<size_t>(b.items.size(), 1) * sizeof(unsigned), device);
-    fixoff.ensure((b.items.size() + 1) * sizeof(unsigned), device);
+    fixoff.ensure((b.items.size() + 1 + 1024) * sizeof(unsigned), device);  // + prefix block sums
     wm16.ensure(static_cast<size_t>(b.pool_elems / 16 + 1) * sizeof(float), device);
     counters.ensure(kCounterBytes, device);
   }
@@ -406,7 +406,7 @@ struct sks_context {
   void fixup_batch(const ScanArgs& a, cudaStream_t st) {
     if (a.n_items == 0) return;
     cuda_check(launch_fixup(a, fixoff.as<unsigned>(), st), "launch fixup");
-    launches += 2;
+    launches += 3;
   }
 
   ~sks_context() {

@@ -23,6 +23,7 @@
 #include <cuda_runtime.h>
 
 #include <cfloat>
+#include <algorithm>
 #include <cstdint>
 
 #include "sks_device.cuh"
@@ -252,43 +253,74 @@ __device__ int exact_pov(const float* row, const float* wm, const float* ivt, in
   return S.cv;
 }
 
-// Exclusive prefix of the queued POVs per scan item (one CTA): off[it] =
-// sum over items < it of fix_cnt * group; off[n_items] = total.
-__global__ void __launch_bounds__(1024) fixup_prefix_kernel(ScanArgs a, unsigned* off) {
-  __shared__ unsigned warp_sums[32];
-  const int n = a.n_items;
-  const int per = (n + blockDim.x - 1) / blockDim.x;
-  const int b0 = threadIdx.x * per, b1 = min(n, b0 + per);
-  const unsigned grp = static_cast<unsigned>(a.fix_group);
-  unsigned local = 0;
-  for (int i = b0; i < b1; ++i) local += a.fix_cnt[i] * grp;
-  // block exclusive scan of the per-thread sums
+// Exclusive prefix of the queued POVs per scan item: off[it] = sum over
+// items < it of fix_cnt * group, off[n_items] = total. Two fully parallel
+// passes over contiguous item chunks (coalesced): block sums, then each
+// block rescans its chunk from the sum of the blocks before it.
+constexpr int kPrefixThreads = 1024;
+
+__device__ __forceinline__ unsigned block_excl_scan(unsigned v, unsigned* warp_tot, unsigned* total) {
   const int lane = threadIdx.x & 31, wp = threadIdx.x >> 5;
-  unsigned incl = local;
+  unsigned incl = v;
 #pragma unroll
   for (int o = 1; o < 32; o <<= 1) {
     const unsigned u = __shfl_up_sync(0xffffffffu, incl, o);
     if (lane >= o) incl += u;
   }
-  if (lane == 31) warp_sums[wp] = incl;
+  if (lane == 31) warp_tot[wp] = incl;
   __syncthreads();
   if (wp == 0) {
-    unsigned ws = warp_sums[lane];
+    const unsigned ws = lane < (blockDim.x >> 5) ? warp_tot[lane] : 0u;
     unsigned wi = ws;
 #pragma unroll
     for (int o = 1; o < 32; o <<= 1) {
       const unsigned u = __shfl_up_sync(0xffffffffu, wi, o);
       if (lane >= o) wi += u;
     }
-    warp_sums[lane] = wi - ws;
+    warp_tot[lane] = wi - ws;
+    if (lane == 31) *total = wi;
   }
   __syncthreads();
-  unsigned run = warp_sums[wp] + incl - local;
-  for (int i = b0; i < b1; ++i) {
-    off[i] = run;
-    run += a.fix_cnt[i] * grp;
+  const unsigned r = warp_tot[wp] + incl - v;
+  __syncthreads();  // warp_tot / total reusable
+  return r;
+}
+
+__global__ void __launch_bounds__(kPrefixThreads) fixup_prefix_sums_kernel(ScanArgs a, int chunk, unsigned* bsum) {
+  __shared__ unsigned wt[32];
+  __shared__ unsigned tot;
+  const int b0 = blockIdx.x * chunk, b1 = min(a.n_items, b0 + chunk);
+  unsigned local = 0;
+  for (int i = b0 + threadIdx.x; i < b1; i += blockDim.x) local += __ldg(a.fix_cnt + i);
+  block_excl_scan(local, wt, &tot);
+  if (threadIdx.x == 0) bsum[blockIdx.x] = tot * static_cast<unsigned>(a.fix_group);
+}
+
+__global__ void __launch_bounds__(kPrefixThreads) fixup_prefix_write_kernel(ScanArgs a, int chunk, const unsigned* bsum,
+                                                                           unsigned* off) {
+  __shared__ unsigned wt[32];
+  __shared__ unsigned tot;
+  __shared__ unsigned base_s;
+  if (threadIdx.x < 32) {
+    unsigned b = 0;
+    for (int k = threadIdx.x; k < static_cast<int>(blockIdx.x); k += 32) b += bsum[k];
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) b += __shfl_down_sync(0xffffffffu, b, o);
+    if (threadIdx.x == 0) base_s = b;
   }
-  if (threadIdx.x == blockDim.x - 1) off[n] = run;
+  __syncthreads();
+  unsigned base = base_s;
+  const unsigned grp = static_cast<unsigned>(a.fix_group);
+  const int b0 = blockIdx.x * chunk, b1 = min(a.n_items, b0 + chunk);
+  for (int t0 = b0; t0 < b1; t0 += blockDim.x) {
+    const int i = t0 + threadIdx.x;
+    const unsigned v = i < b1 ? __ldg(a.fix_cnt + i) * grp : 0u;
+    const unsigned ex = block_excl_scan(v, wt, &tot);
+    if (i < b1) off[i] = base + ex;
+    base += tot;
+    __syncthreads();
+  }
+  if (b1 == a.n_items && b0 < b1 && threadIdx.x == 0) off[a.n_items] = base;
 }
 
 // One thread per queued POV (flat list over all rows, in row order, so
@@ -340,11 +372,18 @@ __global__ void __launch_bounds__(kWarps * 32) fixup_kernel(ScanArgs a, int tab_
 
 int launch_fixup(const ScanArgs& a, unsigned* off, void* stream) {
   if (a.n_items == 0) return 0;
-  fixup_prefix_kernel<<<1, 1024, 0, static_cast<cudaStream_t>(stream)>>>(a, off);
   int dev = 0;
   cudaGetDevice(&dev);
   int sms = 0;
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  {
+    // off[] has n_items + 1 slots plus room for the block sums after them
+    const int nb = std::max(1, std::min(sms, (a.n_items + kPrefixThreads - 1) / kPrefixThreads));
+    const int chunk = (a.n_items + nb - 1) / nb;
+    unsigned* bsum = off + a.n_items + 1;
+    fixup_prefix_sums_kernel<<<nb, kPrefixThreads, 0, static_cast<cudaStream_t>(stream)>>>(a, chunk, bsum);
+    fixup_prefix_write_kernel<<<nb, kPrefixThreads, 0, static_cast<cudaStream_t>(stream)>>>(a, chunk, bsum, off);
+  }
   const int tab_len = ((a.lmax + 31) / 32) * 32;
   const size_t smem = static_cast<size_t>(tab_len) * sizeof(float);
   if (smem > 200 * 1024) return static_cast<int>(cudaErrorInvalidValue);  // rows beyond 51200 cells
