@@ -1222,6 +1222,19 @@ void sweep_areas(sks_context* ctx, const float* dem, int dimy, int dimx, double 
              "H2D sweep table");
   cuda_check(cudaMemcpyAsync(d_len.p, tab.len.data(), tab.len.size() * sizeof(int), cudaMemcpyHostToDevice, st),
              "H2D sweep lengths");
+  // FP32 filter preconditions (elevation magnitudes)
+  ctx->check.ensure(2 * sizeof(unsigned long long), ctx->device);
+  cuda_check(cudaMemsetAsync(ctx->check.p, 0xff, sizeof(unsigned long long), st), "memset check");
+  cuda_check(cudaMemsetAsync(static_cast<char*>(ctx->check.p) + 8, 0, sizeof(unsigned long long), st),
+             "memset check");
+  cuda_check(launch_dem_check(ctx->dem.as<float>(), static_cast<long long>(n), ctx->check.as<unsigned long long>(),
+                              st),
+             "launch dem check");
+  unsigned long long chk[2] = {0, 0};
+  cuda_check(cudaMemcpyAsync(chk, ctx->check.p, sizeof(chk), cudaMemcpyDeviceToHost, st), "D2H check");
+  cuda_check(cudaStreamSynchronize(st), "sync check");
+  const bool filter = chk[1] == 0 && !(h0 != 0.0 && (std::fabs(h0) < std::ldexp(1.0, -40) ||
+                                                     std::fabs(h0) > std::ldexp(1.0, 40)));
   if (povs) {
     d_povs.ensure(static_cast<size_t>(npov) * sizeof(int2), ctx->device);
     cuda_check(cudaMemcpyAsync(d_povs.p, povs, static_cast<size_t>(npov) * sizeof(int2), cudaMemcpyHostToDevice, st),
@@ -1232,7 +1245,7 @@ void sweep_areas(sks_context* ctx, const float* dem, int dimy, int dimx, double 
     const int nb = static_cast<int>(std::min(batch, npov - b0));
     cuda_check(launch_sweep(ctx->dem.as<float>(), dimy, dimx, d_tab.as<SweepStepDev>(), d_len.as<int>(),
                             tab.stride, tab.ndir, povs ? d_povs.as<int2>() + b0 : nullptr, b0, nb, h0,
-                            d_buf.as<double>(), st),
+                            d_buf.as<double>(), filter && std::getenv("SKS_SWEEP_EXACT") == nullptr, st),
                "launch sweep");
     cuda_check(launch_sweep_sum(d_buf.as<double>(), tab.ndir, nb, pi_over_ns, cellsize, unit_factor,
                                 d_out.as<double>(), b0, st),

@@ -117,10 +117,12 @@ int launch_cv_to_vs(const int* cvf, const int* cvb, double* out,
 struct SweepStepDev {
   int di, dj;
   double dist;
+  float inv;
+  int pad;
 };
 int launch_sweep(const float* dem, int rows, int cols, const SweepStepDev* tab, const int* len,
                  int stride, int ndir, const int2* povs, long long pov0, int npov, double h0,
-                 double* buf, void* stream);
+                 double* buf, bool filter, void* stream);
 int launch_sweep_sum(const double* buf, int ndir, int npov, double pi_over_ns, double cellsize,
                      double unit_factor, double* out, long long out_off, void* stream);
 

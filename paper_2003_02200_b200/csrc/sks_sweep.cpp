@@ -48,7 +48,7 @@ SweepTable build_sweep_table(int ns, int dimy, int dimx, double max_cells) {
   SweepTable t;
   t.ndir = ns;
   t.stride = std::max(1, std::max(dimy, dimx) - 1);
-  t.steps.assign(static_cast<size_t>(t.ndir) * t.stride, SweepStep{0, 0, 0.0});
+  t.steps.assign(static_cast<size_t>(t.ndir) * t.stride, SweepStep{0, 0, 0.0, 0.0f, 0});
   t.len.assign(t.ndir, 0);
   for (int d = 0; d < t.ndir; ++d) {
     SweepStep* row = t.steps.data() + static_cast<size_t>(d) * t.stride;
@@ -57,7 +57,7 @@ SweepTable build_sweep_table(int ns, int dimy, int dimx, double max_cells) {
       // the grid bound is per observer (device); the distance cap is not
       const double dist = std::hypot(static_cast<double>(di), static_cast<double>(dj));
       if (dist > max_cells) return false;  // oracle.cpp:84
-      row[n++] = SweepStep{di, dj, dist};
+      row[n++] = SweepStep{di, dj, dist, static_cast<float>(1.0 / dist), 0};
       return true;
     });
     t.len[d] = n;
@@ -70,7 +70,8 @@ std::vector<SweepStep> axis_points(int dimy, int dimx, int i0, int j0, double az
   ray_offsets(dimy, dimx, azimuth_deg, [&](int di, int dj) {
     const int i = i0 + di, j = j0 + dj;
     if (i < 0 || i >= dimy || j < 0 || j >= dimx) return false;  // oracle.cpp:40,52
-    pts.push_back(SweepStep{i, j, std::hypot(static_cast<double>(di), static_cast<double>(dj))});
+    const double d = std::hypot(static_cast<double>(di), static_cast<double>(dj));
+    pts.push_back(SweepStep{i, j, d, static_cast<float>(1.0 / d), 0});
     return true;
   });
   return pts;

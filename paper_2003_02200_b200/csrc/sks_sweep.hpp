@@ -19,6 +19,8 @@ namespace sks {
 struct SweepStep {
   int di, dj;   // offset of the ray cell from the observer
   double dist;  // std::hypot(di, dj), oracle.cpp:43-44
+  float inv;    // fl32(1 / dist): the device's FP32 filter
+  int pad;
 };
 
 struct SweepTable {

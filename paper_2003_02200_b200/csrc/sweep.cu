@@ -13,8 +13,9 @@
 // reference's order (forward, backward, k ascending; oracle.cpp:122-126) and
 // applies (pi/ns)*cellsize^2 (oracle.cpp:128).
 //
-// Roofline: FP64-issue bound (one IEEE double divide per ray cell); DEM reads
-// hit L1/L2 (the rays of a warp share rows).
+// Roofline: issue bound — FP32 filter per ray cell, an IEEE double divide
+// only for the cells it cannot certify; DEM reads hit L1/L2 (the rays of a
+// warp share rows).
 #include <cuda_runtime.h>
 
 #include <cmath>
@@ -26,7 +27,17 @@ namespace sks {
 namespace {
 
 constexpr int kSweepThreads = 128;
+constexpr float kBand = 5.9604644775390625e-07f;  // 10 * 2^-24, as in the scan kernels
 
+// kFilter: an FP32 filter certifies the hidden targets —
+// t = fl(fl(fl(e - hf) - hl) * fl32(1/dist)) below lo = Mf - 10u|Mf|, with
+// Mf = fl32(M) of the exact running max M, cannot beat M (t is within ~4.5u
+// of the exact slope); every other target (records, the band) takes the
+// reference's FP64 divide and compare, so every decision is the reference's. Preconditions as in the scan: h splits
+// exactly into hf + hl and every elevation magnitude is 0 or in
+// [2^-40, 2^40] (checked on the device first; else the kernel runs without
+// the filter).
+template <bool kFilter>
 __global__ void __launch_bounds__(kSweepThreads)
 sweep_dirs_kernel(const float* __restrict__ dem, int rows, int cols, const SweepStepDev* __restrict__ tab,
                   const int* __restrict__ len, int stride, int ndir, const int2* __restrict__ povs,
@@ -45,10 +56,15 @@ sweep_dirs_kernel(const float* __restrict__ dem, int rows, int cols, const Sweep
   }
   // pov_h = dem(i0, j0) + h0 (oracle.cpp:116)
   const double h = static_cast<double>(dem[static_cast<long long>(i0) * cols + j0]) + h0;
+  const float hf = __double2float_rn(h);
+  const double hld = h - static_cast<double>(hf);
+  const float hl = __double2float_rn(hld);
+  const bool filt = kFilter && static_cast<double>(hl) == hld && fabsf(hf) < 1e30f;
   for (int d = blockIdx.y; d < ndir; d += gridDim.y) {
     const SweepStepDev* s = tab + static_cast<long long>(d) * stride;
     const int L = len[d];
     double cv = 0.0, max_theta = -INFINITY, open_d = 0.0, last_d = 0.0;
+    float lo = -INFINITY;  // fl32(M) - 10u|fl32(M)|
     bool visible = false;
     for (int n = 0; n < L; ++n) {
       const SweepStepDev st = s[n];
@@ -57,15 +73,32 @@ sweep_dirs_kernel(const float* __restrict__ dem, int rows, int cols, const Sweep
           static_cast<unsigned>(j) >= static_cast<unsigned>(cols)) {
         break;  // the ray left the grid (oracle.cpp:40,52)
       }
-      const double theta = (static_cast<double>(__ldg(dem + static_cast<long long>(i) * cols + j)) - h) / st.dist;
-      const bool above = theta > max_theta;
+      const float e = __ldg(dem + static_cast<long long>(i) * cols + j);
+      bool above;
+      if (filt) {
+        const float tf = __fmul_rn(__fadd_rn(__fadd_rn(e, -hf), -hl), st.inv);
+        if (tf < lo) {
+          above = false;  // certainly below the running max
+        } else {
+          const double theta = (static_cast<double>(e) - h) / st.dist;
+          above = theta > max_theta;
+          if (above) {
+            max_theta = theta;
+            const float mf = __double2float_rn(theta);
+            lo = __fmaf_rn(fabsf(mf), -kBand, mf);
+          }
+        }
+      } else {
+        const double theta = (static_cast<double>(e) - h) / st.dist;  // oracle.cpp:86
+        above = theta > max_theta;
+        if (above) max_theta = theta;
+      }
       if (above && !visible) {
         open_d = st.dist;
       } else if (!above && visible) {
         cv += st.dist * st.dist - open_d * open_d;
       }
       visible = above;
-      if (above) max_theta = theta;
       last_d = st.dist;
     }
     if (visible) {  // close at the last cell + 1 (oracle.cpp:101-105)
@@ -91,12 +124,17 @@ __global__ void sweep_sum_kernel(const double* __restrict__ buf, int ndir, int n
 }  // namespace
 
 int launch_sweep(const float* dem, int rows, int cols, const SweepStepDev* tab, const int* len, int stride,
-                 int ndir, const int2* povs, long long pov0, int npov, double h0, double* buf,
+                 int ndir, const int2* povs, long long pov0, int npov, double h0, double* buf, bool filter,
                  void* stream) {
   if (npov <= 0) return 0;
   const dim3 grid((npov + kSweepThreads - 1) / kSweepThreads, ndir < 65535 ? ndir : 65535);
-  sweep_dirs_kernel<<<grid, kSweepThreads, 0, static_cast<cudaStream_t>(stream)>>>(
-      dem, rows, cols, tab, len, stride, ndir, povs, pov0, npov, h0, buf);
+  if (filter) {
+    sweep_dirs_kernel<true><<<grid, kSweepThreads, 0, static_cast<cudaStream_t>(stream)>>>(
+        dem, rows, cols, tab, len, stride, ndir, povs, pov0, npov, h0, buf);
+  } else {
+    sweep_dirs_kernel<false><<<grid, kSweepThreads, 0, static_cast<cudaStream_t>(stream)>>>(
+        dem, rows, cols, tab, len, stride, ndir, povs, pov0, npov, h0, buf);
+  }
   return static_cast<int>(cudaGetLastError());
 }
 

@@ -217,3 +217,21 @@ def test_acceptance_criterion_1_engine_vs_sweep(n, seed):
     rel = np.sort((np.abs(eng - ref) / ref).ravel())
     p99 = rel[int(math.ceil(0.99 * rel.size)) - 1]
     assert rel.mean() <= 0.05 and p99 <= 0.15, (rel.mean(), p99)
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("scale", [1.0, 3.0e12, 2.0e-13])
+def test_sweep_filter_matches_exact_path(scale, monkeypatch):
+    """The FP32 filter of sweep_dirs_kernel only certifies hidden cells:
+    its results equal the pure-FP64 kernel's (SKS_SWEEP_EXACT) and the
+    restated oracle bit for bit, including elevations outside the filter's
+    proven range (the filter is then switched off)."""
+    v = sk.make_synthetic(sk.SyntheticKind.Fractal, 128, 120, 10.0, 11).values * np.float32(scale)
+    dem = sk.Dem(np.ascontiguousarray(v, np.float32), 10.0)
+    cfg = sk.RunConfig(ns=90, h0=1.5, units=sk.Units.SquareMeters)
+    fast = sw.total_viewshed_reference(dem, cfg, force=True).values
+    monkeypatch.setenv("SKS_SWEEP_EXACT", "1")
+    exact = sw.total_viewshed_reference(dem, cfg, force=True).values
+    assert np.array_equal(_bits(fast), _bits(exact))
+    want = Orc().rotational_rows(dem.values, 90, 1.5, None, 0, rows=(60, 62))
+    assert np.array_equal(_bits(fast[60:62]), _bits(want[60:62]))
