@@ -78,6 +78,25 @@ def test_relocation_2000_sampled_sectors(ora):
         assert np.array_equal(b32(g.values), b32(v)), k
 
 
+def test_config2_full_size_sectors_bitexact(ora):
+    """P2 + P3 at the benchmark's own size: whole sectors of config 2
+    (2000^2 fractal, ns = 180) — relocation, the scan of every POV in both
+    directions, the fixup and the unskew — against the reference's
+    sector_sweep, bit for bit. Four sectors (0, 22, 44 and 134 degrees: no
+    shear, sheared, near 45, transposed + flipped) run on host threads in
+    parallel (~30 s)."""
+    from concurrent.futures import ThreadPoolExecutor
+
+    dem = sk.make_synthetic(sk.SyntheticKind.Fractal, 2000, 2000, 10.0, 7)
+    cfg = sk.RunConfig(ns=180, h0=1.5, units=sk.Units.SquareMeters)
+    ks = [0, 11, 22, 67]
+    with ThreadPoolExecutor(len(ks)) as ex:
+        refs = list(ex.map(lambda k: ora.sector_sweep(dem.values, 10.0, 180, 1.5, None, k), ks))
+    for k, ref in zip(ks, refs):
+        ours = sk.sector_sweep(dem, cfg, k).contribution
+        assert np.array_equal(b64(ours), b64(ref)), k
+
+
 # ---- P2 scan -----------------------------------------------------------------
 
 def _ref_sdem(ora, dem, k, ns):
