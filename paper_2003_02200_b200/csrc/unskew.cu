@@ -90,18 +90,12 @@ constexpr int kUT = 32;           // tile edge (cells)
 // cp.async into the second buffer while sector s is computed.
 constexpr int kTR = kUT + 1;  // staged source rows (the tile's rows + the row above)
 
-__device__ __forceinline__ void cp_async4(void* smem_dst, const void* gmem_src) {
-  asm volatile("cp.async.ca.shared.global [%0], [%1], 4;\n" ::"r"(static_cast<unsigned>(__cvta_generic_to_shared(smem_dst))),
-               "l"(gmem_src));
-}
-
-__device__ __forceinline__ void cp_async8(void* smem_dst, const void* gmem_src) {
-  asm volatile("cp.async.ca.shared.global [%0], [%1], 8;\n" ::"r"(static_cast<unsigned>(__cvta_generic_to_shared(smem_dst))),
-               "l"(gmem_src));
-}
+#ifndef SKS_UNSKEW_MINB
+#define SKS_UNSKEW_MINB 5  // CTAs per SM (48 registers)
+#endif
 
 template <bool kBlocks>  // row-block sharding: some tiles own no row of a sector
-__global__ void __launch_bounds__(256) unskew_pipe_kernel(BatchDev b, double* __restrict__ map, int dimy,
+__global__ void __launch_bounds__(256, SKS_UNSKEW_MINB) unskew_pipe_kernel(BatchDev b, double* __restrict__ map, int dimy,
                                                               int dimx) {
   __shared__ int scv[2][kTR][kUT + 1];
   __shared__ int sown[2];  // sector staged in the buffer has owned rows in the tile
@@ -112,53 +106,60 @@ __global__ void __launch_bounds__(256) unskew_pipe_kernel(BatchDev b, double* __
   const int y0 = blockIdx.y * kUT, x0 = blockIdx.x * kUT;
   const int ye = min(dimy, y0 + kUT) - 1, xe = min(dimx, x0 + kUT) - 1;
   const int sj = x0 + tx;
+  const unsigned scv_u32 = static_cast<unsigned>(__cvta_generic_to_shared(&scv[0][0][0]));
+  const unsigned sdest_u32 = static_cast<unsigned>(__cvta_generic_to_shared(&sdest[0][0]));
+  const unsigned sfrac_u32 = static_cast<unsigned>(__cvta_generic_to_shared(&sfrac[0][0]));
   double acc[4];
 #pragma unroll
   for (int u = 0; u < 4; ++u) {
     const int si = y0 + ty + 8 * u;
     acc[u] = (si < dimy && sj < dimx) ? map[static_cast<long long>(si) * dimx + sj] : 0.0;
   }
-  // the tile's pre_ops box of sector s (axis permutations/flips: corners)
-  auto box = [&](int s, int* i_lo, int* j_lo) {
-    const int* iv = b.sectors[s].inv;
+  // the tile's pre_ops box of a sector (axis permutations/flips: corners)
+  auto box = [&](const int* iv, int* i_lo, int* j_lo) {
     const int ia = iv[0] * y0 + iv[1] * x0 + iv[2], ib = iv[0] * ye + iv[1] * xe + iv[2];
     const int ja = iv[3] * y0 + iv[4] * x0 + iv[5], jb = iv[3] * ye + iv[4] * xe + iv[5];
     *i_lo = min(ia, ib);
     *j_lo = min(ja, jb);
     return max(ja, jb) - *j_lo + 1;  // nj
   };
-  // false when none of the skewed rows the tile reads belongs to this run
-  // (row-block sharding; uniform across the CTA)
-  auto owned = [&](int s) {
-    if (!kBlocks) return true;
-    const SectorDev& sd = b.sectors[s];
-    if (sd.q_lo <= 0 && sd.q_hi >= sd.skw_rows) return true;
-    int i_lo, j_lo;
-    const int nj = box(s, &i_lo, &j_lo);
-    const int d_lo = __double2int_rz(__dmul_rn(sd.shear_tan, static_cast<double>(j_lo)));
-    const int d_hi = __double2int_rz(__dmul_rn(sd.shear_tan, static_cast<double>(j_lo + nj - 1)));
-    const int p_min = sd.base + i_lo - 1 - d_hi, p_max = sd.base + i_lo + kUT - 1 - d_lo;
-    return max(p_min, sd.q_lo) <= min(p_max, sd.q_hi - 1);
-  };
   auto stage = [&](int s, int bf) {
-    const SectorDev& sd = b.sectors[s];
-    const bool own = owned(s);
+    const SectorDev* sdp = b.sectors + s;
+    int iv[6];
+#pragma unroll
+    for (int k = 0; k < 6; ++k) iv[k] = __ldg(sdp->inv + k);
+    const int base = __ldg(&sdp->base), q_lo = __ldg(&sdp->q_lo), q_hi = __ldg(&sdp->q_hi);
+    const int skw_rows = __ldg(&sdp->skw_rows), pitch = __ldg(&sdp->pitch), col_off = __ldg(&sdp->col_off);
+    const long long sdem_off = __ldg(&sdp->sdem_off);
+    const double tan = __ldg(&sdp->shear_tan);
+    int i_lo, j_lo;
+    const int nj = box(iv, &i_lo, &j_lo);
+    bool own = true;
+    if (kBlocks && !(q_lo <= 0 && q_hi >= skw_rows)) {
+      // none of the skewed rows the tile reads may belong to this run
+      const int d_lo = __double2int_rz(__dmul_rn(tan, static_cast<double>(j_lo)));
+      const int d_hi = __double2int_rz(__dmul_rn(tan, static_cast<double>(j_lo + nj - 1)));
+      const int p_min = base + i_lo - 1 - d_hi, p_max = base + i_lo + kUT - 1 - d_lo;
+      own = max(p_min, q_lo) <= min(p_max, q_hi - 1);
+    }
     if (kBlocks && threadIdx.x == 0) sown[bf] = own ? 1 : 0;
     if (!own) return;
-    int i_lo, j_lo;
-    const int nj = box(s, &i_lo, &j_lo);
     if (threadIdx.x < nj) {
-      cp_async4(&sdest[bf][threadIdx.x], b.dest + sd.col_off + j_lo + threadIdx.x);
-      cp_async8(&sfrac[bf][threadIdx.x], b.fracd + sd.col_off + j_lo + threadIdx.x);
+      asm volatile("cp.async.ca.shared.global [%0], [%1], 4;\n" ::"r"(sdest_u32 + 4u * (bf * kUT + threadIdx.x)),
+                   "l"(b.dest + col_off + j_lo + threadIdx.x));
+      asm volatile("cp.async.ca.shared.global [%0], [%1], 8;\n" ::"r"(sfrac_u32 + 8u * (bf * kUT + threadIdx.x)),
+                   "l"(b.fracd + col_off + j_lo + threadIdx.x));
     }
     if (tx < nj) {
       const int j = j_lo + tx;
-      const int dj = __double2int_rz(__dmul_rn(sd.shear_tan, static_cast<double>(j)));
-      const int* col = b.cv + sd.sdem_off + j;
+      const int dj = __double2int_rz(__dmul_rn(tan, static_cast<double>(j)));
+      const int* col = b.cv + sdem_off + j;
+      const int p0 = base + i_lo - 1 - dj;  // skewed row of T row 0
       for (int ir = ty; ir < kTR; ir += 8) {
-        const int p = sd.base + (i_lo - 1 + ir) - dj;
-        if (p >= sd.q_lo && p < sd.q_hi && p >= 0 && p < sd.skw_rows) {
-          cp_async4(&scv[bf][ir][tx], col + static_cast<long long>(p) * sd.pitch);
+        const int p = p0 + ir;
+        const unsigned dst = scv_u32 + 4u * ((bf * kTR + ir) * (kUT + 1) + tx);
+        if (p >= q_lo && p < q_hi && p >= 0 && p < skw_rows) {
+          asm volatile("cp.async.ca.shared.global [%0], [%1], 4;\n" ::"r"(dst), "l"(col + static_cast<long long>(p) * pitch));
         } else {
           scv[bf][ir][tx] = 0;  // outside the sector or another run's row
         }
@@ -172,37 +173,45 @@ __global__ void __launch_bounds__(256) unskew_pipe_kernel(BatchDev b, double* __
     if (s + 1 < b.n_sectors) {
       stage(s + 1, bf ^ 1);
       asm volatile("cp.async.commit_group;\n" ::);
-      asm volatile("cp.async.wait_group 1;\n" ::);
+      asm volatile("cp.async.wait_group 1;\n" ::: "memory");
     } else {
-      asm volatile("cp.async.wait_group 0;\n" ::);
+      asm volatile("cp.async.wait_group 0;\n" ::: "memory");
     }
     __syncthreads();  // sector s's buffer complete for every thread
-    const SectorDev& sd = b.sectors[s];
     if (kBlocks && sown[bf] == 0) {
       __syncthreads();
       continue;
     }
+    const SectorDev* sdp = b.sectors + s;
+    int iv[6];
+#pragma unroll
+    for (int k = 0; k < 6; ++k) iv[k] = __ldg(sdp->inv + k);
+    const int rows = __ldg(&sdp->rows);
+    const double corr = __ldg(&sdp->correction);
     int i_lo, j_lo;
-    box(s, &i_lo, &j_lo);
-    const int* iv = sd.inv;
+    box(iv, &i_lo, &j_lo);
+    // cell u of this thread: si = y0 + ty + 8u, sj fixed; (i, j) step by 8 * (iv[0], iv[3])
+    const int i0 = iv[0] * (y0 + ty) + iv[1] * sj + iv[2];
+    const int j0 = iv[3] * (y0 + ty) + iv[4] * sj + iv[5];
 #pragma unroll
     for (int u = 0; u < 4; ++u) {
       const int si = y0 + ty + 8 * u;
       if (si >= dimy || sj >= dimx) continue;
-      const int i = iv[0] * si + iv[1] * sj + iv[2];
-      const int j = iv[3] * si + iv[4] * sj + iv[5];
+      const int i = i0 + 8 * u * iv[0];
+      const int j = j0 + 8 * u * iv[3];
       const int jl = j - j_lo;
       const int ir = i - i_lo + 1;  // T row of p; p - 1 is T row ir - 1
       const double r = sfrac[bf][jl];
       const double omr = __dsub_rn(1.0, r);
-      const double w_p = (i + 1 < sd.rows) ? __dadd_rn(omr, r) : omr;
+      const double w_p = (i + 1 < rows) ? __dadd_rn(omr, r) : omr;
       const double w_m = (i >= 1) ? __dadd_rn(omr, r) : r;
       const bool a = full_d(w_p);
       const bool c = full_d(w_m);
       double va = 0.0, vb = 0.0;
-      if (a) va = __dmul_rn(static_cast<double>(scv[bf][ir][jl]), sd.correction);
-      if (!a || c) vb = __dmul_rn(static_cast<double>(scv[bf][ir - 1][jl]), sd.correction);
+      if (a) va = __dmul_rn(static_cast<double>(scv[bf][ir][jl]), corr);
+      if (!a || c) vb = __dmul_rn(static_cast<double>(scv[bf][ir - 1][jl]), corr);
       if (!a && !c && b.dem != nullptr) {
+        const SectorDev& sd = b.sectors[s];
         const int p = sd.base + i - sdest[bf][jl];
         const int2 rg = (p >= 1 && p - 1 < sd.skw_rows) ? __ldg(b.ranges + sd.row_off + p - 1) : make_int2(0, 0);
         if (j < rg.x || j >= rg.y) vb = 0.0;
