@@ -406,6 +406,60 @@ __device__ __forceinline__ void eval16(Pov2& P, unsigned sb, unsigned ivb0, unsi
   }
 }
 
+// eval16 for the windows past kmain of a capped row: target k of POV y is a
+// no-op (fl(1/d) replaced by NaN: every comparison false) once
+// d = k - y exceeds the cap. kc0 = y0 + cap, the last target of the first POV.
+template <bool kHl, int kNC>
+__device__ __forceinline__ void eval16_capped(Pov2& P, unsigned sb, unsigned ivb0, unsigned ivb1, int k0, int kc0) {
+  const float qn = __int_as_float(0x7fc00000);
+#pragma unroll
+  for (int g = 0; g < kW / 4; ++g) {
+    const int k = k0 + 4 * g;
+    const float4 e = lds128(sb + 4 * k);
+    float4 q0, q1;
+    if (kNC == 4) {
+      q0 = lds128(ivb0 + 4 * k);
+      q1 = lds128(ivb1 + 4 * k);
+    } else {
+      const float2 a0 = lds64(ivb0 + 4 * k), b0 = lds64(ivb0 + 4 * k + 8);
+      const float2 a1 = lds64(ivb1 + 4 * k), b1 = lds64(ivb1 + 4 * k + 8);
+      q0 = make_float4(a0.x, a0.y, b0.x, b0.y);
+      q1 = make_float4(a1.x, a1.y, b1.x, b1.y);
+    }
+    const int m0 = kc0 - k, m1 = m0 + 1;  // last valid slot index per POV
+    q0.x = m0 >= 0 ? q0.x : qn;
+    q0.y = m0 >= 1 ? q0.y : qn;
+    q0.z = m0 >= 2 ? q0.z : qn;
+    q0.w = m0 >= 3 ? q0.w : qn;
+    q1.x = m1 >= 0 ? q1.x : qn;
+    q1.y = m1 >= 1 ? q1.y : qn;
+    q1.z = m1 >= 2 ? q1.z : qn;
+    q1.w = m1 >= 3 ? q1.w : qn;
+    float2 n0a = __fadd2_rn(make_float2(e.x, e.y), make_float2(-P.hf0, -P.hf0));
+    float2 n0b = __fadd2_rn(make_float2(e.z, e.w), make_float2(-P.hf0, -P.hf0));
+    float2 n1a = __fadd2_rn(make_float2(e.x, e.y), make_float2(-P.hf1, -P.hf1));
+    float2 n1b = __fadd2_rn(make_float2(e.z, e.w), make_float2(-P.hf1, -P.hf1));
+    if (kHl) {
+      n0a = __fadd2_rn(n0a, make_float2(-P.hl0, -P.hl0));
+      n0b = __fadd2_rn(n0b, make_float2(-P.hl0, -P.hl0));
+      n1a = __fadd2_rn(n1a, make_float2(-P.hl1, -P.hl1));
+      n1b = __fadd2_rn(n1b, make_float2(-P.hl1, -P.hl1));
+    }
+    const float2 t0a = __fmul2_rn(n0a, make_float2(q0.x, q0.y));
+    const float2 t0b = __fmul2_rn(n0b, make_float2(q0.z, q0.w));
+    const float2 t1a = __fmul2_rn(n1a, make_float2(q1.x, q1.y));
+    const float2 t1b = __fmul2_rn(n1b, make_float2(q1.z, q1.w));
+    const float t0[4] = {t0a.x, t0a.y, t0b.x, t0b.y};
+    const float t1[4] = {t1a.x, t1a.y, t1b.x, t1b.y};
+    const int kb = k + (1 << kSumShift);
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+      step(t0[i], P.hi0, P.lo0, P.A0[i], P.G0, kb);
+      step(t1[i], P.hi1, P.lo1, P.A1[i], P.G1, kb);
+    }
+  }
+}
+
 template <bool kHl, bool kVis, int kNC>
 __device__ void run_task(const ScanArgs& a, const Layout2& lay, const Slot& sl, const float* IV,
                          int dir, int chunk, int L, int cap, Pov2& P, int vis_p, uint8_t* vis,
@@ -467,8 +521,23 @@ __device__ void run_task(const ScanArgs& a, const Layout2& lay, const Slot& sl, 
     if (k0 < kc && k0 <= klast) break;  // next window crosses the cap: tail
   }
   flush(P);
-  if (capped) {
-    // masked tail: targets beyond some POVs' distance cap
+  if (capped && !kVis) {
+    // masked tail: targets beyond some POVs' distance cap, packed like the
+    // main loop (no skip tests: every window here reaches some POV's cap)
+    const int ylast = min(L - 1, ymin + kTaskPovs - 1);
+    const int kt_end = min(klast, ylast + cap);
+    const int kc0 = P.y0 + cap;
+    int cnt = 0;
+    for (; k0 <= kt_end; k0 += kW) {
+      eval16_capped<kHl, kNC>(P, sb, ivb0, ivb1, k0, kc0);
+      if (++cnt == 32) {
+        flush(P);
+        cnt = 0;
+      }
+    }
+    flush(P);
+  } else if (capped) {
+    // masked tail, one target at a time (debug visibility capture)
     const int ylast = min(L - 1, ymin + kTaskPovs - 1);
     const int kt_end = min(klast, ylast + cap);
     const float* IVf = IV + lay.copy(0) + kOff;
