@@ -327,7 +327,10 @@ __global__ void __launch_bounds__(kPrefixThreads) fixup_prefix_write_kernel(Scan
 // neighbouring threads share rows): the POV's row is found by a binary search
 // of the prefix, then the POV is re-run exactly (exact_pov). Rows are read
 // through L1/L2; the fl(1/d) table sits in shared memory.
-__global__ void __launch_bounds__(kWarps * 32) fixup_kernel(ScanArgs a, int tab_len, const unsigned* off) {
+#ifndef SKS_FIX_MINB
+#define SKS_FIX_MINB 3  // 24 warps per SM (80 registers): the kernel is latency-bound
+#endif
+__global__ void __launch_bounds__(kWarps * 32, SKS_FIX_MINB) fixup_kernel(ScanArgs a, int tab_len, const unsigned* off) {
   extern __shared__ __align__(16) float ivt[];  // fl(1/d), d = 0 .. tab_len - 1
   for (int d = threadIdx.x; d < tab_len; d += blockDim.x) ivt[d] = __frcp_rn(static_cast<float>(d));
   __syncthreads();
