@@ -65,7 +65,10 @@ constexpr int kW = SKS_FINE_W;  // fine window (targets): 8 or 16
 constexpr int kH = SKS_COARSE_W;  // coarse window (targets)
 static_assert(kTaskPovs % kH == 0, "task starts must be aligned to coarse windows");
 constexpr int kOff = 128;  // table index offset (dd >= -kOff + 1 addressable)
-constexpr int kThreads = 768;  // 24 warps: 80 registers, no spills (1024 spills at 64)
+#ifndef SKS_SCAN_THREADS
+#define SKS_SCAN_THREADS 768
+#endif
+constexpr int kThreads = SKS_SCAN_THREADS;  // 24 warps: 80 registers, no spills (1024 spills at 64)
 constexpr int kMaxSlots = 8;
 constexpr int kCtlInts = 16;  // per slot control block
 constexpr float kBand = 5.9604644775390625e-07f;  // 10 * 2^-24

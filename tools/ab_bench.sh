@@ -4,8 +4,8 @@ mkdir -p gpurun_out/ab
 i=0
 for v in "$@"; do
   for rep in 1 2; do
-    env $v timeout 300 python bench.py --no-cpu-baseline > gpurun_out/ab/b_$i_$rep.json 2>/dev/null
-    python - "$v" gpurun_out/ab/b_$i_$rep.json <<'PY'
+    env $v timeout 300 python bench.py --no-cpu-baseline > gpurun_out/ab/b_${i}_${rep}.json 2>/dev/null
+    python - "$v" gpurun_out/ab/b_${i}_${rep}.json <<'PY'
 import json, sys
 d = json.loads(open(sys.argv[2]).read().strip().splitlines()[-1])
 print(sys.argv[1], round(d["ms_per_step"], 2), {k: round(v, 2) for k, v in d["phase_ms_per_step"].items()},
