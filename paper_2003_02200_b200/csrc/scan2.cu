@@ -526,12 +526,19 @@ __device__ void run_task(const ScanArgs& a, const Layout2& lay, const Slot& sl, 
   flush(P);
   if (capped && !kVis) {
     // masked tail: targets beyond some POVs' distance cap, packed like the
-    // main loop (no skip tests: every window here reaches some POV's cap)
+    // main loop, with the same hidden-window skip
     const int ylast = min(L - 1, ymin + kTaskPovs - 1);
     const int kt_end = min(klast, ylast + cap);
     const int kc0 = P.y0 + cap;
     int cnt = 0;
     for (; k0 <= kt_end; k0 += kW) {
+      if (k0 >= ktest) {  // the bound over the whole window also covers the masked targets
+        const float2 em = lds64(w16a + 8u * (static_cast<unsigned>(k0) / kW));
+        if (window_hidden<kHl>(P, em, tb, k0, kW)) {
+          nskip += kW;
+          continue;
+        }
+      }
       eval16_capped<kHl, kNC>(P, sb, ivb0, ivb1, k0, kc0);
       if (++cnt == 32) {
         flush(P);
