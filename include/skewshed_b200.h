@@ -293,6 +293,14 @@ sks_status sks_total_viewshed_reference(const float* dem, int dimy, int dimx, do
                                         const float* nodata, const sks_run_config* cfg, int force,
                                         double* out);
 
+/* linear_scan(dem, i0, j0, pov_h, azimuth, max_dist_cells, rings_out)
+   (oracle.cpp:74-106) on the GPU: *cv, and the first min(cap, *nrings) ring
+   sectors (r_open, r_close pairs, cell units) into rings (may be null).
+   max_dist_cells: INFINITY for none. */
+sks_status sks_linear_scan(const float* dem, int dimy, int dimx, int i0, int j0, double pov_h,
+                           double azimuth_deg, double max_dist_cells, int device, double* cv,
+                           double* rings, int cap, int* nrings);
+
 /* select_axis_point_set (oracle.cpp:62-71): *count cells of the ray, the
    first min(cap, *count) written to ij as (i, j) pairs. Host only. */
 sks_status sks_axis_point_set(int dimy, int dimx, int i0, int j0, double azimuth_deg, int* ij, int cap,

@@ -459,6 +459,21 @@ int ref_total_viewshed_reference(const float* dem, int dimy, int dimx, double ce
   });
 }
 
+// oracle.cpp:74-106 linear_scan with the ring sectors
+int ref_linear_scan(const float* dem, int dimy, int dimx, int i0, int j0, double pov_h, double az, double max_cells,
+                    double* cv, double* rings, int cap, int* nrings) {
+  return guarded([&] {
+    Dem d = make_dem(dem, dimy, dimx, 1.0);
+    oracle::RingSectorSet rs;
+    *cv = oracle::linear_scan(d, i0, j0, pov_h, az, max_cells, &rs);
+    *nrings = static_cast<int>(rs.size());
+    for (int t = 0; t < std::min(cap, *nrings); ++t) {
+      rings[2 * t] = rs[t].r_open;
+      rings[2 * t + 1] = rs[t].r_close;
+    }
+  });
+}
+
 // oracle.cpp:62-71 select_axis_point_set
 int ref_axis_point_set(int dimy, int dimx, int i0, int j0, double azimuth_deg, int* ij, int cap, int* count) {
   return guarded([&] {

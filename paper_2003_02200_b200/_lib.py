@@ -124,6 +124,8 @@ SIGNATURES = {
                                      C.c_double, C.c_int, _vp, _vp, _vp]),
     "sks_total_viewshed_reference": (C.c_int, [_vp, C.c_int, C.c_int, C.c_double, _vp, C.POINTER(RunConfigC),
                                                C.c_int, _vp]),
+    "sks_linear_scan": (C.c_int, [_vp, C.c_int, C.c_int, C.c_int, C.c_int, C.c_double, C.c_double, C.c_double,
+                                  C.c_int, _vp, _vp, C.c_int, _vp]),
     "sks_axis_point_set": (C.c_int, [C.c_int, C.c_int, C.c_int, C.c_int, C.c_double, _vp, C.c_int, _vp]),
     "sks_random_povs": (C.c_int, [C.c_int, C.c_int, C.c_int, C.c_uint32, _vp]),
     "sks_write_heatmap": (C.c_int, [C.c_char_p, _vp, C.c_int, C.c_int, C.c_int]),

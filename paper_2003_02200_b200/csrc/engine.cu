@@ -1329,6 +1329,45 @@ sks_status sks_total_viewshed_reference(const float* dem, int dimy, int dimx, do
   });
 }
 
+sks_status sks_linear_scan(const float* dem, int dimy, int dimx, int i0, int j0, double pov_h, double azimuth_deg,
+                           double max_dist_cells, int device, double* cv, double* rings, int cap, int* nrings) {
+  return guarded([&] {
+    if (!dem || !cv) throw std::invalid_argument("null argument");
+    require_inside(dimy, dimx, i0, j0);
+    const std::vector<SweepStep> tab = ray_table(dimy, dimx, azimuth_deg, max_dist_cells);
+    sks_context* ctx = default_context(device);
+    ctx->activate();
+    std::lock_guard<std::mutex> lk(ctx->mu);
+    cudaStream_t st = ctx->own_stream;
+    const size_t n = static_cast<size_t>(dimy) * dimx;
+    const int rcap = std::max(cap, 0);
+    DevBuf d_tab, d_out;
+    ctx->dem.ensure(n * sizeof(float), ctx->device);
+    d_tab.ensure(std::max<size_t>(tab.size(), 1) * sizeof(SweepStep), ctx->device);
+    d_out.ensure((1 + 2 * static_cast<size_t>(rcap)) * sizeof(double) + sizeof(int), ctx->device);
+    cuda_check(cudaMemcpyAsync(ctx->dem.p, dem, n * sizeof(float), cudaMemcpyHostToDevice, st), "H2D dem");
+    if (!tab.empty()) {
+      cuda_check(cudaMemcpyAsync(d_tab.p, tab.data(), tab.size() * sizeof(SweepStep), cudaMemcpyHostToDevice, st),
+                 "H2D ray");
+    }
+    double* dcv = d_out.as<double>();
+    double* drings = dcv + 1;
+    int* dn = reinterpret_cast<int*>(drings + 2 * rcap);
+    cuda_check(launch_linear_scan(ctx->dem.as<float>(), dimy, dimx, i0, j0, pov_h, d_tab.as<SweepStepDev>(),
+                                  static_cast<int>(tab.size()), dcv, drings, rcap, dn, st),
+               "launch linear scan");
+    ++ctx->launches;
+    std::vector<double> host(1 + 2 * static_cast<size_t>(rcap));
+    int nr = 0;
+    cuda_check(cudaMemcpyAsync(host.data(), dcv, host.size() * sizeof(double), cudaMemcpyDeviceToHost, st), "D2H");
+    cuda_check(cudaMemcpyAsync(&nr, dn, sizeof(int), cudaMemcpyDeviceToHost, st), "D2H");
+    cuda_check(cudaStreamSynchronize(st), "sync");
+    *cv = host[0];
+    if (nrings) *nrings = nr;
+    if (rings) std::copy(host.begin() + 1, host.begin() + 1 + 2 * std::min(nr, rcap), rings);
+  });
+}
+
 sks_status sks_axis_point_set(int dimy, int dimx, int i0, int j0, double azimuth_deg, int* ij, int cap,
                               int* count) {
   return guarded([&] {

@@ -123,6 +123,9 @@ struct SweepStepDev {
 int launch_sweep(const float* dem, int rows, int cols, const SweepStepDev* tab, const int* len,
                  int stride, int ndir, const int2* povs, long long pov0, int npov, double h0,
                  double* buf, bool filter, void* stream);
+int launch_linear_scan(const float* dem, int rows, int cols, int i0, int j0, double pov_h,
+                       const SweepStepDev* tab, int len, double* out_cv, double* rings, int cap,
+                       int* nrings, void* stream);
 int launch_sweep_sum(const double* buf, int ndir, int npov, double pi_over_ns, double cellsize,
                      double unit_factor, double* out, long long out_off, void* stream);
 

@@ -65,6 +65,17 @@ SweepTable build_sweep_table(int ns, int dimy, int dimx, double max_cells) {
   return t;
 }
 
+std::vector<SweepStep> ray_table(int dimy, int dimx, double azimuth_deg, double max_cells) {
+  std::vector<SweepStep> steps;
+  ray_offsets(dimy, dimx, azimuth_deg, [&](int di, int dj) {
+    const double dist = std::hypot(static_cast<double>(di), static_cast<double>(dj));
+    if (dist > max_cells) return false;  // oracle.cpp:84
+    steps.push_back(SweepStep{di, dj, dist, static_cast<float>(1.0 / dist), 0});
+    return true;
+  });
+  return steps;
+}
+
 std::vector<SweepStep> axis_points(int dimy, int dimx, int i0, int j0, double azimuth_deg) {
   std::vector<SweepStep> pts;
   ray_offsets(dimy, dimx, azimuth_deg, [&](int di, int dj) {

@@ -33,6 +33,9 @@ struct SweepTable {
 // max_cells = max_distance / cellsize, +inf when uncapped (oracle.cpp:117-119).
 SweepTable build_sweep_table(int ns, int dimy, int dimx, double max_cells);
 
+// The ray of one azimuth (any observer), steps with dist > max_cells cut.
+std::vector<SweepStep> ray_table(int dimy, int dimx, double azimuth_deg, double max_cells);
+
 // select_axis_point_set (oracle.cpp:62-71) for one observer and azimuth.
 std::vector<SweepStep> axis_points(int dimy, int dimx, int i0, int j0, double azimuth_deg);
 

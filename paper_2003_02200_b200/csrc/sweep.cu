@@ -121,6 +121,51 @@ __global__ void sweep_sum_kernel(const double* __restrict__ buf, int ndir, int n
   out[out_stride_off + t] = area;
 }
 
+// linear_scan (oracle.cpp:74-106) of one ray with its ring sectors: the
+// reference's FP64 recurrence verbatim, one thread (a debug / API entry).
+__global__ void linear_scan_kernel(const float* __restrict__ dem, int rows, int cols, int i0, int j0, double pov_h,
+                                   const SweepStepDev* __restrict__ tab, int len, double* out_cv,
+                                   double* rings, int cap, int* nrings) {
+  if (threadIdx.x != 0 || blockIdx.x != 0) return;
+  double cv = 0.0, max_theta = -INFINITY, open_d = 0.0, last_d = 0.0;
+  bool visible = false;
+  int nr = 0;
+  for (int n = 0; n < len; ++n) {
+    const SweepStepDev st = tab[n];
+    const int i = i0 + st.di, j = j0 + st.dj;
+    if (static_cast<unsigned>(i) >= static_cast<unsigned>(rows) ||
+        static_cast<unsigned>(j) >= static_cast<unsigned>(cols)) {
+      break;
+    }
+    const double theta = (static_cast<double>(dem[static_cast<long long>(i) * cols + j]) - pov_h) / st.dist;
+    const bool above = theta > max_theta;
+    if (above && !visible) {
+      open_d = st.dist;
+    } else if (!above && visible) {
+      cv += st.dist * st.dist - open_d * open_d;
+      if (nr < cap) {
+        rings[2 * nr] = open_d;
+        rings[2 * nr + 1] = st.dist;
+      }
+      ++nr;
+    }
+    visible = above;
+    if (above) max_theta = theta;
+    last_d = st.dist;
+  }
+  if (visible) {
+    const double close_d = last_d + 1.0;
+    cv += close_d * close_d - open_d * open_d;
+    if (nr < cap) {
+      rings[2 * nr] = open_d;
+      rings[2 * nr + 1] = close_d;
+    }
+    ++nr;
+  }
+  *out_cv = cv;
+  *nrings = nr;
+}
+
 }  // namespace
 
 int launch_sweep(const float* dem, int rows, int cols, const SweepStepDev* tab, const int* len, int stride,
@@ -135,6 +180,13 @@ int launch_sweep(const float* dem, int rows, int cols, const SweepStepDev* tab, 
     sweep_dirs_kernel<false><<<grid, kSweepThreads, 0, static_cast<cudaStream_t>(stream)>>>(
         dem, rows, cols, tab, len, stride, ndir, povs, pov0, npov, h0, buf);
   }
+  return static_cast<int>(cudaGetLastError());
+}
+
+int launch_linear_scan(const float* dem, int rows, int cols, int i0, int j0, double pov_h, const SweepStepDev* tab,
+                       int len, double* out_cv, double* rings, int cap, int* nrings, void* stream) {
+  linear_scan_kernel<<<1, 32, 0, static_cast<cudaStream_t>(stream)>>>(dem, rows, cols, i0, j0, pov_h, tab, len, out_cv,
+                                                                      rings, cap, nrings);
   return static_cast<int>(cudaGetLastError());
 }
 

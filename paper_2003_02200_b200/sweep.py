@@ -29,6 +29,13 @@ class GridPoint:
     j: int = 0
 
 
+@dataclass(frozen=True)
+class RingSector:
+    """oracle.hpp:24-27: visible interval [r_open, r_close) in cell units."""
+    r_open: float = 0.0
+    r_close: float = 0.0
+
+
 @dataclass
 class MultiViewshed:
     """oracle.hpp:53-56: grid nonzero only at the observer cells (m^2)."""
@@ -48,6 +55,24 @@ def select_axis_point_set(dem: Dem, i0: int, j0: int, azimuth_deg: float) -> lis
     check(lib.sks_axis_point_set(dem.dimy(), dem.dimx(), i0, j0, float(azimuth_deg), ij.ctypes.data, cnt.value,
                                  C.byref(cnt)))
     return [GridPoint(int(ij[2 * t]), int(ij[2 * t + 1])) for t in range(cnt.value)]
+
+
+def linear_scan(dem: Dem, i0: int, j0: int, pov_h: float, azimuth_deg: float,
+                max_dist_cells: float = float("inf"), rings_out: Optional[list] = None, device: int = 0) -> float:
+    """oracle.cpp:74-106: ring sum of one ray (sum of r_close^2 - r_open^2);
+    appends the ring sectors to rings_out when given."""
+    cv = C.c_double()
+    nr = C.c_int()
+    check(lib.sks_linear_scan(dem.values.ctypes.data, dem.dimy(), dem.dimx(), int(i0), int(j0), float(pov_h),
+                              float(azimuth_deg), float(max_dist_cells), int(device), C.byref(cv), None, 0,
+                              C.byref(nr)))
+    if rings_out is not None and nr.value > 0:
+        buf = np.empty(2 * nr.value, np.float64)
+        check(lib.sks_linear_scan(dem.values.ctypes.data, dem.dimy(), dem.dimx(), int(i0), int(j0), float(pov_h),
+                                  float(azimuth_deg), float(max_dist_cells), int(device), C.byref(cv),
+                                  buf.ctypes.data, nr.value, C.byref(nr)))
+        rings_out.extend(RingSector(float(buf[2 * t]), float(buf[2 * t + 1])) for t in range(nr.value))
+    return cv.value
 
 
 def singular_viewshed(dem: Dem, i0: int, j0: int, h0: float, ns: int, max_distance: Optional[float] = None,

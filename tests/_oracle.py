@@ -109,6 +109,8 @@ class Ref:
         lib.ref_axis_point_set.argtypes = [C.c_int, C.c_int, C.c_int, C.c_int, C.c_double, C.c_void_p, C.c_int,
                                            C.POINTER(C.c_int)]
         lib.ref_write_heatmap.argtypes = [C.c_char_p, C.c_void_p, C.c_int, C.c_int, C.c_int]
+        lib.ref_linear_scan.argtypes = [_f32p, C.c_int, C.c_int, C.c_int, C.c_int, C.c_double, C.c_double, C.c_double,
+                                        C.POINTER(C.c_double), C.c_void_p, C.c_int, C.POINTER(C.c_int)]
 
     # ---- rotational sweep (oracle.cpp) / heatmap (heatmap.cpp) ----
     def singular_viewshed(self, dem, i, j, h0, ns, max_distance=None, cellsize=10.0):
@@ -143,6 +145,14 @@ class Ref:
         self._check(self.lib.ref_axis_point_set(dimy, dimx, i0, j0, az, ij.ctypes.data, dimy + dimx + 1,
                                                 C.byref(cnt)))
         return [(int(ij[2 * t]), int(ij[2 * t + 1])) for t in range(cnt.value)]
+
+    def linear_scan(self, dem, i0, j0, pov_h, az, max_cells=float("inf")):
+        d = np.ascontiguousarray(dem, np.float32)
+        cv, nr = C.c_double(), C.c_int()
+        buf = np.empty(2 * (d.shape[0] + d.shape[1] + 2), np.float64)
+        self._check(self.lib.ref_linear_scan(d, d.shape[0], d.shape[1], i0, j0, pov_h, az, max_cells, C.byref(cv),
+                                             buf.ctypes.data, buf.size // 2, C.byref(nr)))
+        return cv.value, [(float(buf[2 * t]), float(buf[2 * t + 1])) for t in range(nr.value)]
 
     def write_heatmap(self, path, values, palette):
         v = np.ascontiguousarray(values, np.float64)

@@ -235,3 +235,41 @@ def test_sweep_filter_matches_exact_path(scale, monkeypatch):
     assert np.array_equal(_bits(fast), _bits(exact))
     want = Orc().rotational_rows(dem.values, 90, 1.5, None, 0, rows=(60, 62))
     assert np.array_equal(_bits(fast[60:62]), _bits(want[60:62]))
+
+
+@pytest.mark.gpu
+def test_linear_scan_rings_bit_exact_and_well_formed():
+    """linear_scan with ring sectors (oracle.cpp:74-106) on the GPU: the
+    reference's ring list and ring sum bit for bit (when oracle/_ref is
+    built), and test_oracle.cpp:187-209's properties: 0 < r_open < r_close,
+    rings ordered, sum of r_close^2 - r_open^2 = cv."""
+    dem = _dem(sk.SyntheticKind.SmoothedNoise, 24, 24, seed=17)
+    rng = random.Random(5)
+    ref = Ref() if have_ref() else None
+    for _ in range(60):
+        i, j = rng.randrange(24), rng.randrange(24)
+        az = rng.randrange(3600) / 10.0
+        cap = rng.choice([float("inf"), 7.5])
+        h = float(dem.values[i, j]) + 1.5
+        rings = []
+        cv = sw.linear_scan(dem, i, j, h, az, cap, rings)
+        prev, measured = 0.0, 0.0
+        for r in rings:
+            assert 0.0 < r.r_open < r.r_close and r.r_open >= prev
+            prev = r.r_close
+            measured += r.r_close * r.r_close - r.r_open * r.r_open
+        assert cv == pytest.approx(measured, rel=1e-12)
+        if ref is not None:
+            rcv, rrings = ref.linear_scan(dem.values, i, j, h, az, cap)
+            assert cv == rcv and [(r.r_open, r.r_close) for r in rings] == rrings
+
+
+@pytest.mark.gpu
+def test_singular_viewshed_shift_invariance():
+    """test_oracle.cpp:175-185: adding 64 m to every elevation changes no
+    singular viewshed (the GPU sweep reproduces the reference's arithmetic,
+    so the reference's invariant carries over exactly)."""
+    dem = _dem(sk.SyntheticKind.SmoothedNoise, 16, 16, seed=3)
+    shifted = sk.Dem(dem.values + np.float32(64.0), dem.cellsize)
+    for i, j in ((0, 0), (5, 7), (11, 3)):
+        assert sw.singular_viewshed(dem, i, j, 1.5, 36) == sw.singular_viewshed(shifted, i, j, 1.5, 36)
