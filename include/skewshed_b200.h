@@ -309,6 +309,11 @@ sks_status sks_axis_point_set(int dimy, int dimx, int i0, int j0, double azimuth
 /* random_povs(dem, count, seed) (cli.cpp:207-221): count (i, j) pairs. */
 sks_status sks_random_povs(int dimy, int dimx, int count, uint32_t seed, int* ij);
 
+/* fill_nodata_nearest(dem) (dem.cpp:175-213): out = dem with every nodata
+   cell replaced by the value the reference's breadth-first search reaches it
+   from (host). SKS_INTERNAL for a grid that is entirely nodata. */
+sks_status sks_fill_nodata_nearest(const float* dem, int dimy, int dimx, float nodata, float* out);
+
 /* write_heatmap(grid, path, palette) (heatmap.cpp:11-56): binary PGM / PPM of
    the min-max normalised map. Host code. */
 enum { SKS_PALETTE_GRAY = 0, SKS_PALETTE_BLUE_RED = 1 };

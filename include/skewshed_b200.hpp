@@ -324,6 +324,16 @@ inline Dem read_ascii_grid(std::istream& in, std::string_view source_name) {
   return detail::take_ascii_grid(g);
 }
 
+// dem.hpp:71 / dem.cpp:175-213 (the CLI's `fill`)
+inline Dem fill_nodata_nearest(const Dem& dem) {
+  Dem out = dem;
+  if (!dem.nodata) return out;
+  check(sks_fill_nodata_nearest(dem.values.data().data(), dem.dimy(), dem.dimx(), *dem.nodata,
+                                out.values.data().data()));
+  out.nodata.reset();
+  return out;
+}
+
 // Binary side format (ESRI .hdr + .flt float32), the fast load of large DEMs.
 inline Dem read_float_grid(const std::filesystem::path& path) {
   sks_ascii_grid* g = nullptr;

@@ -474,6 +474,16 @@ int ref_linear_scan(const float* dem, int dimy, int dimx, int i0, int j0, double
   });
 }
 
+// dem.cpp:175-213 fill_nodata_nearest
+int ref_fill_nodata_nearest(const float* v, int dimy, int dimx, float nodata, float* out) {
+  return guarded([&] {
+    Dem d = make_dem(v, dimy, dimx, 1.0);
+    d.nodata = nodata;
+    Dem f = fill_nodata_nearest(d);
+    std::memcpy(out, f.values.data().data(), sizeof(float) * f.values.size());
+  });
+}
+
 // oracle.cpp:62-71 select_axis_point_set
 int ref_axis_point_set(int dimy, int dimx, int i0, int j0, double azimuth_deg, int* ij, int cap, int* count) {
   return guarded([&] {

@@ -128,6 +128,7 @@ SIGNATURES = {
                                   C.c_int, _vp, _vp, C.c_int, _vp]),
     "sks_axis_point_set": (C.c_int, [C.c_int, C.c_int, C.c_int, C.c_int, C.c_double, _vp, C.c_int, _vp]),
     "sks_random_povs": (C.c_int, [C.c_int, C.c_int, C.c_int, C.c_uint32, _vp]),
+    "sks_fill_nodata_nearest": (C.c_int, [_vp, C.c_int, C.c_int, C.c_float, _vp]),
     "sks_write_heatmap": (C.c_int, [C.c_char_p, _vp, C.c_int, C.c_int, C.c_int]),
     "sks_context_scale": (C.c_int, [_vp, _vp, C.c_longlong, C.c_int, C.c_double, C.c_int, _vp]),
     "sks_context_total_viewshed": (C.c_int, [_vp, _vp, C.c_int, C.c_int, C.c_double,

@@ -1389,6 +1389,14 @@ sks_status sks_random_povs(int dimy, int dimx, int count, uint32_t seed, int* ij
   });
 }
 
+sks_status sks_fill_nodata_nearest(const float* dem, int dimy, int dimx, float nodata, float* out) {
+  return guarded([&] {
+    if ((!dem || !out) && static_cast<long long>(dimy) * dimx > 0) throw std::invalid_argument("null argument");
+    if (dimy < 0 || dimx < 0) throw std::invalid_argument("grid dimensions must be non-negative");
+    fill_nodata_nearest(dem, dimy, dimx, nodata, out);
+  });
+}
+
 sks_status sks_write_heatmap(const char* path, const double* values, int rows, int cols, int palette) {
   return guarded([&] {
     if (!path || (!values && static_cast<long long>(rows) * cols > 0)) throw std::invalid_argument("null argument");

@@ -495,6 +495,38 @@ void write_float_grid(const std::string& path, const float* values, int nrows, i
   if (std::fclose(f) != 0 || !ok) throw std::runtime_error("failed while writing '" + fp + "'");
 }
 
+void fill_nodata_nearest(const float* in, int rows, int cols, float nodata, float* out) {
+  const size_t n = static_cast<size_t>(std::max(rows, 0)) * static_cast<size_t>(std::max(cols, 0));
+  std::copy(in, in + n, out);
+  // a ring buffer of cell indices is the reference's deque: every cell is
+  // pushed exactly once, seeds first in row-major order
+  std::vector<int> queue;
+  queue.reserve(n);
+  std::vector<unsigned char> filled(n, 0);
+  for (size_t c = 0; c < n; ++c) {
+    if (!(in[c] == nodata)) {  // Dem::is_nodata (dem.hpp:35)
+      filled[c] = 1;
+      queue.push_back(static_cast<int>(c));
+    }
+  }
+  if (queue.empty()) throw std::runtime_error("cannot fill a grid that is entirely nodata");
+  static constexpr int kDi[4] = {-1, 1, 0, 0};
+  static constexpr int kDj[4] = {0, 0, -1, 1};
+  for (size_t head = 0; head < queue.size(); ++head) {
+    const int c = queue[head];
+    const int i = c / cols, j = c % cols;
+    for (int k = 0; k < 4; ++k) {
+      const int ii = i + kDi[k], jj = j + kDj[k];
+      if (ii < 0 || ii >= rows || jj < 0 || jj >= cols) continue;
+      const int cc = ii * cols + jj;
+      if (filled[cc]) continue;
+      out[cc] = out[c];
+      filled[cc] = 1;
+      queue.push_back(cc);
+    }
+  }
+}
+
 void write_heatmap(const std::string& path, const double* values, int rows, int cols, int palette) {
   const size_t n = static_cast<size_t>(std::max(rows, 0)) * static_cast<size_t>(std::max(cols, 0));
   if (n == 0) throw std::invalid_argument("cannot render an empty grid");

@@ -43,6 +43,12 @@ AsciiGrid read_float_grid(const std::string& path);
 void write_float_grid(const std::string& path, const float* values, int nrows, int ncols, double xll,
                       double yll, double cellsize, const float* nodata);
 
+// fill_nodata_nearest (dem.cpp:175-213): every nodata cell takes the value
+// of the cell the multi-source breadth-first search (seeds in row-major
+// order, neighbours up/down/left/right) reaches it from. Throws
+// std::runtime_error for a grid that is entirely nodata.
+void fill_nodata_nearest(const float* in, int rows, int cols, float nodata, float* out);
+
 // write_heatmap (heatmap.cpp:11-56): min-max normalised 8-bit raster, binary
 // PGM (palette 0, Gray) or PPM (palette 1, BlueRed).
 void write_heatmap(const std::string& path, const double* values, int rows, int cols, int palette);

@@ -524,3 +524,14 @@ def write_heatmap(grid: VsGrid, path, palette: Palette = Palette.Gray) -> None:
     vals = np.ascontiguousarray(grid.values if isinstance(grid, VsGrid) else grid, np.float64)
     rows, cols = (vals.shape + (0, 0))[:2] if vals.ndim == 2 else (0, 0)
     check(lib.sks_write_heatmap(str(path).encode(), vals.ctypes.data, rows, cols, int(palette)))
+
+
+def fill_nodata_nearest(dem: Dem) -> Dem:
+    """fill_nodata_nearest (dem.cpp:175-213): nodata cells take the value the
+    reference's breadth-first search reaches them from; nodata is cleared."""
+    if dem.nodata is None:
+        return Dem(dem.values.copy(), dem.cellsize, None, dem.origin)
+    out = np.empty_like(dem.values)
+    check(lib.sks_fill_nodata_nearest(dem.values.ctypes.data, dem.dimy(), dem.dimx(), float(dem.nodata),
+                                      out.ctypes.data))
+    return Dem(out, dem.cellsize, None, dem.origin)

@@ -109,6 +109,7 @@ class Ref:
         lib.ref_axis_point_set.argtypes = [C.c_int, C.c_int, C.c_int, C.c_int, C.c_double, C.c_void_p, C.c_int,
                                            C.POINTER(C.c_int)]
         lib.ref_write_heatmap.argtypes = [C.c_char_p, C.c_void_p, C.c_int, C.c_int, C.c_int]
+        lib.ref_fill_nodata_nearest.argtypes = [_f32p, C.c_int, C.c_int, C.c_float, _f32p]
         lib.ref_linear_scan.argtypes = [_f32p, C.c_int, C.c_int, C.c_int, C.c_int, C.c_double, C.c_double, C.c_double,
                                         C.POINTER(C.c_double), C.c_void_p, C.c_int, C.POINTER(C.c_int)]
 
@@ -145,6 +146,12 @@ class Ref:
         self._check(self.lib.ref_axis_point_set(dimy, dimx, i0, j0, az, ij.ctypes.data, dimy + dimx + 1,
                                                 C.byref(cnt)))
         return [(int(ij[2 * t]), int(ij[2 * t + 1])) for t in range(cnt.value)]
+
+    def fill_nodata_nearest(self, dem, nodata):
+        d = np.ascontiguousarray(dem, np.float32)
+        out = np.empty_like(d)
+        self._check(self.lib.ref_fill_nodata_nearest(d, d.shape[0], d.shape[1], nodata, out))
+        return out
 
     def linear_scan(self, dem, i0, j0, pov_h, az, max_cells=float("inf")):
         d = np.ascontiguousarray(dem, np.float32)

@@ -223,3 +223,25 @@ def test_float_grid_errors(tmp_path, hdr, flt_bytes, msg):
         sk.read_float_grid(tmp_path / "b")
     with pytest.raises(sk.GridFormatError, match="cannot open"):
         sk.read_float_grid(tmp_path / "nope.flt")
+
+
+# ---- nodata fill (dem.cpp:175-213; the CLI's `fill`, cli.cpp:278-284) ------
+
+def test_fill_nodata_nearest_matches_reference_bits():
+    from _oracle import Ref
+    ref = Ref()
+    rng = np.random.default_rng(4)
+    for shape, frac in (((40, 56), 0.3), ((7, 3), 0.8), ((1, 9), 0.5), ((64, 64), 0.02)):
+        v = (rng.standard_normal(shape) * 50).astype(np.float32)
+        v[rng.random(shape) < frac] = -9999.0
+        if np.all(v == -9999.0):
+            v[0, 0] = 1.0
+        dem = sk.Dem(v, 10.0, -9999.0)
+        got = sk.fill_nodata_nearest(dem)
+        assert got.nodata is None and not np.any(got.values == -9999.0)
+        assert np.array_equal(got.values.view(np.uint32), ref.fill_nodata_nearest(v, -9999.0).view(np.uint32))
+    # NaN nodata never equals itself: nothing is filled, as in the reference
+    w = np.array([[1.0, np.nan], [2.0, 3.0]], np.float32)
+    assert np.array_equal(sk.fill_nodata_nearest(sk.Dem(w, 1.0, float("nan"))).values, w, equal_nan=True)
+    with pytest.raises(RuntimeError, match="entirely nodata"):
+        sk.fill_nodata_nearest(sk.Dem(np.full((3, 3), -1.0, np.float32), 1.0, -1.0))
