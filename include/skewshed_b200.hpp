@@ -15,6 +15,7 @@
 
 #include <cmath>
 #include <cstdint>
+#include <cstdio>
 #include <filesystem>
 #include <functional>
 #include <istream>
@@ -359,6 +360,52 @@ inline void write_ascii_grid(const VsGrid& grid, Units out_units, double cellsiz
                                 grid.values.cols(), static_cast<int>(grid.units),
                                 static_cast<int>(out_units), cellsize, origin.easting,
                                 origin.northing));
+}
+
+// ---- bench report (bench.hpp:14-40) ----
+// scan_seconds is the GPU scan phase (scan + exact fixup kernels); workers is
+// the number of GPUs.
+struct BenchReport {
+  std::string dataset;
+  int dimy = 0, dimx = 0, ns = 0, workers = 0;
+  double skew_seconds = 0.0, scan_seconds = 0.0, unskew_seconds = 0.0, reduce_seconds = 0.0;
+  double total_seconds = 0.0, povs_per_second = 0.0, speedup = 0.0;
+};
+
+inline BenchReport make_bench_report(const std::string& dataset, int dimy, int dimx, const RunConfig& cfg,
+                                     const EngineStats& stats, double baseline_total_seconds = 0.0,
+                                     int workers = 1) {
+  BenchReport r;
+  r.dataset = dataset;
+  r.dimy = dimy;
+  r.dimx = dimx;
+  r.ns = cfg.ns;
+  r.workers = workers;
+  r.skew_seconds = stats.skew_seconds;
+  r.scan_seconds = stats.scan_seconds + stats.fixup_seconds;
+  r.unskew_seconds = stats.unskew_seconds;
+  r.reduce_seconds = stats.reduce_seconds;
+  r.total_seconds = stats.total_seconds;
+  r.povs_per_second = static_cast<double>(dimy) * static_cast<double>(dimx) * static_cast<double>(cfg.ns / 2) /
+                      r.scan_seconds;
+  if (baseline_total_seconds > 0.0) r.speedup = baseline_total_seconds / r.total_seconds;
+  return r;
+}
+
+inline std::string format_bench_report(const BenchReport& r) {
+  auto num = [](double v) {
+    char b[64];
+    std::snprintf(b, sizeof(b), "%.17g", v);
+    return std::string(b);
+  };
+  std::string s = "dataset: " + r.dataset + "\n" + "dimy: " + std::to_string(r.dimy) + "\n" +
+                  "dimx: " + std::to_string(r.dimx) + "\n" + "ns: " + std::to_string(r.ns) + "\n" +
+                  "workers: " + std::to_string(r.workers) + "\n" + "skew_seconds: " + num(r.skew_seconds) + "\n" +
+                  "scan_seconds: " + num(r.scan_seconds) + "\n" + "unskew_seconds: " + num(r.unskew_seconds) +
+                  "\n" + "reduce_seconds: " + num(r.reduce_seconds) + "\n" + "total_seconds: " +
+                  num(r.total_seconds) + "\n" + "povs_per_second: " + num(r.povs_per_second) + "\n";
+  if (r.speedup > 0.0) s += "speedup: " + num(r.speedup) + "\n";
+  return s;
 }
 
 }  // namespace skewshed_b200

@@ -535,3 +535,46 @@ def fill_nodata_nearest(dem: Dem) -> Dem:
     check(lib.sks_fill_nodata_nearest(dem.values.ctypes.data, dem.dimy(), dem.dimx(), float(dem.nodata),
                                       out.ctypes.data))
     return Dem(out, dem.cellsize, None, dem.origin)
+
+
+@dataclass
+class BenchReport:
+    """bench.hpp:14-28. scan_seconds here is the whole scan phase on the GPU
+    (scan + exact fixup kernels); workers is the number of GPUs."""
+    dataset: str = ""
+    dimy: int = 0
+    dimx: int = 0
+    ns: int = 0
+    workers: int = 0
+    skew_seconds: float = 0.0
+    scan_seconds: float = 0.0
+    unskew_seconds: float = 0.0
+    reduce_seconds: float = 0.0
+    total_seconds: float = 0.0
+    povs_per_second: float = 0.0
+    speedup: float = 0.0
+
+
+def make_bench_report(dataset: str, dimy: int, dimx: int, cfg: RunConfig, stats: EngineStats,
+                      baseline_total_seconds: float = 0.0, workers: int = 1) -> BenchReport:
+    """make_bench_report (bench.cpp:8-28): one observer scan per cell per
+    sector over the scan-phase seconds; speedup against a baseline total."""
+    scan = stats.scan_seconds + stats.fixup_seconds
+    r = BenchReport(dataset, dimy, dimx, cfg.ns, workers, stats.skew_seconds, scan, stats.unskew_seconds,
+                    stats.reduce_seconds, stats.total_seconds)
+    r.povs_per_second = float(dimy) * float(dimx) * float(cfg.ns // 2) / scan if scan > 0 else float("inf")
+    if baseline_total_seconds > 0.0:
+        r.speedup = baseline_total_seconds / r.total_seconds
+    return r
+
+
+def format_bench_report(r: BenchReport) -> str:
+    """format_bench_report (bench.cpp:30-52): stable key: value lines."""
+    num = lambda v: "%.17g" % v  # noqa: E731
+    lines = [f"dataset: {r.dataset}", f"dimy: {r.dimy}", f"dimx: {r.dimx}", f"ns: {r.ns}", f"workers: {r.workers}",
+             f"skew_seconds: {num(r.skew_seconds)}", f"scan_seconds: {num(r.scan_seconds)}",
+             f"unskew_seconds: {num(r.unskew_seconds)}", f"reduce_seconds: {num(r.reduce_seconds)}",
+             f"total_seconds: {num(r.total_seconds)}", f"povs_per_second: {num(r.povs_per_second)}"]
+    if r.speedup > 0.0:
+        lines.append(f"speedup: {num(r.speedup)}")
+    return "\n".join(lines) + "\n"

@@ -113,3 +113,20 @@ int main(int, char** argv) {
     assert r.returncode == 0, (r.returncode, r.stderr)
     assert r.stdout.strip() == "bad:7:3: expected a number for cell value, got 'q'"
     assert (tmp_path / "v.asc").read_text().splitlines()[-1] == "1.5 1.5 1.5"
+
+
+def test_bench_report_format_matches_reference_layout():
+    """make/format_bench_report (bench.cpp:8-52): same keys, order and %.17g."""
+    st = sk.EngineStats()
+    st.skew_seconds, st.scan_seconds, st.fixup_seconds, st.unskew_seconds = 0.001, 0.06, 0.002, 0.0015
+    st.total_seconds = 0.07
+    cfg = sk.RunConfig(ns=180)
+    r = sk.make_bench_report("dem.asc", 2000, 2000, cfg, st, baseline_total_seconds=70.0)
+    text = sk.format_bench_report(r)
+    keys = [ln.split(":")[0] for ln in text.splitlines()]
+    assert keys == ["dataset", "dimy", "dimx", "ns", "workers", "skew_seconds", "scan_seconds", "unskew_seconds",
+                    "reduce_seconds", "total_seconds", "povs_per_second", "speedup"]
+    assert "scan_seconds: 0.062000000000000000" not in text and "scan_seconds: %.17g" % 0.062 in text
+    assert "povs_per_second: %.17g" % (2000.0 * 2000.0 * 90 / 0.062) in text
+    assert text.endswith("speedup: %.17g\n" % (70.0 / 0.07))
+    assert "speedup" not in sk.format_bench_report(sk.make_bench_report("x", 2, 2, cfg, st))
