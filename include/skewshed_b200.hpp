@@ -185,17 +185,34 @@ inline void validate_or_throw(const Dem& dem, const RunConfig& cfg) {
   check(sks_validate(dem.values.data().data(), dem.dimy(), dem.dimx(), dem.cellsize, nod, &c));
 }
 
+namespace detail {
+// ProgressFn (engine.hpp:34-36): once per sector, ascending k, on the calling
+// thread; sectors run batched on the GPU, so each gets the device time of the
+// phases attributed by its exact scan work.
+inline void report_progress(const Dem& dem, const RunConfig& cfg, const EngineStats& st, const ProgressFn& progress) {
+  const double busy = st.skew_seconds + st.scan_seconds + st.fixup_seconds + st.unskew_seconds;
+  std::vector<double> work(cfg.ns / 2);
+  double total = 0.0;
+  for (int k = 0; k < cfg.ns / 2; ++k) {
+    work[k] = static_cast<double>(sks_sector_target_evals(k, cfg.ns, dem.dimy(), dem.dimx(), dem.cellsize,
+                                                          cfg.max_distance.value_or(0.0)));
+    total += work[k];
+  }
+  for (int k = 0; k < cfg.ns / 2; ++k) progress(k, total > 0.0 ? busy * work[k] / total : 0.0);
+}
+}  // namespace detail
+
 inline Grid<double> total_viewshed_raw(const Dem& dem, const RunConfig& cfg,
                                        EngineStats* stats = nullptr,
                                        const ProgressFn& progress = {}) {
   if (dem.nodata) validate_or_throw(dem, cfg);
   Grid<double> out(dem.dimy(), dem.dimx());
   sks_run_config c = cfg.to_c();
+  EngineStats local;
+  EngineStats* st = stats ? stats : (progress ? &local : nullptr);
   check(sks_total_viewshed_raw(dem.values.data().data(), dem.dimy(), dem.dimx(), dem.cellsize, &c,
-                               out.data().data(), stats));
-  if (progress) {
-    for (int k = 0; k < cfg.ns / 2; ++k) progress(k, 0.0);
-  }
+                               out.data().data(), st));
+  if (progress) detail::report_progress(dem, cfg, *st, progress);
   return out;
 }
 
@@ -206,11 +223,11 @@ inline VsGrid total_viewshed(const Dem& dem, const RunConfig& cfg, EngineStats* 
   out.units = cfg.units;
   out.values.reset(dem.dimy(), dem.dimx());
   sks_run_config c = cfg.to_c();
+  EngineStats local;
+  EngineStats* st = stats ? stats : (progress ? &local : nullptr);
   check(sks_total_viewshed(dem.values.data().data(), dem.dimy(), dem.dimx(), dem.cellsize, &c,
-                           out.values.data().data(), stats));
-  if (progress) {
-    for (int k = 0; k < cfg.ns / 2; ++k) progress(k, 0.0);
-  }
+                           out.values.data().data(), st));
+  if (progress) detail::report_progress(dem, cfg, *st, progress);
   return out;
 }
 

@@ -320,23 +320,35 @@ def _require_no_nodata(dem: Dem, cfg: RunConfig) -> None:
         validate(dem, cfg)
 
 
+def _report_progress(dem: Dem, cfg: RunConfig, st: "EngineStats", progress) -> None:
+    """ProgressFn (engine.hpp:34-36): once per sector, ascending k, on the
+    calling thread. Sectors run batched on the GPU, so each gets the batch
+    phases' device time attributed by its exact scan work."""
+    busy = st.skew_seconds + st.scan_seconds + st.fixup_seconds + st.unskew_seconds
+    work = [sector_target_evals(k, cfg.ns, dem.dimy(), dem.dimx(), dem.cellsize, cfg.max_distance)
+            for k in range(cfg.ns // 2)]
+    total = float(sum(work)) or 1.0
+    for k, w in enumerate(work):
+        progress(k, busy * w / total)
+
+
 def total_viewshed_raw(dem: Dem, cfg: RunConfig, stats: Optional[EngineStats] = None,
                        progress=None) -> np.ndarray:
     _require_no_nodata(dem, cfg)
-    out = _total(dem, cfg, True, stats)
-    if progress is not None:  # engine.hpp:34-36: ascending sector order
-        for k in range(cfg.ns // 2):
-            progress(k, 0.0)
+    st = stats if stats is not None else (EngineStats() if progress is not None else None)
+    out = _total(dem, cfg, True, st)
+    if progress is not None:
+        _report_progress(dem, cfg, st, progress)
     return out
 
 
 def total_viewshed(dem: Dem, cfg: RunConfig, stats: Optional[EngineStats] = None,
                    progress=None) -> VsGrid:
     _require_no_nodata(dem, cfg)
-    out = _total(dem, cfg, False, stats)
+    st = stats if stats is not None else (EngineStats() if progress is not None else None)
+    out = _total(dem, cfg, False, st)
     if progress is not None:
-        for k in range(cfg.ns // 2):
-            progress(k, 0.0)
+        _report_progress(dem, cfg, st, progress)
     return VsGrid(out, Units(cfg.units))
 
 

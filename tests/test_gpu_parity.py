@@ -525,3 +525,19 @@ def test_rejects_bad_inputs():
     bad[1, 1] = np.nan
     with pytest.raises(ValueError, match="non-finite"):
         sk.total_viewshed(sk.Dem(bad, 10.0), sk.RunConfig())
+
+
+def test_progress_reports_every_sector_once_in_order():
+    """engine.hpp:34-36 / test_engine.cpp "every sector is reported exactly
+    once, in order": the callback runs once per sector, ascending, with the
+    batched device time attributed by exact work (non-negative, summing to
+    the phase total)."""
+    dem = sk.make_synthetic(sk.SyntheticKind.Fractal, 48, 40, 10.0, 2)
+    cfg = sk.RunConfig(ns=36, h0=1.5)
+    seen = []
+    st = sk.EngineStats()
+    sk.total_viewshed(dem, cfg, st, progress=lambda k, s: seen.append((k, s)))
+    assert [k for k, _ in seen] == list(range(18))
+    assert all(s >= 0.0 for _, s in seen)
+    busy = st.skew_seconds + st.scan_seconds + st.fixup_seconds + st.unskew_seconds
+    assert sum(s for _, s in seen) == pytest.approx(busy, rel=1e-9)
