@@ -601,6 +601,10 @@ __global__ void __launch_bounds__(kThr, 1) scan2_kernel(const __grid_constant__ 
   if (warp < nslots) load_slot(a, ctl_all + warp * kCtlInts, slots + warp * lay.slot, lay, lane);
 
   unsigned long long skipped = 0;
+#ifdef SKS_EXP_TAIL
+  unsigned long long t_idle = 0;   // start of the current wait for a task
+  unsigned long long idle_ns = 0;  // accumulated waits
+#endif
   int cur = warp % nslots;
   for (;;) {
     int sl = -1, task = 0, alldead = 0;
@@ -628,11 +632,22 @@ __global__ void __launch_bounds__(kThr, 1) scan2_kernel(const __grid_constant__ 
     }
     sl = __shfl_sync(0xffffffffu, sl, 0);
     if (sl < 0) {
+#ifdef SKS_EXP_TAIL
+      if (t_idle == 0) asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_idle));
+#endif
       if (__shfl_sync(0xffffffffu, alldead, 0)) break;
       __nanosleep(200);
       continue;
     }
     task = __shfl_sync(0xffffffffu, task, 0);
+#ifdef SKS_EXP_TAIL
+    if (t_idle != 0) {
+      unsigned long long t_now;
+      asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_now));
+      idle_ns += t_now - t_idle;
+      t_idle = 0;
+    }
+#endif
     cur = sl;
     __threadfence_block();
     int* ctl = ctl_all + sl * kCtlInts;
@@ -732,6 +747,15 @@ __global__ void __launch_bounds__(kThr, 1) scan2_kernel(const __grid_constant__ 
   if (a.skipped != nullptr && lane == 0 && skipped != 0) {
     atomicAdd(a.skipped, 64ull * skipped);
   }
+#ifdef SKS_EXP_TAIL
+  // experiment build: warp-nanoseconds spent without a task (waiting for a
+  // slot's next row or for the end), added << 20 to the skipped counter
+  // (tools/loader_cycles.py reads it back)
+  unsigned long long t_end;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_end));
+  if (t_idle != 0) idle_ns += t_end - t_idle;
+  if (a.skipped != nullptr && lane == 0) atomicAdd(a.skipped, idle_ns << 20);
+#endif
 }
 
 }  // namespace
