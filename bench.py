@@ -369,7 +369,10 @@ def run_ours(args, world, rank, local):
     line = {
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": ms_per_step, "higher_is_better": True, "scaling": "strong",
-        "vs_baseline": None, "dtype": "f32 filter + f64 exact fixup/accumulate", "data": "synthetic",
+        "vs_baseline": None, "dtype": "f32+f64",
+        "dtype_note": "certified f32 filter for the line-of-sight decisions, f64 for every uncertain decision "
+                      "(the reference's own operations) and for the accumulated map; integer ring sums",
+        "data": "synthetic",
         "config": {"workload": workload_name(cfgid, args.terrain), "dimy": n, "dimx": n, "ns": ns, "h0": H0,
                    "max_distance": maxd, "terrain": args.terrain, "cellsize": CELLSIZE,
                    "l2": "flushed between timed steps (256 MiB device write, untimed)",
