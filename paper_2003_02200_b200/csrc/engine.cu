@@ -117,6 +117,7 @@ struct Batch {
   long long pool_elems = 0;  // sdem / cv pool elements
   int lmax = 0;
   bool fused = false;  // relocation fused into scan2's row loader
+  bool any_capped = false;  // some item row is longer than its sector's distance cap + 1
   unsigned fix_cap = 0;
   std::vector<unsigned> fix_off;  // per item: fixup queue segment offset
   int tiles_x = 0, tiles_total = 0;
@@ -196,6 +197,7 @@ std::unique_ptr<Batch> make_batch(const std::vector<SectorPlanH>& plans,
       const RowRange& r = p.ranges[q];
       b->ranges.push_back(make_int2(r.first, r.last));
       const int L = r.last - r.first;
+      if (L >= 2 && p.max_dd < L - 1 && q >= d.q_lo && q < d.q_hi) b->any_capped = true;
       if (L >= 1 && q >= d.q_lo && q < d.q_hi) {
         // rows with no target (L = 1 or a zero cap) only matter to the fused
         // loader, which zeroes their cv range; dropped below otherwise
@@ -369,6 +371,7 @@ struct sks_context {
     a.dbg_vis_bwd = nullptr;
     a.force_exact = 0;
     a.fix_group = scan2_slots_for(a.lmax) > 0 ? 1 : 4;  // POVs per fixup entry
+    a.any_capped = b.any_capped ? 1 : 0;
     return a;
   }
 

@@ -463,7 +463,7 @@ __device__ __forceinline__ void eval16_capped(Pov2& P, unsigned sb, unsigned ivb
   }
 }
 
-template <bool kHl, bool kVis, int kNC>
+template <bool kHl, bool kVis, int kNC, bool kCapped>
 __device__ void run_task(const ScanArgs& a, const Layout2& lay, const Slot& sl, const float* IV,
                          int dir, int chunk, int L, int cap, Pov2& P, int vis_p, uint8_t* vis,
                          int vis_D, unsigned long long& skipped) {
@@ -481,6 +481,9 @@ __device__ void run_task(const ScanArgs& a, const Layout2& lay, const Slot& sl, 
   const unsigned ivb1 = smem_u32(IV + lay.copy(r1)) + 4u * static_cast<unsigned>(kOff - r1 - y1);
   const unsigned w16a = smem_u32(W16), w64a = smem_u32(W64);
   const int ymin = chunk * kTaskPovs;
+  // kCapped: the batch has distance-capped rows and gets the packed tail
+  // (the uncapped kernel keeps the one-target tail only, which leaves its
+  // main loop's code generation as measured fastest)
   const bool capped = cap < L - 1;
   // last target every POV of the task may still use (windows wholly inside
   // run in the main loop; the remainder is the masked tail)
@@ -524,7 +527,7 @@ __device__ void run_task(const ScanArgs& a, const Layout2& lay, const Slot& sl, 
     if (k0 < kc && k0 <= klast) break;  // next window crosses the cap: tail
   }
   flush(P);
-  if (capped && !kVis) {
+  if (kCapped && capped && !kVis) {
     // masked tail: targets beyond some POVs' distance cap, packed like the
     // main loop, with the same hidden-window skip
     const int ylast = min(L - 1, ymin + kTaskPovs - 1);
@@ -577,7 +580,7 @@ __device__ void run_task(const ScanArgs& a, const Layout2& lay, const Slot& sl, 
   skipped += nskip;
 }
 
-template <int kThr, int kNC>
+template <int kThr, int kNC, bool kCapped>
 __global__ void __launch_bounds__(kThr, 1) scan2_kernel(const __grid_constant__ ScanArgs a, int nslots, int lmax) {
   extern __shared__ __align__(16) float smem[];
   const Layout2 lay(lmax, kNC);
@@ -708,14 +711,14 @@ __global__ void __launch_bounds__(kThr, 1) scan2_kernel(const __grid_constant__ 
     const bool any_hl = __any_sync(0xffffffffu, P.hl0 != 0.f || P.hl1 != 0.f);
     if (vis_mode) {
       if (any_hl) {
-        run_task<true, true, kNC>(a, lay, sp, IV, dir, chunk, L, cap, P, vis ? vis_p : -1, vis, vis_D, skipped);
+        run_task<true, true, kNC, kCapped>(a, lay, sp, IV, dir, chunk, L, cap, P, vis ? vis_p : -1, vis, vis_D, skipped);
       } else {
-        run_task<false, true, kNC>(a, lay, sp, IV, dir, chunk, L, cap, P, vis ? vis_p : -1, vis, vis_D, skipped);
+        run_task<false, true, kNC, kCapped>(a, lay, sp, IV, dir, chunk, L, cap, P, vis ? vis_p : -1, vis, vis_D, skipped);
       }
     } else if (any_hl) {
-      run_task<true, false, kNC>(a, lay, sp, IV, dir, chunk, L, cap, P, -1, nullptr, 0, skipped);
+      run_task<true, false, kNC, kCapped>(a, lay, sp, IV, dir, chunk, L, cap, P, -1, nullptr, 0, skipped);
     } else {
-      run_task<false, false, kNC>(a, lay, sp, IV, dir, chunk, L, cap, P, -1, nullptr, 0, skipped);
+      run_task<false, false, kNC, kCapped>(a, lay, sp, IV, dir, chunk, L, cap, P, -1, nullptr, 0, skipped);
     }
 
     {
@@ -792,13 +795,13 @@ size_t scan2_smem_bytes(int lmax, int nslots) {
   return static_cast<size_t>(Layout2(lmax, c > 0 ? c : 4).total(nslots)) * sizeof(float);
 }
 
-template <int kThr, int kNC>
+template <int kThr, int kNC, bool kCapped>
 static int launch_scan2_t(const ScanArgs& a, int nslots, int sms, cudaStream_t st) {
   const size_t smem = static_cast<size_t>(Layout2(a.lmax, kNC).total(nslots)) * sizeof(float);
-  cudaError_t e = cudaFuncSetAttribute(scan2_kernel<kThr, kNC>,
+  cudaError_t e = cudaFuncSetAttribute(scan2_kernel<kThr, kNC, kCapped>,
                                        cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
   if (e != cudaSuccess) return static_cast<int>(e);
-  scan2_kernel<kThr, kNC><<<sms, kThr, smem, st>>>(a, nslots, a.lmax);
+  scan2_kernel<kThr, kNC, kCapped><<<sms, kThr, smem, st>>>(a, nslots, a.lmax);
   return static_cast<int>(cudaGetLastError());
 }
 
@@ -811,8 +814,12 @@ int launch_scan2(const ScanArgs& a, int nslots, void* stream) {
   scan2_config(a.lmax, &copies, &fit);
   if (copies == 0 || nslots < 1 || nslots > fit) return static_cast<int>(cudaErrorInvalidValue);
   cudaStream_t st = static_cast<cudaStream_t>(stream);
-  return copies == 4 ? launch_scan2_t<kThreads, 4>(a, nslots, sms, st)
-                     : launch_scan2_t<kThreads, 2>(a, nslots, sms, st);
+  if (a.any_capped) {
+    return copies == 4 ? launch_scan2_t<kThreads, 4, true>(a, nslots, sms, st)
+                       : launch_scan2_t<kThreads, 2, true>(a, nslots, sms, st);
+  }
+  return copies == 4 ? launch_scan2_t<kThreads, 4, false>(a, nslots, sms, st)
+                     : launch_scan2_t<kThreads, 2, false>(a, nslots, sms, st);
 }
 
 }  // namespace sks

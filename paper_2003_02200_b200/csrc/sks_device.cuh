@@ -85,6 +85,7 @@ struct ScanArgs {
   uint8_t* dbg_vis_fwd;
   uint8_t* dbg_vis_bwd;
   int force_exact;        // every POV group goes through the FP64 fixup
+  int any_capped;         // some row's distance cap is shorter than the row
   int fix_group;          // POVs per fixup entry: 1 (scan2_kernel) or 4 (scan_kernel)
 };
 
