@@ -19,6 +19,7 @@
 #include <filesystem>
 #include <functional>
 #include <istream>
+#include <limits>
 #include <iterator>
 #include <numbers>
 #include <optional>
@@ -424,5 +425,98 @@ inline std::string format_bench_report(const BenchReport& r) {
   if (r.speedup > 0.0) s += "speedup: " + num(r.speedup) + "\n";
   return s;
 }
+
+// ---- heatmaps (heatmap.hpp) ----
+enum class Palette { Gray = SKS_PALETTE_GRAY, BlueRed = SKS_PALETTE_BLUE_RED };
+
+inline void write_heatmap(const VsGrid& grid, const std::filesystem::path& path, Palette palette) {
+  check(sks_write_heatmap(path.string().c_str(), grid.values.data().data(), grid.values.rows(), grid.values.cols(),
+                          static_cast<int>(palette)));
+}
+
+// ---- the rotational-sweep oracle on the GPU (oracle.hpp) ----
+namespace oracle {
+
+struct GridPoint {
+  int i = 0;
+  int j = 0;
+};
+
+struct RingSector {
+  double r_open = 0.0;
+  double r_close = 0.0;
+};
+
+using RingSectorSet = std::vector<RingSector>;
+
+inline constexpr int kReferenceCellGuard = SKS_REFERENCE_CELL_GUARD;
+
+inline std::vector<GridPoint> select_axis_point_set(const Dem& dem, int i0, int j0, double azimuth_deg) {
+  int n = 0;
+  check(sks_axis_point_set(dem.dimy(), dem.dimx(), i0, j0, azimuth_deg, nullptr, 0, &n));
+  std::vector<int> ij(2 * static_cast<size_t>(std::max(n, 1)));
+  check(sks_axis_point_set(dem.dimy(), dem.dimx(), i0, j0, azimuth_deg, ij.data(), n, &n));
+  std::vector<GridPoint> pts(static_cast<size_t>(n));
+  for (int t = 0; t < n; ++t) pts[t] = {ij[2 * t], ij[2 * t + 1]};
+  return pts;
+}
+
+inline double linear_scan(const Dem& dem, int i0, int j0, double pov_h, double azimuth_deg,
+                          double max_dist_cells = std::numeric_limits<double>::infinity(),
+                          RingSectorSet* rings_out = nullptr, int device = 0) {
+  double cv = 0.0;
+  int n = 0;
+  check(sks_linear_scan(dem.values.data().data(), dem.dimy(), dem.dimx(), i0, j0, pov_h, azimuth_deg,
+                        max_dist_cells, device, &cv, nullptr, 0, &n));
+  if (rings_out && n > 0) {
+    std::vector<double> r(2 * static_cast<size_t>(n));
+    check(sks_linear_scan(dem.values.data().data(), dem.dimy(), dem.dimx(), i0, j0, pov_h, azimuth_deg,
+                          max_dist_cells, device, &cv, r.data(), n, &n));
+    for (int t = 0; t < n; ++t) rings_out->push_back({r[2 * t], r[2 * t + 1]});
+  }
+  return cv;
+}
+
+inline double singular_viewshed(const Dem& dem, int i0, int j0, double h0, int ns,
+                                std::optional<double> max_distance = {}, int device = 0) {
+  double area = 0.0;
+  check(sks_singular_viewshed(dem.values.data().data(), dem.dimy(), dem.dimx(), dem.cellsize, i0, j0, h0, ns,
+                              max_distance.value_or(0.0), device, &area));
+  return area;
+}
+
+struct MultiViewshed {
+  VsGrid grid;  // nonzero only at the observer cells, m^2
+  double total_area = 0.0;
+};
+
+inline MultiViewshed multi_viewshed(const Dem& dem, std::span<const GridPoint> povs, double h0, int ns,
+                                    std::optional<double> max_distance = {}, int device = 0) {
+  std::vector<int> ij(2 * povs.size());
+  for (size_t t = 0; t < povs.size(); ++t) {
+    ij[2 * t] = povs[t].i;
+    ij[2 * t + 1] = povs[t].j;
+  }
+  MultiViewshed out;
+  out.grid.units = Units::SquareMeters;
+  out.grid.values.reset(dem.dimy(), dem.dimx(), 0.0);
+  check(sks_multi_viewshed(dem.values.data().data(), dem.dimy(), dem.dimx(), dem.cellsize, ij.data(),
+                           static_cast<int>(povs.size()), h0, ns, max_distance.value_or(0.0), device, nullptr,
+                           out.grid.values.data().data(), &out.total_area));
+  return out;
+}
+
+inline VsGrid total_viewshed_reference(const Dem& dem, const RunConfig& cfg, bool force = false) {
+  VsGrid out;
+  out.units = cfg.units;
+  out.values.reset(dem.dimy(), dem.dimx());
+  const sks_run_config c = cfg.to_c();
+  const float nod = dem.nodata.value_or(0.0f);
+  check(sks_total_viewshed_reference(dem.values.data().data(), dem.dimy(), dem.dimx(), dem.cellsize,
+                                     dem.nodata ? &nod : nullptr, &c, force ? 1 : 0, out.values.data().data()));
+  return out;
+}
+
+}  // namespace oracle
 
 }  // namespace skewshed_b200

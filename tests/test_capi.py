@@ -130,3 +130,43 @@ def test_bench_report_format_matches_reference_layout():
     assert "povs_per_second: %.17g" % (2000.0 * 2000.0 * 90 / 0.062) in text
     assert text.endswith("speedup: %.17g\n" % (70.0 / 0.07))
     assert "speedup" not in sk.format_bench_report(sk.make_bench_report("x", 2, 2, cfg, st))
+
+
+def test_cpp_facade_host_utilities(tmp_path):
+    """The facade's host-side pieces of the reference API, linked against the
+    shipped library: oracle::select_axis_point_set, fill_nodata_nearest,
+    write_heatmap, bench report (no GPU needed)."""
+    src = tmp_path / "u.cpp"
+    src.write_text(r'''
+#include "skewshed_b200.hpp"
+#include <cstdio>
+namespace sk = skewshed_b200;
+int main(int, char** argv) {
+  sk::Dem d;
+  d.values.reset(6, 9, 2.0f);
+  d.cellsize = 10.0;
+  auto pts = sk::oracle::select_axis_point_set(d, 2, 3, 0.0);  // eastward: (2,4) .. (2,8)
+  if (pts.size() != 5 || pts[0].i != 2 || pts[0].j != 4 || pts[4].j != 8) return 1;
+  d.nodata = -1.0f;
+  d.values(0, 0) = -1.0f;
+  sk::Dem f = sk::fill_nodata_nearest(d);
+  if (f.nodata || f.values(0, 0) != 2.0f) return 2;
+  sk::VsGrid vs{sk::Grid<double>(2, 2, 0.0), sk::Units::SquareMeters};
+  vs.values(1, 1) = 4.0;
+  sk::write_heatmap(vs, argv[1], sk::Palette::Gray);
+  sk::EngineStats st;
+  st.scan_seconds = 0.5;
+  st.total_seconds = 1.0;
+  std::fputs(sk::format_bench_report(sk::make_bench_report("d", 2, 2, sk::RunConfig{}, st)).c_str(), stdout);
+  return 0;
+}
+''')
+    exe = tmp_path / "u"
+    libdir = os.path.join(ROOT, "paper_2003_02200_b200")
+    r = subprocess.run(["g++", "-std=c++20", "-I", os.path.join(ROOT, "include"), str(src), "-o", str(exe),
+                        "-L", libdir, "-lskewshed_b200", f"-Wl,-rpath,{libdir}"], capture_output=True, text=True)
+    assert r.returncode == 0, r.stderr
+    r = subprocess.run([str(exe), str(tmp_path / "h.pgm")], capture_output=True, text=True)
+    assert r.returncode == 0, (r.returncode, r.stderr)
+    assert (tmp_path / "h.pgm").read_bytes() == b"P5\n2 2\n255\n\x00\x00\x00\xff"
+    assert "povs_per_second: 1440\n" in r.stdout
