@@ -170,3 +170,40 @@ int main(int, char** argv) {
     assert r.returncode == 0, (r.returncode, r.stderr)
     assert (tmp_path / "h.pgm").read_bytes() == b"P5\n2 2\n255\n\x00\x00\x00\xff"
     assert "povs_per_second: 1440\n" in r.stdout
+
+
+@pytest.mark.gpu
+def test_cpp_facade_reference_style_engine_test(tmp_path):
+    """test_engine.cpp:93-106 ("per-sector sweeps reduce to exactly the engine
+    accumulator") and :231-241 (units) written as a C++ program against the
+    facade, run on the GPU."""
+    src = tmp_path / "e.cpp"
+    src.write_text(r'''
+#include "skewshed_b200.hpp"
+namespace sk = skewshed_b200;
+int main() {
+  sk::Dem dem = sk::make_synthetic(sk::SyntheticKind::SmoothedNoise, 40, 56, 10.0, 3);
+  sk::RunConfig cfg;
+  cfg.ns = 24;
+  cfg.units = sk::Units::SquareMeters;
+  sk::Grid<double> raw = sk::total_viewshed_raw(dem, cfg);
+  sk::Grid<double> acc(40, 56, 0.0);
+  for (int k = 0; k < cfg.ns / 2; ++k) sk::accumulate_into(acc, sk::sector_sweep(dem, cfg, k).contribution);
+  if (!(acc == raw)) return 1;
+  sk::VsGrid m2 = sk::total_viewshed(dem, cfg);
+  cfg.units = sk::Units::SquareKilometers;
+  sk::VsGrid km2 = sk::total_viewshed(dem, cfg);
+  for (size_t n = 0; n < m2.values.size(); ++n) {
+    if (km2.values.data()[n] != m2.values.data()[n] * 1e-6 &&
+        std::abs(km2.values.data()[n] - m2.values.data()[n] * 1e-6) > 1e-15 * m2.values.data()[n]) return 2;
+  }
+  return 0;
+}
+''')
+    exe = tmp_path / "e"
+    libdir = os.path.join(ROOT, "paper_2003_02200_b200")
+    r = subprocess.run(["g++", "-std=c++20", "-I", os.path.join(ROOT, "include"), str(src), "-o", str(exe),
+                        "-L", libdir, "-lskewshed_b200", f"-Wl,-rpath,{libdir}"], capture_output=True, text=True)
+    assert r.returncode == 0, r.stderr
+    r = subprocess.run([str(exe)], capture_output=True, text=True)
+    assert r.returncode == 0, (r.returncode, r.stderr)
