@@ -27,7 +27,8 @@ __device__ __forceinline__ bool full_d(double w) {
   return w > __dsub_rn(1.0, kTolD) && w < __dadd_rn(1.0, kTolD);
 }
 
-template <bool kFromCv>
+// Untiled form over a caller's skwVS (sks_unskew_accumulate, the per-phase
+// debug entry): one thread per DEM cell.
 __global__ void __launch_bounds__(256) unskew_kernel(BatchDev b, const double* __restrict__ vs,
                                                      double* __restrict__ map, int dimy,
                                                      int dimx) {
@@ -53,13 +54,8 @@ __global__ void __launch_bounds__(256) unskew_kernel(BatchDev b, const double* _
     const bool c = full_d(w_m);
     const long long cell = sd.sdem_off + static_cast<long long>(p) * sd.pitch + j;
     double va = 0.0, vb = 0.0;
-    if (kFromCv) {
-      if (a) va = __dmul_rn(static_cast<double>(__ldg(b.cv + cell)), sd.correction);
-      if (!a || c) vb = __dmul_rn(static_cast<double>(__ldg(b.cv + cell - sd.pitch)), sd.correction);
-    } else {
-      if (a) va = vs[cell];
-      if (!a || c) vb = vs[cell - sd.pitch];
-    }
+    if (a) va = vs[cell];
+    if (!a || c) vb = vs[cell - sd.pitch];
     double v;
     if (a && c) {
       v = __dadd_rn(__dmul_rn(omr, va), __dmul_rn(r, vb));
@@ -75,7 +71,7 @@ __global__ void __launch_bounds__(256) unskew_kernel(BatchDev b, const double* _
 
 constexpr int kUT = 32;           // tile edge (cells)
 
-// Tiled unskew (same per-cell arithmetic as unskew_kernel<true>, same
+// Tiled unskew (same per-cell arithmetic as unskew_kernel, same
 // ascending-k order). A CTA owns a 32x32 tile of DEM cells (each thread 4
 // cells of one column) and walks the batch's sectors; the cv block is staged
 // by SOURCE row: T[ir][jl] =
@@ -285,7 +281,7 @@ int launch_unskew_from_vs(const BatchDev& b, const double* skw_vs, double* map, 
   const long long n = static_cast<long long>(dimy) * dimx;
   const int threads = 256;
   const unsigned grid = static_cast<unsigned>((n + threads - 1) / threads);
-  unskew_kernel<false><<<grid, threads, 0, static_cast<cudaStream_t>(stream)>>>(b, skw_vs, map,
+  unskew_kernel<<<grid, threads, 0, static_cast<cudaStream_t>(stream)>>>(b, skw_vs, map,
                                                                                 dimy, dimx);
   return static_cast<int>(cudaGetLastError());
 }
