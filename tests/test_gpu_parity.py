@@ -541,3 +541,19 @@ def test_progress_reports_every_sector_once_in_order():
     assert all(s >= 0.0 for _, s in seen)
     busy = st.skew_seconds + st.scan_seconds + st.fixup_seconds + st.unskew_seconds
     assert sum(s for _, s in seen) == pytest.approx(busy, rel=1e-9)
+
+
+@pytest.mark.parametrize("maxd", [1000.0, 2410.0])
+def test_long_capped_rows_packed_tail_bitexact(ora, maxd):
+    """Distance caps long enough for the main loop, the hidden-window skip
+    and the packed, NaN-masked tail windows of scan2 (config 3's regime:
+    cap 100-241 cells on rows of ~300-420) — every POV bit-exact against the
+    reference's sector_viewshed."""
+    dem = sk.make_synthetic(sk.SyntheticKind.Fractal, 300, 260, 10.0, 19).values
+    for k in (0, 3, 5, 9):
+        p, v, rr, base = _ref_sdem(ora, dem, k, 20)
+        cap = sk.distance_cap_cells(maxd, p.shear_tan, 10.0)
+        ref = ora.sector_viewshed(v, rr, p.rows, base, p.shear_tan, 1.5, cap)
+        skw = sk.SkwGrid(v, rr, base, p.rows, p.shear_tan)
+        ours = sk.sector_viewshed(skw, 1.5, cap)
+        assert np.array_equal(b64(ours), b64(ref)), (k, cap)
