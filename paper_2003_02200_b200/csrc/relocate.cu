@@ -129,8 +129,10 @@ relocate_kernel(const float* __restrict__ dem, BatchDev b, int tiles_x) {
       const int q = q0 + r0 + u;
       if (q < sd.skw_rows) {
         const size_t o = static_cast<size_t>(q) * sd.pitch + j0 + cx;
-        *reinterpret_cast<float4*>(out + o) = make_float4(v[u][0], v[u][1], v[u][2], v[u][3]);
-        *reinterpret_cast<int4*>(cvz + o) = make_int4(0, 0, 0, 0);
+        // streaming (evict-first) stores: 2.9 GB of sDEM + cv must not push
+        // the 16 MB DEM, which every tile gathers from, out of L2
+        __stcs(reinterpret_cast<float4*>(out + o), make_float4(v[u][0], v[u][1], v[u][2], v[u][3]));
+        __stcs(reinterpret_cast<int4*>(cvz + o), make_int4(0, 0, 0, 0));
       }
     }
   }
