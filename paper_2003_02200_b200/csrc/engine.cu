@@ -521,6 +521,7 @@ void run_sectors(sks_context* ctx, const float* d_dem, int dimy, int dimx, doubl
         long long rows = 0, chunks = 0, tot = 0, work = 0, maxw = 0;
         unsigned mx = 0;
         for (size_t i = 0; i < fc.size(); ++i) {
+          fc[i] = (fc[i] & 0xffffu) + (fc[i] >> 16);  // forward | backward << 16
           if (fc[i] == 0) continue;
           const int2 r = b.ranges[b.sdev[b.items[i].s].row_off + b.items[i].q];
           ++rows;

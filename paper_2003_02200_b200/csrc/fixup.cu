@@ -291,7 +291,10 @@ __global__ void __launch_bounds__(kPrefixThreads) fixup_prefix_sums_kernel(ScanA
   __shared__ unsigned tot;
   const int b0 = blockIdx.x * chunk, b1 = min(a.n_items, b0 + chunk);
   unsigned local = 0;
-  for (int i = b0 + threadIdx.x; i < b1; i += blockDim.x) local += __ldg(a.fix_cnt + i);
+  for (int i = b0 + threadIdx.x; i < b1; i += blockDim.x) {
+    const unsigned c = __ldg(a.fix_cnt + i);  // forward | backward << 16
+    local += (c & 0xffffu) + (c >> 16);
+  }
   block_excl_scan(local, wt, &tot);
   if (threadIdx.x == 0) bsum[blockIdx.x] = tot * static_cast<unsigned>(a.fix_group);
 }
@@ -314,7 +317,8 @@ __global__ void __launch_bounds__(kPrefixThreads) fixup_prefix_write_kernel(Scan
   const int b0 = blockIdx.x * chunk, b1 = min(a.n_items, b0 + chunk);
   for (int t0 = b0; t0 < b1; t0 += blockDim.x) {
     const int i = t0 + threadIdx.x;
-    const unsigned v = i < b1 ? __ldg(a.fix_cnt + i) * grp : 0u;
+    const unsigned c = i < b1 ? __ldg(a.fix_cnt + i) : 0u;
+    const unsigned v = ((c & 0xffffu) + (c >> 16)) * grp;
     const unsigned ex = block_excl_scan(v, wt, &tot);
     if (i < b1) off[i] = base + ex;
     base += tot;
@@ -353,7 +357,10 @@ __global__ void __launch_bounds__(kWarps * 32, SKS_FIX_MINB) fixup_kernel(ScanAr
     const int L = rg.y - rg.x;
     const long long rowoff = sd.sdem_off + static_cast<long long>(item.q) * sd.pitch;
     const float* row = a.b.sdem + rowoff + first;
-    const unsigned ent = a.fix_queue[a.fix_off[it] + wj / grp];
+    // forward entries at the segment start, backward ones from slot L
+    const unsigned nf = __ldg(a.fix_cnt + it) & 0xffffu;
+    const unsigned e = wj / grp;
+    const unsigned ent = a.fix_queue[a.fix_off[it] + (e < nf ? e : static_cast<unsigned>(L) + (e - nf))];
     const int dir = static_cast<int>(ent >> 31);
     const int y = static_cast<int>((ent & 0x7fffffffu) * grp + wj % grp);
     if (y >= L) continue;

@@ -459,7 +459,9 @@ __global__ void __launch_bounds__(512, 2) scan_kernel(ScanArgs a) {
       if (!any_valid) continue;
       if (flag) {
         atomicAdd(a.fix_count, 1u);
-        const unsigned slot = atomicAdd(a.fix_cnt + cur, 1u);
+        // forward groups first, backward groups from slot L (packed counts)
+        const unsigned old = atomicAdd(a.fix_cnt + cur, dir ? 0x10000u : 1u);
+        const unsigned slot = dir ? static_cast<unsigned>(L) + (old >> 16) : (old & 0xffffu);
         a.fix_queue[a.fix_off[cur] + slot] = pack_fix(static_cast<unsigned>(dir), static_cast<unsigned>(y0 >> 2));
       } else {
         int* dst = dir ? cvrow_b : cvrow;

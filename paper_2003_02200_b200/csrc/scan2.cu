@@ -735,7 +735,11 @@ __global__ void __launch_bounds__(kThr, 1) scan2_kernel(const __grid_constant__ 
         if (!v) continue;
         if (fl) {
           atomicAdd(a.fix_count, 1u);
-          const unsigned slot = atomicAdd(a.fix_cnt + item, 1u);
+          // forward entries fill the segment's first L slots, backward ones
+          // the next L (16-bit counts packed in one counter), so the fixup's
+          // neighbouring lanes walk the same direction
+          const unsigned old = atomicAdd(a.fix_cnt + item, dir ? 0x10000u : 1u);
+          const unsigned slot = dir ? static_cast<unsigned>(L) + (old >> 16) : (old & 0xffffu);
           a.fix_queue[a.fix_off[item] + slot] = pack_fix(static_cast<unsigned>(dir), static_cast<unsigned>(y));
         } else if (cvp != 0) {
           atomicAdd(dst + (dir ? L - 1 - y : y), cvp);
