@@ -57,7 +57,7 @@ constexpr int kTaskPovs = 64;
 #endif
 constexpr int kW = SKS_FINE_W;  // fine window (targets): 8 or 16
 #ifndef SKS_NEAR_NOTEST
-#define SKS_NEAR_NOTEST 64
+#define SKS_NEAR_NOTEST 80  // measured: 32 60.6, 48 60.4, 64 60.2, 80 59.7, 96 59.8, 128 61.4 ms (config 2)
 #endif
 #ifndef SKS_COARSE_W
 #define SKS_COARSE_W 64
