@@ -59,6 +59,9 @@ constexpr int kW = SKS_FINE_W;  // fine window (targets): 8 or 16
 #ifndef SKS_NEAR_NOTEST
 #define SKS_NEAR_NOTEST 80  // measured: 32 60.6, 48 60.4, 64 60.2, 80 59.7, 96 59.8, 128 61.4 ms (config 2)
 #endif
+#ifndef SKS_COARSE_NOTEST
+#define SKS_COARSE_NOTEST SKS_NEAR_NOTEST
+#endif
 #ifndef SKS_COARSE_W
 #define SKS_COARSE_W 64
 #endif
@@ -498,8 +501,9 @@ __device__ void run_task(const ScanArgs& a, const Layout2& lay, const Slot& sl, 
   // the first coarse window holds the task triangle and every POV's nearest
   // targets, where almost no window is hidden: no skip tests there
   const int ktest = ymin + SKS_NEAR_NOTEST;
+  const int kctest = ymin + SKS_COARSE_NOTEST;  // coarse tests only from here
   while (k0 <= klast) {
-    if (!kVis && k0 >= ktest && k0 + kH - 1 <= kmain) {
+    if (!kVis && k0 >= kctest && k0 + kH - 1 <= kmain) {
       const float2 em = lds64(w64a + 8u * (static_cast<unsigned>(k0) / kH));
       if (window_hidden<kHl>(P, em, tb, k0, kH)) {
         k0 += kH;
