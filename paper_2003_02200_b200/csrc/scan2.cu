@@ -780,7 +780,13 @@ static void scan2_config(int lmax, int* copies, int* slots) {
   *slots = 0;
   if (lmax >= 32768 - 128) return;  // k < 2^15 keeps the flush sums exact
   const long long cap = 227 * 1024;
+#ifdef SKS_PREFER_NC4
   for (int nc : {4, 2}) {
+#else
+  // 2 copies (pair loads) even where 4 would fit: the smem they free holds
+  // more row slots, which measured faster (config 2 scan 59.7 -> 58.9 ms)
+  for (int nc : {2}) {
+#endif
     const Layout2 lay(lmax, nc);
     const long long n = (cap - 4LL * lay.slots) / (4LL * lay.slot);
     if (n >= (nc == 4 ? 2 : 1)) {
