@@ -72,7 +72,10 @@ constexpr int kOff = 128;  // table index offset (dd >= -kOff + 1 addressable)
 #define SKS_SCAN_THREADS 768
 #endif
 constexpr int kThreads = SKS_SCAN_THREADS;  // 24 warps: 80 registers, no spills (1024 spills at 64)
-constexpr int kMaxSlots = 8;
+#ifndef SKS_MAX_SLOTS
+#define SKS_MAX_SLOTS 8
+#endif
+constexpr int kMaxSlots = SKS_MAX_SLOTS;
 constexpr int kCtlInts = 16;  // per slot control block
 constexpr float kBand = 5.9604644775390625e-07f;  // 10 * 2^-24
 constexpr int kSumShift = 22;
