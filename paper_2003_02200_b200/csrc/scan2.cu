@@ -15,8 +15,10 @@
 // fractal 2000^2: 27% of target slots evaluated vs 46%).
 //
 // Per group of 4 targets a lane loads one broadcast quad of elevations and,
-// per POV, one quad of fl(1/dd) from a table copy whose shift makes the quad
-// 16-byte aligned (4 shifted copies; dd = k - y differs per lane). The ring
+// per POV, the 4 fl(1/dd) from a table copy whose shift aligns them (dd =
+// k - y differs per lane): two pair loads from one of 2 shifted copies by
+// default (the smaller tables leave room for one more row slot, measured
+// faster), or one quad from one of 4 copies with -DSKS_PREFER_NC4. The ring
 // sum cv = sum over visible targets of (2dd+1) is accumulated without a
 // per-lane table: records add (k + 2^22) to an integer (one predicated IADD3;
 // one accumulator per slot of a 4-target group so that the added register is
