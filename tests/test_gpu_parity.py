@@ -557,3 +557,21 @@ def test_long_capped_rows_packed_tail_bitexact(ora, maxd):
         skw = sk.SkwGrid(v, rr, base, p.rows, p.shear_tan)
         ours = sk.sector_viewshed(skw, 1.5, cap)
         assert np.array_equal(b64(ours), b64(ref)), (k, cap)
+
+
+@pytest.mark.parametrize("maxd", [None, 120.0])
+def test_many_batches_bitexact(ora, maxd, monkeypatch):
+    """A memory budget small enough to split the sectors into several
+    batches (SKS_BATCH_GB, read when a context builds its plans): every batch
+    runs relocate -> scan -> fixup -> unskew into the same map in ascending
+    sector order, so the raw map is still bit-identical (configs 4-5 run in
+    batches)."""
+    monkeypatch.setenv("SKS_BATCH_GB", "0.0004")
+    dem = sk.make_synthetic(sk.SyntheticKind.Fractal, 56, 48, 10.0, 21)
+    cfg = sk.RunConfig(ns=36, h0=1.5, max_distance=maxd, units=sk.Units.SquareMeters)
+    ref = ora.total_viewshed(dem.values, 10.0, 36, 1.5, max_distance=maxd or 0.0, raw=True)
+    ctx = sk.Context(0)
+    ours, st = ctx.total_viewshed(dem.values, 10.0, cfg, raw=True, want_stats=True)
+    assert st.batches > 3
+    assert np.array_equal(b64(ours), b64(ref))
+    ctx.close()
