@@ -33,7 +33,10 @@ namespace sks {
 namespace {
 
 constexpr float kBand = 5.9604644775390625e-07f;  // 10 * 2^-24, as in the scan kernels
-constexpr int kWarps = 8;
+#ifndef SKS_FIX_WARPS
+#define SKS_FIX_WARPS 8
+#endif
+constexpr int kWarps = SKS_FIX_WARPS;
 
 // Exact state of one POV scan (the reference recurrence under the filter).
 struct ExactState {
