@@ -93,6 +93,11 @@ const char* sks_last_error(void);
 const char* sks_version(void);
 /* Number of visible CUDA devices (0 on a host without a GPU). */
 int sks_device_count(void);
+/* Longest skewed row (cells) the shared-memory scan kernel holds; longer rows
+ * are scanned POV by POV by the exact kernel (same results, slower). Rows are
+ * limited to 46340 cells overall (the int32 ring sums; SKS_INVALID_ARGUMENT
+ * beyond). No GPU needed. */
+int sks_scan_row_limit(void);
 
 /* ---- host planning (no GPU needed) ---------------------------------- */
 

@@ -10,7 +10,7 @@ from .engine import (AxisOp, BenchReport, Palette, fill_nodata_nearest, format_b
                      SkwGrid, SyntheticKind, Units, VsGrid, accumulate_into, area_scale, area_scale_factor,
                      build_sector_sdem, build_skw, convert_units, device_count, distance_cap_cells,
                      kNoDistanceCap, linear_viewshed_row, make_synthetic, partition_sectors, plan_sector,
-                     reduce_ordered, row_ranges, sector_sweep, sector_target_evals, sector_viewshed,
+                     reduce_ordered, row_ranges, scan_row_limit, sector_sweep, sector_target_evals, sector_viewshed,
                      shear_params, total_target_evals, total_viewshed, total_viewshed_raw,
                      unskew_accumulate, validate)
 from . import sweep  # noqa: E402  (rotational-sweep oracle API, oracle.hpp)
@@ -21,7 +21,7 @@ __all__ = [
     "SkwGrid", "SyntheticKind", "Units", "VsGrid", "accumulate_into", "area_scale", "area_scale_factor",
     "build_sector_sdem", "build_skw", "convert_units", "device_count", "distance_cap_cells",
     "kNoDistanceCap", "linear_viewshed_row", "make_synthetic", "partition_sectors", "plan_sector",
-    "reduce_ordered", "row_ranges", "sector_sweep", "sector_target_evals", "sector_viewshed",
+    "reduce_ordered", "row_ranges", "scan_row_limit", "sector_sweep", "sector_target_evals", "sector_viewshed",
     "shear_params", "total_target_evals", "total_viewshed", "total_viewshed_raw", "unskew_accumulate",
     "validate",
 ]

@@ -77,6 +77,7 @@ SIGNATURES = {
     "sks_last_error": (C.c_char_p, []),
     "sks_version": (C.c_char_p, []),
     "sks_device_count": (C.c_int, []),
+    "sks_scan_row_limit": (C.c_int, []),
     "sks_plan_sector": (C.c_int, [C.c_int, C.c_int, C.c_int, C.c_int, C.POINTER(SectorPlanC)]),
     "sks_shear_params": (None, [C.c_double, C.c_int, _ip, _dp]),
     "sks_distance_cap_cells": (C.c_int, [C.c_double, C.c_double, C.c_double]),

@@ -46,14 +46,20 @@ def build(force: bool = False, verbose: bool = False, defines=(), out: str = Non
         return LIB
     objdir = os.path.join(HERE, "_obj" + ("_" + "_".join(d.replace("=", "") for d in defines) if defines else ""))
     os.makedirs(objdir, exist_ok=True)
-    objs = []
-    for src in sources():
+    from concurrent.futures import ThreadPoolExecutor
+
+    def compile_one(src):
         obj = os.path.join(objdir, os.path.basename(src) + ".o")
         dflags = [f"-D{d}" for d in defines]
         cmd = ["nvcc", *NVCC_FLAGS, *dflags, "-c", src, "-o", obj]
         if src.endswith(".cpp"):
             cmd = ["nvcc", *NVCC_FLAGS, *dflags, "-x", "cu", "-c", src, "-o", obj]
-        r = subprocess.run(cmd, capture_output=True, text=True)
+        return src, obj, subprocess.run(cmd, capture_output=True, text=True)
+
+    objs = []
+    with ThreadPoolExecutor(max(1, min(8, os.cpu_count() or 1))) as ex:
+        results = list(ex.map(compile_one, sources()))
+    for src, obj, r in results:
         if r.returncode != 0:
             sys.stderr.write(r.stdout + r.stderr)
             raise RuntimeError(f"nvcc failed on {src}")

@@ -115,7 +115,9 @@ struct Batch {
   std::vector<int2> ranges;
   std::vector<ScanItem> items;
   long long pool_elems = 0;  // sdem / cv pool elements
-  int lmax = 0;
+  int lmax = 0;      // longest row scan2 scans
+  int lmax_all = 0;  // longest row incl. long rows
+  int n_long = 0;    // items [0, n_long): rows longer than scan2's slots (fixup only)
   bool fused = false;  // relocation fused into scan2's row loader
   bool any_capped = false;  // some item row is longer than its sector's distance cap + 1
   unsigned fix_cap = 0;
@@ -131,15 +133,24 @@ struct Plans {
   std::vector<std::unique_ptr<Batch>> batches;
 };
 
-// Target-lockstep scan (scan2.cu) unless disabled with SKS_SCAN=1 or the rows
-// are too long for its shared-memory slots.
-int scan2_slots_for(int lmax) {
-  static const bool off = [] {
-    const char* s = std::getenv("SKS_SCAN");
-    return s != nullptr && std::atoi(s) == 1;
-  }();
-  return off ? 0 : scan2_slots(lmax);
+// Rows longer than this go through the fixup kernel whole (every POV, both
+// directions) instead of scan2: scan2's shared-memory slots hold rows up to
+// scan2_max_row() cells. SKS_LONG_ROW lowers the limit (tests exercise the
+// long-row path at small sizes with it); read when a batch is built.
+int long_row_limit() {
+  int lim = scan2_max_row();
+  if (const char* s = std::getenv("SKS_LONG_ROW")) {
+    const int v = std::atoi(s);
+    if (v >= 2) lim = std::min(lim, v);
+  }
+  return lim;
 }
+
+// The ring sums are exact int32s: a POV's cv is at most L^2 - 1 (forward +
+// backward over a row of L cells), and the fixup queue counts pack two 16-bit
+// halves, so rows are limited to 46340 cells (a DEM side of 46340 cells:
+// 8.6 GB of f32 elevations).
+constexpr int kMaxRow = 46340;
 
 // Relocation fused into scan2's row loader: opt-in with
 // SKS_FUSED=1, read when a batch is built. Measured on config 2 it removes
@@ -203,7 +214,7 @@ std::unique_ptr<Batch> make_batch(const std::vector<SectorPlanH>& plans,
         // loader, which zeroes their cv range; dropped below otherwise
         b->items.push_back(ScanItem{static_cast<int>(s), q});
         if (L >= 2 && p.max_dd > 0) {
-          b->lmax = std::max(b->lmax, L);
+          b->lmax_all = std::max(b->lmax_all, L);
           b->target_evals += row_target_evals(L, p.max_dd);
         }
       }
@@ -213,27 +224,49 @@ std::unique_ptr<Batch> make_batch(const std::vector<SectorPlanH>& plans,
     b->sdev.push_back(d);
   }
   b->pool_elems = off;
-  b->fused = fused_relocation() && scan2_slots_for(b->lmax) > 0;
+  if (b->lmax_all > kMaxRow) {
+    std::ostringstream os;
+    os << "grid too large: skewed rows of " << b->lmax_all << " cells exceed the " << kMaxRow
+       << "-cell limit of the exact int32 ring sums";
+    throw std::invalid_argument(os.str());
+  }
+  const int limit = long_row_limit();
+  auto item_len = [&](const ScanItem& it) {
+    const int2 r = b->ranges[b->sdev[it.s].row_off + it.q];
+    return r.y - r.x;
+  };
+  bool any_long = false;
+  for (const ScanItem& it : b->items) any_long |= item_len(it) > limit;
+  // the fused loader builds the rows scan2 reads; long rows are not scanned
+  b->fused = fused_relocation() && !any_long;
   if (!b->fused) {
     std::erase_if(b->items, [&](const ScanItem& it) {
       const int2 r = b->ranges[b->sdev[it.s].row_off + it.q];
       return r.y - r.x < 2 || b->sdev[it.s].max_dd <= 0;
     });
   }
-  // longest rows first (load balance of the persistent scan)
+  // longest rows first (load balance of the persistent scan; long rows, the
+  // fixup-only items, therefore come first: items [0, n_long))
   std::stable_sort(b->items.begin(), b->items.end(), [&](const ScanItem& x, const ScanItem& y) {
     const int2 rx = b->ranges[b->sdev[x.s].row_off + x.q];
     const int2 ry = b->ranges[b->sdev[y.s].row_off + y.q];
     return (rx.y - rx.x) > (ry.y - ry.x);
   });
+  for (const ScanItem& it : b->items) {
+    const int L = item_len(it);
+    if (L > limit) ++b->n_long; else if (L >= 2 && b->sdev[it.s].max_dd > 0) b->lmax = std::max(b->lmax, L);
+  }
   // fixup queue segments, in item order: one entry per POV and direction,
   // the exact bound
   b->fix_off.resize(b->items.size());
+  long long fix_total = 0;
   for (size_t i = 0; i < b->items.size(); ++i) {
     const int2 r = b->ranges[b->sdev[b->items[i].s].row_off + b->items[i].q];
-    b->fix_off[i] = b->fix_cap;
-    b->fix_cap += 2u * static_cast<unsigned>(r.y - r.x);
+    b->fix_off[i] = static_cast<unsigned>(fix_total);
+    fix_total += 2LL * (r.y - r.x);
   }
+  if (fix_total >= (1LL << 32)) throw std::runtime_error("fixup queue of one batch exceeds 2^32 entries");
+  b->fix_cap = static_cast<unsigned>(fix_total);
   b->tiles_x = (max_cols + relocate_tile_cols() - 1) / relocate_tile_cols();
   // tile rows from each sector's first owned tile row to its last owned row
   int tq_max = 0;
@@ -260,23 +293,37 @@ std::unique_ptr<Batch> make_batch(const std::vector<SectorPlanH>& plans,
   return b;
 }
 
-// Split plans (ascending k) into batches under the memory budget.
+// Device bytes one sector adds to a batch, from the formulas ensure_pools
+// and make_batch size the buffers with: sdem f32 + cv i32 per pool element,
+// window maxima (one f32 per 16 pool elements), the fixup queue (2 u32
+// entries per covered cell: one per POV and direction) and per-row metadata
+// (range, item, fix_off, fix_cnt, prefix).
+long long sector_batch_bytes(const SectorPlanH& p) {
+  const long long pool = static_cast<long long>(p.skw_rows) * round_up(p.cols, 32);
+  const long long cells = static_cast<long long>(p.rows) * p.cols;
+  return pool * 8 + (pool / 16) * 4 + cells * 8 + static_cast<long long>(p.skw_rows) * 28 +
+         static_cast<long long>(p.cols) * 16;
+}
+
+// Split plans (ascending k) into batches under the memory budget (and under
+// 2^31 fixup queue entries per batch: the queue offsets are 32-bit).
 void make_batches(Plans& P, int device) {
   const long long budget = batch_budget_bytes();
   std::vector<int> cur;
-  long long cur_bytes = 0;
+  long long cur_bytes = 0, cur_queue = 0;
   for (int s = 0; s < static_cast<int>(P.plans.size()); ++s) {
     const SectorPlanH& p = P.plans[s];
-    // sdem f32 + cv i32 + fixup queue (<= 2 entries of 8 B per 4 POVs)
-    long long bytes = static_cast<long long>(p.skw_rows) * round_up(p.cols, 32) * 8LL +
-                      static_cast<long long>(p.rows) * p.cols * 4LL + 64LL * p.skw_rows;
-    if (!cur.empty() && cur_bytes + bytes > budget) {
+    const long long bytes = sector_batch_bytes(p);
+    const long long queue = 2LL * p.rows * p.cols;
+    if (!cur.empty() && (cur_bytes + bytes > budget || cur_queue + queue >= (1LL << 31))) {
       P.batches.push_back(make_batch(P.plans, cur, device));
       cur.clear();
       cur_bytes = 0;
+      cur_queue = 0;
     }
     cur.push_back(s);
     cur_bytes += bytes;
+    cur_queue += queue;
   }
   if (!cur.empty()) P.batches.push_back(make_batch(P.plans, cur, device));
 }
@@ -297,7 +344,8 @@ struct sks_context {
            std::unique_ptr<Plans>>
       cache;
   // work buffers
-  DevBuf sdem, cv, cvb, queue, fixcnt, fixoff, wm16, counters, dem, map, vis, check;
+  DevBuf sdem, cv, cvb, queue, fixcnt, fixoff, wm16, counters, dem, map, vis, check, ivt;
+  int ivt_len = 0;  // entries of the global fl(1/d) table computed so far
   unsigned long long* h_check = nullptr;  // pinned: device DEM scan result
   cudaEvent_t ev[8] = {};
   long long launches = 0;
@@ -350,19 +398,35 @@ struct sks_context {
     counters.ensure(kCounterBytes, device);
   }
 
-  ScanArgs scan_args(const Batch& b, const BatchDev& bd, double h0) {
+  // Global fl(1/d) table for batches whose longest row exceeds the fixup's
+  // shared-memory table (long rows); nullptr otherwise.
+  const float* ivt_for(const Batch& b, cudaStream_t st) {
+    const int need = round_up(std::max(b.lmax_all, b.lmax) + 1, 32);
+    if (need <= fixup_smem_table_max()) return nullptr;
+    if (need > ivt_len) {
+      ivt.ensure(static_cast<size_t>(need) * sizeof(float), device);
+      cuda_check(launch_ivt_table(ivt.as<float>(), need, st), "launch ivt table");
+      ++launches;
+      ivt_len = need;
+    }
+    return ivt.as<float>();
+  }
+
+  ScanArgs scan_args(const Batch& b, const BatchDev& bd, double h0, cudaStream_t st) {
     ScanArgs a{};
     a.b = bd;
     a.items = b.d_items.as<ScanItem>();
     a.n_items = static_cast<int>(b.items.size());
     a.lmax = std::max(b.lmax, 4);
+    a.lmax_all = std::max(b.lmax_all, a.lmax);
+    a.ivt = ivt_for(b, st);
     a.item_counter = counters.as<unsigned>();
     a.fix_queue = queue.as<unsigned>();
     a.fix_off = b.d_fix_off.as<unsigned>();
     a.fix_cnt = fixcnt.as<unsigned>();
     a.fix_count = counters.as<unsigned>() + 1;
     a.fix_item_counter = counters.as<unsigned>() + 4;
-    a.wm16 = scan2_slots_for(std::max(b.lmax, 4)) > 0 ? wm16.as<float>() : nullptr;
+    a.wm16 = wm16.as<float>();
     a.skipped = reinterpret_cast<unsigned long long*>(counters.as<unsigned>() + 8);
     a.h0 = h0;
     a.dbg_j0 = -1;
@@ -370,7 +434,7 @@ struct sks_context {
     a.dbg_vis_fwd = nullptr;
     a.dbg_vis_bwd = nullptr;
     a.force_exact = 0;
-    a.fix_group = scan2_slots_for(a.lmax) > 0 ? 1 : 4;  // POVs per fixup entry
+    a.fix_group = 1;  // one POV per fixup entry
     a.any_capped = b.any_capped ? 1 : 0;
     return a;
   }
@@ -392,16 +456,18 @@ struct sks_context {
     if (!b.items.empty()) {
       cuda_check(cudaMemsetAsync(fixcnt.p, 0, b.items.size() * sizeof(unsigned), st), "memset fix_cnt");
     }
-    if (a.n_items > 0) {
-      const int nslots = scan2_slots_for(a.lmax);
-      if (nslots > 0) {
-        cuda_check(launch_scan2(a, nslots, st), "launch scan2");
-      } else {
-        int grid = 0;
-        cuda_check(scan_occupancy(a.lmax, &grid), "scan occupancy");
-        grid = std::min(grid, std::max(1, a.n_items));
-        cuda_check(launch_scan(a, grid, st), "launch scan");
-      }
+    if (b.n_long > 0) {
+      cuda_check(launch_long_rows(a, b.n_long, st), "launch long rows");
+      ++launches;
+    }
+    if (a.n_items > b.n_long) {
+      // scan2 sees only the rows that fit its slots (items [n_long, n_items))
+      ScanArgs s2 = a;
+      s2.items += b.n_long;
+      s2.n_items -= b.n_long;
+      s2.fix_off += b.n_long;
+      s2.fix_cnt += b.n_long;
+      cuda_check(launch_scan2(s2, scan2_slots(s2.lmax), st), "launch scan2");
       ++launches;
     }
   }
@@ -489,7 +555,7 @@ void run_sectors(sks_context* ctx, const float* d_dem, int dimy, int dimx, doubl
     BatchDev bd = ctx->batch_dev(b, false);
     const bool fused = b.fused;  // relocation inside scan2's row loader
     if (fused) bd.dem = d_dem;
-    ScanArgs a = ctx->scan_args(b, bd, cfg->h0);
+    ScanArgs a = ctx->scan_args(b, bd, cfg->h0, st);
     a.force_exact = force_exact ? 1 : 0;
     if (stats) cuda_check(cudaEventRecord(ctx->ev[0], st), "event");
     if (!fused) {
@@ -652,7 +718,9 @@ extern "C" {
 
 const char* sks_last_error(void) { return g_error.c_str(); }
 
-const char* sks_version(void) { return "skewshed_b200 0.1.0 (sm_100a)"; }
+const char* sks_version(void) { return "skewshed_b200 0.2.0 (sm_100a)"; }
+
+int sks_scan_row_limit(void) { return scan2_max_row(); }
 
 int sks_device_count(void) {
   int n = 0;
@@ -972,7 +1040,7 @@ void debug_scan(sks_context* ctx, const float* values, const int* ranges, int sk
                                sizeof(float) * cols, skw_rows, cudaMemcpyHostToDevice, st),
              "H2D sdem");
   BatchDev bd = ctx->batch_dev(*b, true);
-  ScanArgs a = ctx->scan_args(*b, bd, h0);
+  ScanArgs a = ctx->scan_args(*b, bd, h0, st);
   uint8_t* dvis = nullptr;
   if (dbg_j0 >= 0) {
     a.dbg_j0 = dbg_j0;

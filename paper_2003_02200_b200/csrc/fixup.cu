@@ -333,14 +333,19 @@ __global__ void __launch_bounds__(kPrefixThreads) fixup_prefix_write_kernel(Scan
 // One thread per queued POV (flat list over all rows, in row order, so
 // neighbouring threads share rows): the POV's row is found by a binary search
 // of the prefix, then the POV is re-run exactly (exact_pov). Rows are read
-// through L1/L2; the fl(1/d) table sits in shared memory.
+// through L1/L2; the fl(1/d) table sits in shared memory (kSmemTab), or in
+// global memory for batches with rows too long for it (long rows).
 #ifndef SKS_FIX_MINB
 #define SKS_FIX_MINB 3  // 24 warps per SM (80 registers): the kernel is latency-bound
 #endif
+template <bool kSmemTab>
 __global__ void __launch_bounds__(kWarps * 32, SKS_FIX_MINB) fixup_kernel(ScanArgs a, int tab_len, const unsigned* off) {
-  extern __shared__ __align__(16) float ivt[];  // fl(1/d), d = 0 .. tab_len - 1
-  for (int d = threadIdx.x; d < tab_len; d += blockDim.x) ivt[d] = __frcp_rn(static_cast<float>(d));
-  __syncthreads();
+  extern __shared__ __align__(16) float ivt_s[];  // fl(1/d), d = 0 .. tab_len - 1
+  if (kSmemTab) {
+    for (int d = threadIdx.x; d < tab_len; d += blockDim.x) ivt_s[d] = __frcp_rn(static_cast<float>(d));
+    __syncthreads();
+  }
+  const float* ivt = kSmemTab ? ivt_s : a.ivt;
   const unsigned grp = static_cast<unsigned>(a.fix_group);
   const unsigned total = off[a.n_items];
   const unsigned stride = gridDim.x * blockDim.x;
@@ -381,6 +386,46 @@ __global__ void __launch_bounds__(kWarps * 32, SKS_FIX_MINB) fixup_kernel(ScanAr
   }
 }
 
+// Long rows (items [0, n_long)): one CTA per row writes the row's 16-cell
+// window maxima (what scan2's row loader writes for the rows it scans) and
+// queues every POV in both directions (forward entries y = 0 .. L-1 at the
+// segment start, backward ones from slot L, as scan2 queues flagged POVs).
+__global__ void __launch_bounds__(256) long_rows_kernel(ScanArgs a) {
+  const int it = blockIdx.x;
+  const ScanItem item = a.items[it];
+  const SectorDev& sd = a.b.sectors[item.s];
+  const int2 rg = a.b.ranges[sd.row_off + item.q];
+  const int L = rg.y - rg.x;
+  const long long rowoff = sd.sdem_off + static_cast<long long>(item.q) * sd.pitch;
+  const float* row = a.b.sdem + rowoff + rg.x;
+  float* wm = a.wm16 + rowoff / 16;
+  for (int w = threadIdx.x; 16 * w < L; w += blockDim.x) {
+    float m = -INFINITY;
+#pragma unroll
+    for (int u = 0; u < 16; ++u) {
+      if (16 * w + u < L) m = fmaxf(m, __ldg(row + 16 * w + u));
+    }
+    wm[w] = m;
+  }
+  unsigned* q = a.fix_queue + a.fix_off[it];
+  for (int y = threadIdx.x; y < L; y += blockDim.x) {
+    q[y] = pack_fix(0u, static_cast<unsigned>(y));
+    q[L + y] = pack_fix(1u, static_cast<unsigned>(y));
+  }
+  if (threadIdx.x == 0) {
+    a.fix_cnt[it] = static_cast<unsigned>(L) | (static_cast<unsigned>(L) << 16);
+    atomicAdd(a.fix_count, 2u * static_cast<unsigned>(L));
+  }
+}
+
+__global__ void ivt_table_kernel(float* ivt, int n) {
+  const int d = blockIdx.x * blockDim.x + threadIdx.x;
+  if (d < n) ivt[d] = __frcp_rn(static_cast<float>(d));
+}
+
+// fl(1/d) tables up to this many entries live in shared memory (64 KB)
+constexpr int kSmemTabMax = 16384;
+
 }  // namespace
 
 int launch_fixup(const ScanArgs& a, unsigned* off, void* stream) {
@@ -397,18 +442,38 @@ int launch_fixup(const ScanArgs& a, unsigned* off, void* stream) {
     fixup_prefix_sums_kernel<<<nb, kPrefixThreads, 0, static_cast<cudaStream_t>(stream)>>>(a, chunk, bsum);
     fixup_prefix_write_kernel<<<nb, kPrefixThreads, 0, static_cast<cudaStream_t>(stream)>>>(a, chunk, bsum, off);
   }
-  const int tab_len = ((a.lmax + 31) / 32) * 32;
-  const size_t smem = static_cast<size_t>(tab_len) * sizeof(float);
-  if (smem > 200 * 1024) return static_cast<int>(cudaErrorInvalidValue);  // rows beyond 51200 cells
-  cudaError_t e = cudaFuncSetAttribute(fixup_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                       static_cast<int>(smem));
-  if (e != cudaSuccess) return static_cast<int>(e);
-  int per_sm = 0;
-  e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fixup_kernel, kWarps * 32, smem);
-  if (e != cudaSuccess) return static_cast<int>(e);
-  fixup_kernel<<<sms * (per_sm > 0 ? per_sm : 1), kWarps * 32, smem, static_cast<cudaStream_t>(stream)>>>(
-      a, tab_len, off);
+  const int tab_len = ((std::max(a.lmax_all, a.lmax) + 31) / 32) * 32;
+  const cudaStream_t st = static_cast<cudaStream_t>(stream);
+  if (tab_len <= kSmemTabMax) {
+    const size_t smem = static_cast<size_t>(tab_len) * sizeof(float);
+    cudaError_t e = cudaFuncSetAttribute(fixup_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         static_cast<int>(smem));
+    if (e != cudaSuccess) return static_cast<int>(e);
+    int per_sm = 0;
+    e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fixup_kernel<true>, kWarps * 32, smem);
+    if (e != cudaSuccess) return static_cast<int>(e);
+    fixup_kernel<true><<<sms * (per_sm > 0 ? per_sm : 1), kWarps * 32, smem, st>>>(a, tab_len, off);
+  } else {
+    if (a.ivt == nullptr) return static_cast<int>(cudaErrorInvalidValue);
+    int per_sm = 0;
+    cudaError_t e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fixup_kernel<false>, kWarps * 32, 0);
+    if (e != cudaSuccess) return static_cast<int>(e);
+    fixup_kernel<false><<<sms * (per_sm > 0 ? per_sm : 1), kWarps * 32, 0, st>>>(a, tab_len, off);
+  }
   return static_cast<int>(cudaGetLastError());
 }
+
+int launch_long_rows(const ScanArgs& a, int n_long, void* stream) {
+  if (n_long <= 0) return 0;
+  long_rows_kernel<<<n_long, 256, 0, static_cast<cudaStream_t>(stream)>>>(a);
+  return static_cast<int>(cudaGetLastError());
+}
+
+int launch_ivt_table(float* ivt, int n, void* stream) {
+  ivt_table_kernel<<<(n + 255) / 256, 256, 0, static_cast<cudaStream_t>(stream)>>>(ivt, n);
+  return static_cast<int>(cudaGetLastError());
+}
+
+int fixup_smem_table_max() { return kSmemTabMax; }
 
 }  // namespace sks

@@ -1,7 +1,7 @@
 // Line-of-sight scan, target-lockstep mapping (sm_100a) — the production scan.
 //
 // Replaces sector_viewshed / linear_viewshed_row (reference scan.cpp:8-85),
-// with the same certified FP32 filter and FP64 fixup as scan.cu (DESIGN.md
+// with a certified FP32 filter and an exact FP64 fixup (DESIGN.md
 // §3.2): per target t = fl(fl(fl(e - hf) - hl) * fl(1/dd)), band
 // [lo, hi] = t_r -+ 10u|t_r| around the last record; t > hi is a record
 // (visible), t < lo hidden, anything else flags the POV for the exact
@@ -777,9 +777,9 @@ __global__ void __launch_bounds__(kThr, 1) scan2_kernel(const __grid_constant__ 
 }  // namespace
 
 // Table copies and slots that fit the opt-in shared memory for rows up to
-// lmax: 4 copies with >= 2 slots (rows up to ~5 800 cells), else 2 copies
-// with >= 1 slot (rows up to ~13 000 cells); 0 slots: use the
-// distance-lockstep kernel of scan.cu instead.
+// lmax: 2 copies (4 with -DSKS_PREFER_NC4 where >= 2 slots fit) with >= 1
+// slot; 0 slots: the rows are too long for shared memory and go through the
+// fixup kernel whole (long rows, engine.cu).
 static void scan2_config(int lmax, int* copies, int* slots) {
   *copies = 0;
   *slots = 0;
@@ -806,6 +806,18 @@ int scan2_slots(int lmax) {
   int c = 0, n = 0;
   scan2_config(lmax, &c, &n);
   return n;
+}
+
+int scan2_max_row() {
+  static const int m = [] {
+    int lo = 4, hi = 32768;  // scan2_slots(lo) >= 1, scan2_slots(hi) == 0
+    while (hi - lo > 1) {
+      const int mid = (lo + hi) / 2;
+      if (scan2_slots(mid) >= 1) lo = mid; else hi = mid;
+    }
+    return lo;
+  }();
+  return m;
 }
 
 size_t scan2_smem_bytes(int lmax, int nslots) {

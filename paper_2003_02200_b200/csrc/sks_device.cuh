@@ -86,7 +86,14 @@ struct ScanArgs {
   uint8_t* dbg_vis_bwd;
   int force_exact;        // every POV group goes through the FP64 fixup
   int any_capped;         // some row's distance cap is shorter than the row
-  int fix_group;          // POVs per fixup entry: 1 (scan2_kernel) or 4 (scan_kernel)
+  int fix_group;          // POVs per fixup entry (1: an entry is one POV)
+  // Rows too long for scan2's shared-memory slots ("long rows", items
+  // [0, n_long) of the fixup's item list): every POV of such a row, both
+  // directions, goes through the fixup kernel (long_rows_kernel fills their
+  // queue segments and window maxima).
+  int lmax_all;           // longest row of the batch incl. long rows (fixup table)
+  const float* ivt;       // global fl(1/d) table (lmax_all + 32 entries) when the
+                          // fixup's shared-memory table would not fit; else nullptr
 };
 
 __host__ __device__ inline unsigned pack_fix(unsigned dir, unsigned g) { return (dir << 31) | g; }
@@ -97,12 +104,14 @@ int launch_relocate_grid(const float* dem, const BatchDev& b, int tiles_x,
                          int tiles_total, void* stream);
 int relocate_tile_rows();
 int relocate_tile_cols();
-size_t scan_smem_bytes(int lmax, bool shifted);
-int scan_block_threads(int lmax);
-int launch_scan(const ScanArgs& a, int grid, void* stream);
-int scan_occupancy(int lmax, int* grid_out);
 int launch_fixup(const ScanArgs& a, unsigned* off, void* stream);  // fixup.cu (off: n_items + 1)
+// Queue every POV (both directions) of items [0, n_long) for the fixup and
+// write their rows' window maxima (fixup.cu).
+int launch_long_rows(const ScanArgs& a, int n_long, void* stream);
+int launch_ivt_table(float* ivt, int n, void* stream);  // ivt[d] = fl(1/d)
+int fixup_smem_table_max();  // longest row whose fl(1/d) table the fixup keeps in shared memory
 int scan2_slots(int lmax);  // 0: rows too long for the target-lockstep kernel
+int scan2_max_row();        // longest row scan2 can hold (>= 1 slot)
 size_t scan2_smem_bytes(int lmax, int nslots);
 int launch_scan2(const ScanArgs& a, int nslots, void* stream);
 int launch_unskew(const BatchDev& b, const float* unused, double* map,

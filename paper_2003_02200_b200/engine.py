@@ -459,6 +459,12 @@ def device_count() -> int:
     return int(lib.sks_device_count())
 
 
+def scan_row_limit() -> int:
+    """Longest skewed row the shared-memory scan holds (longer rows run POV by
+    POV through the exact kernel)."""
+    return int(lib.sks_scan_row_limit())
+
+
 # ---- ESRI ASCII grid I/O (ascii_grid.hpp:15-31) ----------------------------
 
 GridFormatError = _lib.GridFormatError
