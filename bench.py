@@ -165,67 +165,138 @@ def make_dem(cfgid, terrain):
     return sk.make_synthetic(kind, n, n, CELLSIZE, SEED).values
 
 
-# ---- CPU baseline: the reference itself (oracle/_ref) ------------------------------
+def parallelism(world):
+    return (f"row-block sharded x{world} (every sector), NCCL reduce of f64 maps" if world > 1
+            else "single GPU, all sectors")
 
-def cpu_reference_sample(dem, ns, max_distance, budget_s, threads):
-    """Times the reference's own per-sector pipeline (plan_sector ->
-    apply_pre_ops -> build_skw -> linear_viewshed_row both directions for every
-    POV of the sampled rows) on `threads` host threads; returns the projected
-    POV-sector/s of the full workload (exact work model)."""
+
+def bench_config(cfgid, terrain, world):
+    """The workload description; identical in both arms."""
+    c = CONFIGS[cfgid]
+    return {"workload": workload_name(cfgid, terrain), "dimy": c["n"], "dimx": c["n"], "ns": c["ns"], "h0": H0,
+            "max_distance": c["max_distance"], "terrain": terrain, "cellsize": CELLSIZE,
+            "l2": "GPU arm: flushed between timed steps (256 MiB device write, untimed)",
+            "parallelism": parallelism(world)}
+
+
+# ---- the reference on the host (oracle/_ref: the unmodified reference sources) ------
+# Nothing below imports the product package: the DEM comes from the shim
+# (ref_make_fractal, or the reference's own make_synthetic for SmoothedNoise).
+
+def _ref():
     sys.path.insert(0, os.path.join(ROOT, "tests"))
     from _oracle import Ref, have_ref
-
-    import paper_2003_02200_b200 as sk
     if not have_ref():
         raise RuntimeError("oracle/_ref/libskewshed_ref.so missing (build() it where /root/reference exists)")
-    ref = Ref()
-    n = dem.shape[0]
-    total = sk.total_target_evals(ns, n, n, CELLSIZE, max_distance)
-    half = ns // 2
-    sectors = sorted(set(int(round(x)) for x in np.linspace(0, half - 1, min(9, half))))
-    # calibrate the row stride to the time budget
-    stride, offset = 97, 13
-    evals, secs = ref.sample_scan(dem, ns, H0, max_distance, CELLSIZE, sectors, stride, offset, threads)
-    rate = evals / max(secs, 1e-9)
-    want = rate * budget_s
-    per_stride = evals * stride
-    stride = max(1, int(per_stride / max(want, 1.0)))
-    evals, secs = ref.sample_scan(dem, ns, H0, max_distance, CELLSIZE, sectors, stride, 7, threads)
-    rate = evals / max(secs, 1e-9)
-    wall = total / rate
-    value = n * n * half / wall
-    sample = (f"reference scan of every POV (both directions) on every {stride}th skewed row of sectors "
-              f"{sectors} ({evals:.3g} target evals in {secs:.1f} s on {threads} threads); projected to the "
-              f"full workload's {total:.4g} target evals (scan = 99.3% of reference time, SURVEY §6)")
-    return value, wall, rate, sample
+    return Ref()
+
+
+def ref_dem(ref, cfgid, terrain):
+    n = CONFIGS[cfgid]["n"]
+    if terrain == "fractal":
+        return ref.make_fractal(n, n, SEED)
+    out = np.empty((n, n), np.float32)
+    ref._check(ref.lib.ref_make_synthetic(3, n, n, CELLSIZE, SEED, out))  # SyntheticKind::SmoothedNoise
+    return out
+
+
+def stratified_sectors(half, count, phase=0.0):
+    """`count` sector indices spread evenly over [0, half) (costs vary with the
+    shear angle, so a sample must span all of them)."""
+    count = min(count, half)
+    return sorted({int((t + phase) * half / count) % half for t in range(count)})
+
+
+def cpu_sweep_sample(ref, dem, cfgid, threads, per_thread=2, phase=0.0):
+    """The reference's public sector_sweep on a stratified sample of
+    per_thread x threads sectors, claimed dynamically by `threads` host threads
+    (as total_viewshed's workers claim them). Returns (POV-sector/s, seconds,
+    sectors); the rate is measured directly (sample POV-sectors / wall)."""
+    c = CONFIGS[cfgid]
+    n, half = c["n"], c["ns"] // 2
+    ks = stratified_sectors(half, per_thread * threads, phase)
+    secs = ref.sweep_sample(dem, CELLSIZE, c["ns"], H0, c["max_distance"], ks, threads)
+    return n * n * len(ks) / secs, secs, ks
+
+
+def cpu_baseline_main(args):
+    """--cpu-baseline-only: runs in a subprocess of the GPU arm, so the GPU
+    arm's process never maps oracle code."""
+    ref = _ref()
+    threads = os.cpu_count() or 1
+    dem = ref_dem(ref, args.config, args.terrain)
+    value, secs, ks = cpu_sweep_sample(ref, dem, args.config, threads)
+    print(json.dumps({"value": value, "unit": UNIT, "cores": threads, "kind": "reference",
+                      "sample": (f"the reference's sector_sweep (engine.cpp:235-244: relocation, scan, unskew) "
+                                 f"on {len(ks)} stratified sectors {ks} of the same workload, {threads} host threads "
+                                 f"claiming sectors dynamically, {secs:.1f} s wall; value = sample POV-sectors / wall "
+                                 f"(no extrapolation)")}), flush=True)
 
 
 def run_reference(args, world, rank):
+    """--impl reference: the reference's own stock code path on the host
+    cores, rank 0 only. Configs 1-3: the stock total_viewshed (engine.cpp:
+    222-233, workers = all host threads) over the WHOLE workload, timed in full
+    as many times as fit the time budget (at least once). Configs 4-5 (hours
+    of CPU): stratified sector_sweep samples, projected with the exact scan
+    work from the reference's own row ranges."""
     if rank != 0:
         return
     cfgid = args.config
     c = CONFIGS[cfgid]
-    dem = make_dem(cfgid, args.terrain)
+    n, ns, half = c["n"], c["ns"], c["ns"] // 2
+    ref = _ref()
+    dem = ref_dem(ref, cfgid, args.terrain)
     threads = os.cpu_count() or 1
-    budget = max(2.0, min(20.0, 150.0 / (args.steps + args.warmup)))
-    vals = []
+    povs = n * n * half
     walls = []
-    sample = ""
-    for i in range(args.warmup + args.steps):
-        v, wall, _rate, sample = cpu_reference_sample(dem, c["ns"], c["max_distance"], budget, threads)
-        if i >= args.warmup:
-            vals.append(v)
-            walls.append(wall)
-    value = float(np.median(vals))
+    t_start = time.perf_counter()
+    if cfgid <= 3:
+        out = np.empty((n, n), np.float64)
+        stats = np.zeros(5, np.float64)
+        while True:
+            t0 = time.perf_counter()
+            ref._check(ref.lib.ref_total_viewshed(dem, n, n, CELLSIZE, ns, H0, threads, c["max_distance"] or 0.0,
+                                                  1, 0, out, stats.ctypes.data))
+            walls.append(time.perf_counter() - t0)
+            elapsed = time.perf_counter() - t_start
+            if len(walls) >= args.steps or elapsed + walls[-1] > args.ref_budget:
+                break
+        wall = float(np.mean(walls))
+        value = povs / wall
+        sample = (f"the stock total_viewshed (engine.cpp:222-233) on the whole workload, workers = {threads} "
+                  f"host threads; {len(walls)} full run(s) timed ({', '.join(f'{w:.1f}' for w in walls)} s), "
+                  f"value = {povs} POV-sectors / mean wall")
+        kind_steps = len(walls)
+    else:
+        work = [ref.sector_work(n, n, CELLSIZE, ns, k, c["max_distance"]) for k in range(half)]
+        total = float(sum(work))
+        rates = []
+        while True:
+            ks = stratified_sectors(half, threads, phase=len(walls) / max(args.steps, 1))
+            secs = ref.sweep_sample(dem, CELLSIZE, ns, H0, c["max_distance"], ks, threads)
+            walls.append(secs)
+            rates.append(sum(work[k] for k in ks) / secs)
+            elapsed = time.perf_counter() - t_start
+            if len(walls) >= args.steps or elapsed + walls[-1] > args.ref_budget:
+                break
+        wall = total / float(np.mean(rates))  # projected whole-workload wall
+        value = povs / wall
+        sample = (f"the reference's sector_sweep (engine.cpp:235-244) on {len(walls)} stratified samples of "
+                  f"{threads} sectors ({threads} host threads); whole-workload wall projected from the exact "
+                  f"scan work of every sector (the reference's own build_skw row ranges; scan = 99.3% of its "
+                  f"time, SURVEY 6): {wall:.0f} s")
+        kind_steps = len(walls)
     line = {
         "impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": args.gpus,
-        "steps": args.steps, "warmup": args.warmup, "ms_per_step": float(np.median(walls)) * 1e3,
-        "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
-        "data": "synthetic", "config": {"workload": workload_name(cfgid, args.terrain), "dimy": c["n"],
-                                        "dimx": c["n"], "ns": c["ns"], "h0": H0,
-                                        "max_distance": c["max_distance"], "terrain": args.terrain},
-        "cpu_baseline": {"value": value, "unit": UNIT, "cores": threads, "kind": "reference",
-                         "sample": sample},
+        "steps": kind_steps, "warmup": 0, "steps_requested": args.steps, "warmup_requested": args.warmup,
+        "steps_note": ("each step is one full stock run of the workload (a CPU needs no warm-up); as many as "
+                       f"fit the {args.ref_budget:.0f} s budget" if cfgid <= 3 else
+                       f"each step is one sector sample; as many as fit the {args.ref_budget:.0f} s budget"),
+        "ms_per_step": float(np.mean(walls)) * 1e3, "higher_is_better": True, "scaling": "strong",
+        "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "config": bench_config(cfgid, args.terrain, world),
+        "cpu_baseline": {"value": value, "unit": UNIT, "cores": threads, "kind": "reference", "sample": sample},
         "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
     print(json.dumps(line), flush=True)
@@ -331,6 +402,18 @@ def run_ours(args, world, rank, local):
     # the map inside every timed step)
     pinned_dem = torch.from_numpy(dem).pin_memory()
     pinned_out = torch.empty((n, n), dtype=torch.float64).pin_memory()
+    # cold: a fresh context's first call (host plans, batch metadata uploads,
+    # device buffer allocation, the run, the copies), once, reported beside
+    # the warm e2e
+    cold_s = None
+    if world == 1:
+        cold = sk.Context(local)
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        cold.total_viewshed(pinned_dem.numpy(), CELLSIZE, cfg, out=pinned_out.numpy())
+        cold_s = time.perf_counter() - t0
+        cold.close()
+        del cold
     e2e_times = []
     for i in range(args.warmup + args.steps):
         barrier(world)
@@ -373,11 +456,7 @@ def run_ours(args, world, rank, local):
         "dtype_note": "certified f32 filter for the line-of-sight decisions, f64 for every uncertain decision "
                       "(the reference's own operations) and for the accumulated map; integer ring sums",
         "data": "synthetic",
-        "config": {"workload": workload_name(cfgid, args.terrain), "dimy": n, "dimx": n, "ns": ns, "h0": H0,
-                   "max_distance": maxd, "terrain": args.terrain, "cellsize": CELLSIZE,
-                   "l2": "flushed between timed steps (256 MiB device write, untimed)",
-                   "parallelism": (f"row-block sharded x{world} (every sector), NCCL reduce of f64 maps" if world > 1
-                                   else "single GPU, all sectors")},
+        "config": bench_config(cfgid, args.terrain, world),
         "row_balance": ({"cuts": [round(float(x), 6) for x in balancer.cuts],
                          "last_warmup_rank_ms": [round(x, 3) for x in rank_ms],
                          "note": "row-block cuts moved from measured per-rank times during warm-up, then frozen"}
@@ -404,15 +483,21 @@ def run_ours(args, world, rank, local):
         "skip_decided_frac": skipped_all / max(evals_all, 1),
         "e2e": {"value": e2e_value, "unit": UNIT, "seconds": e2e_s,
                 "h2d_bytes_per_step": int(n * n * 4 * world), "d2h_bytes_per_step": int(n * n * 8)},
+        "e2e_cold": ({"value": povs / cold_s, "unit": UNIT, "seconds": cold_s,
+                      "note": "a fresh context's first total_viewshed call: host plans, metadata uploads and "
+                              "device allocations included (the warm e2e reuses them)"}
+                     if cold_s else None),
         "gpu_launches": launches_all,
         "clocks": clocks,
     }
     if world == 1 and not args.no_cpu_baseline:
+        # the reference on the host cores, in a subprocess (this process never
+        # maps oracle code); a bounded sample of the same workload
         try:
-            threads = os.cpu_count() or 1
-            v, wall, rate, sample = cpu_reference_sample(dem, ns, maxd, args.cpu_budget, threads)
-            line["cpu_baseline"] = {"value": v, "unit": UNIT, "cores": threads, "kind": "reference",
-                                    "sample": sample, "projected_wall_s": wall}
+            r = subprocess.run([sys.executable, os.path.abspath(__file__), "--cpu-baseline-only", "--config",
+                                str(cfgid), "--terrain", args.terrain], capture_output=True, text=True,
+                               timeout=600)
+            line["cpu_baseline"] = json.loads(r.stdout.strip().splitlines()[-1])
         except Exception as e:  # reported, never fatal
             line["cpu_baseline"] = {"value": None, "unit": UNIT, "cores": None, "kind": "reference",
                                     "sample": f"unavailable: {e}"}
@@ -428,8 +513,13 @@ def main():
     ap.add_argument("--config", type=int, default=2, choices=sorted(CONFIGS))
     ap.add_argument("--terrain", choices=["fractal", "smooth"], default="fractal")
     ap.add_argument("--no-cpu-baseline", action="store_true")
-    ap.add_argument("--cpu-budget", type=float, default=15.0)
+    ap.add_argument("--cpu-baseline-only", action="store_true", help=argparse.SUPPRESS)
+    ap.add_argument("--ref-budget", type=float, default=150.0,
+                    help="seconds of reference runs in --impl reference (at least one full run)")
     args = ap.parse_args()
+    if args.cpu_baseline_only:
+        cpu_baseline_main(args)
+        return
     args.warmup = max(args.warmup, 3) if args.impl == "ours" else args.warmup
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))

@@ -16,7 +16,9 @@
 #include <cstdint>
 #include <cstring>
 #include <exception>
+#include <mutex>
 #include <optional>
+#include <random>
 #include <string>
 #include <thread>
 #include <vector>
@@ -279,81 +281,122 @@ int ref_rotational_total_viewshed(const float* dem, int dimy, int dimx,
   });
 }
 
-// CPU baseline sampler. Runs the reference's own per-sector pipeline
-// (plan_sector -> apply_pre_ops -> build_skw -> linear_viewshed_row for every
-// POV of the sampled skewed rows, both directions) on `threads` host threads
-// and returns the target evaluations done and the wall seconds. Rows are
-// sampled with a stride so the sample is stratified over row lengths; the
-// caller extrapolates with the exact work count of the full workload.
-int ref_sample_scan(const float* dem, int dimy, int dimx, int ns, double h0,
-                    double max_distance, double cellsize, const int* sectors,
-                    int n_sectors,
-                    int row_stride, int row_offset, int threads,
-                    double* target_evals_out, double* seconds_out) {
+// Benchmark input: the fractal terrain of BASELINE config 1-5 (DESIGN.md
+// "Inputs"). The reference has no fractal generator (its kinds are Flat, Ramp,
+// Cone, SmoothedNoise, dem.hpp:60-67), so this is the bench's own definition,
+// restated here so that the reference arm never loads the product library:
+// diamond-square midpoint displacement on the smallest (2^m+1)^2 lattice
+// covering the grid, cropped top-left; raw std::mt19937(seed) words mapped to
+// [-1, 1) as 2*(x/2^32)-1 (as dem.cpp:94-96 maps its draws); corners first at
+// amplitude 300 m, then per level l the diamond step and the square step in
+// row-major order at amplitude 300*2^(-0.8(l+1)); 500 m + lattice as float32.
+// tests/test_oracle.py pins it to the product's generator bit for bit.
+int ref_make_fractal(int dimy, int dimx, uint32_t seed, float* out) {
   return guarded([&] {
-    Dem d = make_dem(dem, dimy, dimx, 10.0);
-    struct Item {
-      int s;
-      int q;
-    };
-    // Relocation is done up front (outside the timed region) because the
-    // scan is >99% of the reference's worker time.
-    std::vector<SkwGrid> skws(n_sectors);
-    std::vector<int> caps(n_sectors, kNoDistanceCap);
-    std::vector<Item> items;
-    for (int s = 0; s < n_sectors; ++s) {
-      SectorPlan p = plan_sector(sectors[s], ns, dimy, dimx);
-      if (max_distance > 0.0) {  // engine.cpp:29-36 distance_cap_cells
-        double step = cellsize * std::sqrt(1.0 + p.shear_tan * p.shear_tan);
-        double cap = std::floor(max_distance / step);
-        caps[s] = cap >= static_cast<double>(kNoDistanceCap)
-                      ? kNoDistanceCap
-                      : std::max(0, static_cast<int>(cap));
-      }
-      Grid<float> pre = apply_pre_ops(d.values, p.pre_ops);
-      skws[s] = build_skw(pre, p.shear_tan);
-      for (int q = row_offset; q < skws[s].skw_rows(); q += row_stride) {
-        auto [f, l] = skws[s].row_ranges[q];
-        if (l > f) items.push_back({s, q});
-      }
+    if (dimy < 2 || dimx < 2) throw std::invalid_argument("synthetic grid dimensions must be >= 2");
+    int m = 0;
+    while ((1 << m) + 1 < std::max(dimy, dimx)) ++m;
+    const int S = (1 << m) + 1;
+    std::vector<double> lat(static_cast<size_t>(S) * S, 0.0);
+    std::mt19937 gen(seed);
+    auto unit = [&] { return 2.0 * (static_cast<double>(gen()) / 4294967296.0) - 1.0; };
+    auto h = [&](int i, int j) -> double& { return lat[static_cast<size_t>(i) * S + j]; };
+    for (auto [ci, cj] : {std::pair{0, 0}, std::pair{0, S - 1}, std::pair{S - 1, 0}, std::pair{S - 1, S - 1}}) {
+      h(ci, cj) = 300.0 * unit();
     }
-    std::atomic<size_t> next{0};
-    std::atomic<long long> evals{0};
-    std::atomic<long long> sink{0};
-    auto worker = [&] {
-      long long local = 0;
-      double acc = 0.0;
-      for (;;) {
-        size_t it = next.fetch_add(1);
-        if (it >= items.size()) break;
-        const SkwGrid& skw = skws[items[it].s];
-        const int max_dd = caps[items[it].s];
-        int q = items[it].q;
-        auto [first, last] = skw.row_ranges[q];
-        std::span<const float> row(skw.values.row(q), skw.cols);
-        for (int j0 = first; j0 < last; ++j0) {
-          double h = row[j0] + h0;
-          acc += linear_viewshed_row(row, first, last, j0, h,
-                                     ScanDir::Forward, max_dd);
-          acc += linear_viewshed_row(row, first, last, j0, h,
-                                     ScanDir::Backward, max_dd);
-          long long fw = std::min<long long>(last - 1 - j0, max_dd);
-          long long bw = std::min<long long>(j0 - first, max_dd);
-          local += fw + bw;
+    for (int l = 0; l < m; ++l) {
+      const int step = 1 << (m - l), half = step / 2;
+      const double amp = 300.0 * std::pow(2.0, -0.8 * (l + 1));
+      for (int i = half; i < S; i += step) {  // diamond: centre of each square
+        for (int j = half; j < S; j += step) {
+          const double corners = h(i - half, j - half) + h(i - half, j + half) + h(i + half, j - half) +
+                                 h(i + half, j + half);
+          h(i, j) = corners / 4.0 + amp * unit();
         }
       }
-      evals += local;
-      sink += static_cast<long long>(acc) & 1;
-    };
-    auto t0 = std::chrono::steady_clock::now();
-    std::vector<std::thread> pool;
-    for (int t = 0; t < std::max(1, threads); ++t) pool.emplace_back(worker);
-    for (auto& t : pool) t.join();
-    *seconds_out = std::chrono::duration<double>(
-                       std::chrono::steady_clock::now() - t0)
-                       .count();
-    *target_evals_out = static_cast<double>(evals.load());
+      for (int i = 0; i < S; i += half) {  // square: edge midpoints, row-major
+        for (int j = ((i / half) % 2 == 0) ? half : 0; j < S; j += step) {
+          double sum = 0.0;
+          int n = 0;
+          if (i >= half) sum += h(i - half, j), ++n;
+          if (i + half < S) sum += h(i + half, j), ++n;
+          if (j >= half) sum += h(i, j - half), ++n;
+          if (j + half < S) sum += h(i, j + half), ++n;
+          h(i, j) = sum / n + amp * unit();
+        }
+      }
+    }
+    for (int i = 0; i < dimy; ++i) {
+      for (int j = 0; j < dimx; ++j) out[static_cast<size_t>(i) * dimx + j] = static_cast<float>(500.0 + h(i, j));
+    }
   });
+}
+
+// CPU baseline sample: the reference's public per-sector entry point
+// sector_sweep (engine.cpp:235-244: plan_sector -> apply_pre_ops ->
+// build_skw -> sector_viewshed -> unskew_accumulate, the same
+// compute_sector the engine's workers run, engine.cpp:45-66) on the listed
+// sectors, claimed dynamically by `threads` host threads as the engine's
+// workers claim them (engine.cpp:150-160). Returns the wall seconds.
+int ref_sweep_sample(const float* dem, int dimy, int dimx, double cellsize, int ns, double h0,
+                     double max_distance, const int* sectors, int n_sectors, int threads,
+                     double* seconds_out) {
+  return guarded([&] {
+    const Dem d = make_dem(dem, dimy, dimx, cellsize);
+    const RunConfig cfg = make_cfg(ns, h0, 1, max_distance, 0);
+    std::atomic<int> next{0};
+    std::atomic<long long> sink{0};
+    std::exception_ptr failure;
+    std::mutex mu;
+    auto worker = [&] {
+      try {
+        for (;;) {
+          const int i = next.fetch_add(1);
+          if (i >= n_sectors) break;
+          SectorResult r = sector_sweep(d, cfg, sectors[i]);
+          sink += static_cast<long long>(r.contribution.data()[0]) & 1;
+        }
+      } catch (...) {
+        std::lock_guard<std::mutex> lk(mu);
+        if (!failure) failure = std::current_exception();
+      }
+    };
+    const auto t0 = std::chrono::steady_clock::now();
+    std::vector<std::thread> pool;
+    for (int t = 0; t < std::max(1, std::min(threads, n_sectors)); ++t) pool.emplace_back(worker);
+    for (auto& t : pool) t.join();
+    *seconds_out = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
+    if (failure) std::rethrow_exception(failure);
+  });
+}
+
+// Exact scan work of sector k (target evaluations: for every full cell of
+// every skewed row, the forward and backward scan lengths, capped by
+// distance_cap_cells, engine.cpp:29-36 / scan.cpp:20-22,37-39), from the
+// reference's own plan_sector and build_skw row ranges (which depend on the
+// geometry only, so a zero grid of the right shape gives them).
+long long ref_sector_work(int dimy, int dimx, double cellsize, int ns, int k, double max_distance) {
+  long long total = -1;
+  guarded([&] {
+    const SectorPlan p = plan_sector(k, ns, dimy, dimx);
+    int max_dd = kNoDistanceCap;
+    if (max_distance > 0.0) {
+      const double step = cellsize * std::sqrt(1.0 + p.shear_tan * p.shear_tan);
+      const double cap = std::floor(max_distance / step);
+      max_dd = cap >= static_cast<double>(kNoDistanceCap) ? kNoDistanceCap : std::max(0, static_cast<int>(cap));
+    }
+    Grid<float> zero;
+    zero.reset(p.rows, p.cols, 0.0f);
+    const SkwGrid skw = build_skw(zero, p.shear_tan);
+    long long w = 0;
+    for (auto [first, last] : skw.row_ranges) {
+      for (int j0 = first; j0 < last; ++j0) {
+        w += std::min<long long>(last - 1 - j0, max_dd) + std::min<long long>(j0 - first, max_dd);
+      }
+    }
+    total = w;
+  });
+  return total;
 }
 
 // read_ascii_grid(istream, source_name) (ascii_grid.cpp:110-196). Returns 0,

@@ -96,9 +96,11 @@ class Ref:
         lib.ref_area_scale_factor.restype = C.c_double
         lib.ref_rotational_total_viewshed.argtypes = [_f32p, C.c_int, C.c_int, C.c_double, C.c_int, C.c_double,
                                                       C.c_double, _f64p]
-        lib.ref_sample_scan.argtypes = [_f32p, C.c_int, C.c_int, C.c_int, C.c_double, C.c_double, C.c_double,
-                                        _i32p, C.c_int, C.c_int, C.c_int, C.c_int, C.POINTER(C.c_double),
-                                        C.POINTER(C.c_double)]
+        lib.ref_make_fractal.argtypes = [C.c_int, C.c_int, C.c_uint32, _f32p]
+        lib.ref_sweep_sample.argtypes = [_f32p, C.c_int, C.c_int, C.c_double, C.c_int, C.c_double, C.c_double,
+                                         _i32p, C.c_int, C.c_int, C.POINTER(C.c_double)]
+        lib.ref_sector_work.argtypes = [C.c_int, C.c_int, C.c_double, C.c_int, C.c_int, C.c_double]
+        lib.ref_sector_work.restype = C.c_longlong
 
         lib.ref_singular_viewshed.argtypes = [_f32p, C.c_int, C.c_int, C.c_double, C.c_int, C.c_int, C.c_double,
                                               C.c_int, C.c_double, C.POINTER(C.c_double)]
@@ -263,14 +265,27 @@ class Ref:
                                                            cellsize, ns, h0, max_distance or 0.0, out))
         return out
 
-    def sample_scan(self, dem, ns, h0, max_distance, cellsize, sectors, row_stride, row_offset, threads):
-        ev = C.c_double()
+    def make_fractal(self, dimy, dimx, seed=7) -> np.ndarray:
+        """The bench's fractal terrain (restated in ref_shim.cpp)."""
+        out = np.empty((dimy, dimx), np.float32)
+        self._check(self.lib.ref_make_fractal(dimy, dimx, seed, out))
+        return out
+
+    def sweep_sample(self, dem, cellsize, ns, h0, max_distance, sectors, threads) -> float:
+        """Wall seconds of the reference's sector_sweep on `sectors`, claimed
+        dynamically by `threads` host threads."""
         sec = C.c_double()
         s = np.ascontiguousarray(sectors, np.int32)
-        self._check(self.lib.ref_sample_scan(np.ascontiguousarray(dem), dem.shape[0], dem.shape[1], ns, h0,
-                                             max_distance or 0.0, cellsize, s, len(s), row_stride, row_offset,
-                                             threads, C.byref(ev), C.byref(sec)))
-        return ev.value, sec.value
+        self._check(self.lib.ref_sweep_sample(np.ascontiguousarray(dem), dem.shape[0], dem.shape[1], cellsize, ns,
+                                              h0, max_distance or 0.0, s, len(s), threads, C.byref(sec)))
+        return sec.value
+
+    def sector_work(self, dimy, dimx, cellsize, ns, k, max_distance=None) -> int:
+        """Exact target evaluations of sector k from the reference's own row ranges."""
+        w = self.lib.ref_sector_work(dimy, dimx, cellsize, ns, k, max_distance or 0.0)
+        if w < 0:
+            raise RuntimeError(self.lib.ref_last_error().decode())
+        return int(w)
 
 
 class Orc:

@@ -201,3 +201,30 @@ def test_acceptance_flat_forward_scans(ora):  # acceptance_main.cpp:218-251 (cri
             for j0 in range(first, last):
                 L = last - 1 - j0
                 assert ora.linear_viewshed_row(v[q], first, last, j0, 1.5, 0) == (L + 1) ** 2 - 1
+
+
+# ---- bench inputs and work counts of the reference arm ------------------------------
+
+@pytest.mark.skipif(not have_ref(), reason="oracle/_ref not built")
+@pytest.mark.parametrize("shape,seed", [((2, 2), 0), ((33, 17), 7), ((500, 500), 7), ((129, 300), 3)])
+def test_reference_arm_fractal_matches_product(shape, seed):
+    """bench.py's reference arm builds the fractal DEM with the shim's
+    restatement (so it never loads the product library); it must be the same
+    float grid the GPU arm consumes."""
+    import paper_2003_02200_b200 as sk
+
+    ours = sk.make_synthetic(sk.SyntheticKind.Fractal, *shape, 10.0, seed).values
+    theirs = Ref().make_fractal(*shape, seed)
+    assert np.array_equal(b32(ours), b32(theirs))
+
+
+@pytest.mark.skipif(not have_ref(), reason="oracle/_ref not built")
+@pytest.mark.parametrize("dims,ns,maxd", [((120, 90), 36, None), ((64, 64), 360, 150.0), ((40, 70), 8, 25.0)])
+def test_reference_work_count_matches_plan(dims, ns, maxd):
+    """The reference arm counts scan work from the reference's own build_skw
+    row ranges; the GPU arm from its host plan. Same numbers, every sector."""
+    import paper_2003_02200_b200 as sk
+
+    ref = Ref()
+    for k in range(ns // 2):
+        assert ref.sector_work(*dims, 10.0, ns, k, maxd) == sk.sector_target_evals(k, ns, *dims, 10.0, maxd)
