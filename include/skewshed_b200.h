@@ -38,16 +38,22 @@ enum { SKS_UNITS_M2 = 0, SKS_UNITS_KM2 = 1 };
 enum { SKS_SCAN_FORWARD = 0, SKS_SCAN_BACKWARD = 1 };
 enum { SKS_NO_DISTANCE_CAP = 2147483647 }; /* scan.hpp:15 kNoDistanceCap */
 
+enum { SKS_ALL_GPUS = -1 }; /* sks_run_config.n_gpus: every visible device */
+
 /* RunConfig, dem.hpp:40-46. std::optional<double> max_distance becomes a
  * double with 0 = off (the CLI's own convention, cli.cpp:82,112); Units
- * becomes an int; `workers` has no meaning on a GPU and is replaced by the
- * CUDA device ordinal. */
+ * becomes an int. The reference's `workers` (host threads sharing one call,
+ * engine.cpp:109-220) becomes n_gpus: GPUs sharing one call, devices
+ * device .. device + n_gpus - 1 (SKS_ALL_GPUS: every visible one from
+ * `device` on), one host thread per GPU and one NCCL reduce of the maps.
+ * Validated like workers (>= 1, or SKS_ALL_GPUS). */
 typedef struct {
   int ns;              /* sector count over 2*pi, even >= 2 */
   double h0;           /* observer height above ground, m, >= 0 */
   double max_distance; /* visibility cap in m; 0 = off */
   int units;           /* SKS_UNITS_M2 or SKS_UNITS_KM2 */
-  int device;          /* CUDA device ordinal */
+  int device;          /* first CUDA device ordinal */
+  int n_gpus;          /* GPUs for total_viewshed[_raw]: >= 1 or SKS_ALL_GPUS */
 } sks_run_config;
 
 /* EngineStats, engine.hpp:25-32, plus GPU evidence. Phase seconds are
@@ -136,7 +142,10 @@ sks_status sks_validate(const float* dem, int dimy, int dimx, double cellsize,
 /* ---- end-to-end (host buffers) -------------------------------------- */
 
 /* total_viewshed, engine.cpp:222-233: out_vs (dimy*dimx doubles) receives
- * the per-cell viewshed area in cfg->units. */
+ * the per-cell viewshed area in cfg->units. With cfg->n_gpus > 1 the call is
+ * shared by that many GPUs (sks_total_viewshed_devices); stats then sum the
+ * per-GPU device seconds (as the reference sums worker seconds) and
+ * reduce_seconds is the NCCL reduce + scaling. */
 sks_status sks_total_viewshed(const float* dem, int dimy, int dimx,
                               double cellsize, const sks_run_config* cfg,
                               double* out_vs, sks_stats* stats);
@@ -144,6 +153,27 @@ sks_status sks_total_viewshed(const float* dem, int dimy, int dimx,
 sks_status sks_total_viewshed_raw(const float* dem, int dimy, int dimx,
                                   double cellsize, const sks_run_config* cfg,
                                   double* out_raw, sks_stats* stats);
+/* In-process multi-GPU total viewshed (raw = 1: total_viewshed_raw): one
+ * host thread per listed device runs its row block of every sector
+ * (sks_context_run_rows_cuts) into a private FP64 map; ONE ncclReduce(sum,
+ * f64) to devices[0] (NCCL loaded at run time) is the only exchange; then
+ * scaling and the D2H copy. A list with repeated devices (ranks sharing a
+ * GPU) reduces with peer adds instead of NCCL. The row-block cuts adapt to
+ * measured per-GPU times over the first 3 calls per workload shape, then
+ * stay fixed. Per-cell sums differ from one GPU only in order (<= 1e-12
+ * relative; the reference bar is 1e-5). SKS_NCCL_ERROR when NCCL fails. */
+sks_status sks_total_viewshed_devices(const float* dem, int dimy, int dimx, double cellsize,
+                                      const sks_run_config* cfg, const int* devices, int n_devices,
+                                      int raw, double* out, sks_stats* stats);
+/* The device list a run config names (n_gpus, device); returns the count
+ * (written up to cap). */
+int sks_config_devices(const sks_run_config* cfg, int* devices, int cap);
+/* One rebalancing step of the row-block cuts (nparts + 1 non-decreasing
+ * fractions): given the per-part times measured with `cuts`, the cuts that
+ * give every part an equal share when time is piecewise linear in the cost
+ * fraction. Host only. */
+void sks_row_cuts_update(const double* cuts, const double* times, int nparts, double* out);
+
 /* sector_sweep, engine.cpp:235-244: one sector's unskewed contribution. */
 sks_status sks_sector_sweep(const float* dem, int dimy, int dimx,
                             double cellsize, const sks_run_config* cfg, int k,

@@ -100,15 +100,18 @@ struct Dem {
   int dimx() const { return values.cols(); }
 };
 
-// dem.hpp:40-46; `workers` is replaced by the CUDA device ordinal.
+// dem.hpp:40-46. `workers` (host threads sharing one call) becomes n_gpus
+// (GPUs sharing one call from `device` on; SKS_ALL_GPUS = every visible one):
+// total_viewshed then runs one host thread per GPU and one NCCL reduce.
 struct RunConfig {
   int ns = 360;
   double h0 = 1.5;
   int device = 0;
+  int n_gpus = 1;
   std::optional<double> max_distance;
   Units units = Units::SquareKilometers;
   sks_run_config to_c() const {
-    return sks_run_config{ns, h0, max_distance.value_or(0.0), static_cast<int>(units), device};
+    return sks_run_config{ns, h0, max_distance.value_or(0.0), static_cast<int>(units), device, n_gpus};
   }
 };
 

@@ -36,7 +36,7 @@ NO_CAP = 2147483647
 
 class RunConfigC(C.Structure):
     _fields_ = [("ns", C.c_int), ("h0", C.c_double), ("max_distance", C.c_double),
-                ("units", C.c_int), ("device", C.c_int)]
+                ("units", C.c_int), ("device", C.c_int), ("n_gpus", C.c_int)]
 
 
 class StatsC(C.Structure):
@@ -91,6 +91,10 @@ SIGNATURES = {
                                      C.POINTER(StatsC)]),
     "sks_total_viewshed_raw": (C.c_int, [_vp, C.c_int, C.c_int, C.c_double, C.POINTER(RunConfigC), _vp,
                                          C.POINTER(StatsC)]),
+    "sks_total_viewshed_devices": (C.c_int, [_vp, C.c_int, C.c_int, C.c_double, C.POINTER(RunConfigC), _vp, C.c_int,
+                                             C.c_int, _vp, C.POINTER(StatsC)]),
+    "sks_config_devices": (C.c_int, [C.POINTER(RunConfigC), _vp, C.c_int]),
+    "sks_row_cuts_update": (None, [_vp, _vp, C.c_int, _vp]),
     "sks_sector_sweep": (C.c_int, [_f32p, C.c_int, C.c_int, C.c_double, C.POINTER(RunConfigC), C.c_int,
                                    _f64p]),
     "sks_build_sector_sdem": (C.c_int, [_f32p, C.c_int, C.c_int, C.c_int, C.c_int, C.c_int, _f32p, _i32p]),

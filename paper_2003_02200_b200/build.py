@@ -26,6 +26,15 @@ NVCC_FLAGS = [
 ]
 
 
+# host-only C++ (planning, I/O, the multi-GPU orchestration): same IEEE
+# rules as the device code (no FMA contraction)
+CXX_FLAGS = [
+    "-std=c++20", "-O3", "-g", "-fPIC", "-ffp-contract=off",
+    "-I", "/usr/local/cuda/include",
+    "-I", os.path.join(ROOT, "include"),
+]
+
+
 def sources():
     return sorted(glob.glob(os.path.join(CSRC, "*.cu")) + glob.glob(os.path.join(CSRC, "*.cpp")))
 
@@ -52,8 +61,8 @@ def build(force: bool = False, verbose: bool = False, defines=(), out: str = Non
         obj = os.path.join(objdir, os.path.basename(src) + ".o")
         dflags = [f"-D{d}" for d in defines]
         cmd = ["nvcc", *NVCC_FLAGS, *dflags, "-c", src, "-o", obj]
-        if src.endswith(".cpp"):
-            cmd = ["nvcc", *NVCC_FLAGS, *dflags, "-x", "cu", "-c", src, "-o", obj]
+        if src.endswith(".cpp"):  # host-only sources: the host compiler directly
+            cmd = ["g++", *CXX_FLAGS, *dflags, "-c", src, "-o", obj]
         return src, obj, subprocess.run(cmd, capture_output=True, text=True)
 
     objs = []
@@ -68,7 +77,7 @@ def build(force: bool = False, verbose: bool = False, defines=(), out: str = Non
         objs.append(obj)
     tmp = lib + ".tmp"
     cmd = ["nvcc", "-gencode", "arch=compute_100a,code=sm_100a", "-shared", "-cudart", "static",
-           "-o", tmp, *objs, "-lpthread"]
+           "-o", tmp, *objs, "-lpthread", "-ldl"]
     r = subprocess.run(cmd, capture_output=True, text=True)
     if r.returncode != 0:
         sys.stderr.write(r.stdout + r.stderr)

@@ -512,7 +512,7 @@ void require_valid(const float* dem, int dimy, int dimx, double cellsize,
   if (!cfg) throw std::invalid_argument("null run config");
   if (!dem) throw std::invalid_argument("null DEM");
   std::string err =
-      validate_inputs(dem, dimy, dimx, cellsize, nullptr, cfg->ns, cfg->h0, cfg->max_distance);
+      validate_inputs(dem, dimy, dimx, cellsize, nullptr, cfg->ns, cfg->h0, cfg->max_distance, cfg->n_gpus);
   if (!err.empty()) throw std::invalid_argument(err);
 }
 
@@ -650,7 +650,7 @@ bool device_check(sks_context* ctx, const float* d_dem, int dimy, int dimx, cons
   if (ctx->h_check[0] != ~0ull) {
     throw std::invalid_argument(nonfinite_message(static_cast<long long>(ctx->h_check[0]), dimx));
   }
-  const std::string err = validate_config(cfg->ns, cfg->h0, cfg->max_distance);
+  const std::string err = validate_config(cfg->ns, cfg->h0, cfg->max_distance, cfg->n_gpus);
   if (!err.empty()) throw std::invalid_argument(err);
   const double plo = std::ldexp(1.0, -40), phi = std::ldexp(1.0, 40);
   return ctx->h_check[1] != 0 || (cfg->h0 != 0.0 && (cfg->h0 < plo || cfg->h0 > phi));
@@ -717,6 +717,8 @@ DebugBatch debug_batch(SectorPlanH plan, int device) {
 extern "C" {
 
 const char* sks_last_error(void) { return g_error.c_str(); }
+
+void sks_set_last_error(const char* msg) { g_error = msg ? msg : ""; }
 
 const char* sks_version(void) { return "skewshed_b200 0.2.0 (sm_100a)"; }
 
@@ -810,7 +812,7 @@ sks_status sks_validate(const float* dem, int dimy, int dimx, double cellsize, c
   return guarded([&] {
     if (!cfg || !dem) throw std::invalid_argument("null argument");
     std::string err =
-        validate_inputs(dem, dimy, dimx, cellsize, nodata, cfg->ns, cfg->h0, cfg->max_distance);
+        validate_inputs(dem, dimy, dimx, cellsize, nodata, cfg->ns, cfg->h0, cfg->max_distance, cfg->n_gpus);
     if (!err.empty()) throw std::invalid_argument(err);
   });
 }
@@ -908,20 +910,30 @@ sks_status sks_context_total_viewshed(sks_context* ctx, const float* dem, int di
   });
 }
 
+// n_gpus > 1 (or SKS_ALL_GPUS with several visible): one host thread per GPU
+// and one NCCL reduce (multi.cu); else the single-device path.
+static sks_status total_dispatch(const float* dem, int dimy, int dimx, double cellsize, const sks_run_config* cfg, int raw,
+                          double* out, sks_stats* stats) {
+  std::vector<int> devs(64);
+  int nd = 0;
+  const sks_status s = guarded([&] {
+    require_valid(dem, dimy, dimx, cellsize, cfg);  // before touching the device
+    nd = sks_config_devices(cfg, devs.data(), static_cast<int>(devs.size()));
+    if (nd > static_cast<int>(devs.size())) throw std::invalid_argument("too many GPUs requested");
+    if (nd <= 1) total_host(default_context(cfg->device), dem, dimy, dimx, cellsize, cfg, raw, out, stats);
+  });
+  if (s != SKS_OK || nd <= 1) return s;
+  return sks_total_viewshed_devices(dem, dimy, dimx, cellsize, cfg, devs.data(), nd, raw, out, stats);
+}
+
 sks_status sks_total_viewshed(const float* dem, int dimy, int dimx, double cellsize,
                               const sks_run_config* cfg, double* out_vs, sks_stats* stats) {
-  return guarded([&] {
-    require_valid(dem, dimy, dimx, cellsize, cfg);  // before touching the device
-    total_host(default_context(cfg->device), dem, dimy, dimx, cellsize, cfg, 0, out_vs, stats);
-  });
+  return total_dispatch(dem, dimy, dimx, cellsize, cfg, 0, out_vs, stats);
 }
 
 sks_status sks_total_viewshed_raw(const float* dem, int dimy, int dimx, double cellsize,
                                   const sks_run_config* cfg, double* out_raw, sks_stats* stats) {
-  return guarded([&] {
-    require_valid(dem, dimy, dimx, cellsize, cfg);  // before touching the device
-    total_host(default_context(cfg->device), dem, dimy, dimx, cellsize, cfg, 1, out_raw, stats);
-  });
+  return total_dispatch(dem, dimy, dimx, cellsize, cfg, 1, out_raw, stats);
 }
 
 sks_status sks_sector_sweep(const float* dem, int dimy, int dimx, double cellsize,
@@ -1386,7 +1398,7 @@ sks_status sks_total_viewshed_reference(const float* dem, int dimy, int dimx, do
       if (nodata && dem[c] == *nodata) continue;
       if (!std::isfinite(dem[c])) throw std::invalid_argument(nonfinite_message(static_cast<long long>(c), dimx));
     }
-    err = validate_config(cfg->ns, cfg->h0, cfg->max_distance);
+    err = validate_config(cfg->ns, cfg->h0, cfg->max_distance, cfg->n_gpus);
     if (!err.empty()) throw std::invalid_argument(err);
     const long long cells = static_cast<long long>(dimy) * dimx;
     if (cells > SKS_REFERENCE_CELL_GUARD && !force) {  // oracle.cpp:154-163

@@ -445,7 +445,7 @@ std::string nonfinite_message(long long idx, int dimx) {
   return os.str();
 }
 
-std::string validate_config(int ns, double h0, double max_distance) {
+std::string validate_config(int ns, double h0, double max_distance, int n_gpus) {
   std::ostringstream os;
   if (ns < 2 || ns % 2 != 0) {
     os << "invalid config: ns must be an even integer >= 2, got " << ns;
@@ -453,6 +453,10 @@ std::string validate_config(int ns, double h0, double max_distance) {
   }
   if (!(h0 >= 0.0) || !std::isfinite(h0)) {
     os << "invalid config: observer height must be >= 0, got " << h0;
+    return os.str();
+  }
+  if (n_gpus < 1 && n_gpus != -1) {  // workers >= 1 (dem.cpp:74-78); -1 = every visible GPU
+    os << "invalid config: GPU count must be >= 1 (or -1 for all), got " << n_gpus;
     return os.str();
   }
   if (max_distance != 0.0 && (!(max_distance > 0.0) || !std::isfinite(max_distance))) {
@@ -464,7 +468,7 @@ std::string validate_config(int ns, double h0, double max_distance) {
 
 std::string validate_inputs(const float* dem, int dimy, int dimx,
                             double cellsize, const float* nodata, int ns,
-                            double h0, double max_distance) {
+                            double h0, double max_distance, int n_gpus) {
   std::string e = validate_grid_header(dimy, dimx, cellsize);
   if (!e.empty()) return e;
   const size_t n = static_cast<size_t>(dimy) * dimx;
@@ -480,7 +484,7 @@ std::string validate_inputs(const float* dem, int dimy, int dimx,
       }
     }
   }
-  return validate_config(ns, h0, max_distance);
+  return validate_config(ns, h0, max_distance, n_gpus);
 }
 
 }  // namespace sks

@@ -93,11 +93,11 @@ void make_synthetic(int kind, int dimy, int dimx, uint32_t seed, float* out);
 // error message with the reference's wording.
 std::string validate_inputs(const float* dem, int dimy, int dimx,
                             double cellsize, const float* nodata, int ns,
-                            double h0, double max_distance);
+                            double h0, double max_distance, int n_gpus = 1);
 // The same checks in pieces, for the device-side cell scan (total_host):
 // grid header (dims, cellsize), the first non-finite cell's message, config.
 std::string validate_grid_header(int dimy, int dimx, double cellsize);
 std::string nonfinite_message(long long idx, int dimx);
-std::string validate_config(int ns, double h0, double max_distance);
+std::string validate_config(int ns, double h0, double max_distance, int n_gpus = 1);
 
 }  // namespace sks

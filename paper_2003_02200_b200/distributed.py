@@ -32,7 +32,7 @@ from typing import Callable, Optional, Sequence
 
 import numpy as np
 
-from .engine import RunConfig, Units, area_scale_factor, partition_sectors
+from .engine import RunConfig, Units, area_scale_factor, partition_sectors, row_cuts_update
 
 
 class RowBalancer:
@@ -54,19 +54,10 @@ class RowBalancer:
 
     def update(self, times: Sequence[float]) -> np.ndarray:
         t = np.asarray(times, np.float64)
-        if t.shape != (self.world,) or not np.all(np.isfinite(t)) or t.sum() <= 0.0:
+        if t.shape != (self.world,):
             return self.cuts
-        c = self.cuts
-        T = np.concatenate([[0.0], np.cumsum(t)])
-        new = [0.0]
-        for b in range(1, self.world):
-            target = b * T[-1] / self.world
-            r = int(np.searchsorted(T, target, side="right") - 1)
-            r = min(max(r, 0), self.world - 1)
-            frac = (target - T[r]) / t[r] if t[r] > 0.0 else 0.0
-            new.append(float(c[r] + min(max(frac, 0.0), 1.0) * (c[r + 1] - c[r])))
-        new.append(1.0)
-        self.cuts = np.maximum.accumulate(np.clip(np.asarray(new), 0.0, 1.0))
+        # the same step the in-process multi-GPU path takes (sks_row_cuts_update)
+        self.cuts = row_cuts_update(self.cuts, t)
         return self.cuts
 
 
@@ -104,20 +95,23 @@ def total_viewshed_distributed(dem: np.ndarray, cellsize: float, cfg: RunConfig,
     dev = torch.device("cuda", torch.cuda.current_device())
     ctx = context or Context(dev.index)
     st = stream or torch.cuda.current_stream(dev)
-    d_dem = torch.from_numpy(np.ascontiguousarray(dem, np.float32)).to(dev, non_blocking=True)
-    d_map = torch.zeros((dimy, dimx), dtype=torch.float64, device=dev)
-    if mode == "rows":
-        es = ctx.run_rows(d_dem.data_ptr(), dimy, dimx, cellsize, cfg, rank, world, d_map.data_ptr(),
-                          stream=st.cuda_stream, want_stats=stats is not None, cuts=cuts)
-    else:
-        es = ctx.run_sectors(d_dem.data_ptr(), dimy, dimx, cellsize, cfg, mine, d_map.data_ptr(),
-                             stream=st.cuda_stream, want_stats=stats is not None)
-    if stats is not None:
-        stats["rank_stats"] = es
-        stats["sectors"] = mine if mode != "rows" else f"rows {rank}/{world} of every sector"
-    dist.reduce(d_map, dst=0, op=dist.ReduceOp.SUM)
-    if rank != 0:
-        return None
-    if not raw:
-        ctx.scale(d_map.data_ptr(), dimy * dimx, cfg.ns, cellsize, int(cfg.units), st.cuda_stream)
-    return d_map.cpu().numpy()
+    # everything below is ordered on `st`: the DEM copy and the map clear
+    # before the engine's kernels, the kernels before the reduce and the D2H
+    with torch.cuda.stream(st):
+        d_dem = torch.from_numpy(np.ascontiguousarray(dem, np.float32)).to(dev, non_blocking=True)
+        d_map = torch.zeros((dimy, dimx), dtype=torch.float64, device=dev)
+        if mode == "rows":
+            es = ctx.run_rows(d_dem.data_ptr(), dimy, dimx, cellsize, cfg, rank, world, d_map.data_ptr(),
+                              stream=st.cuda_stream, want_stats=stats is not None, cuts=cuts)
+        else:
+            es = ctx.run_sectors(d_dem.data_ptr(), dimy, dimx, cellsize, cfg, mine, d_map.data_ptr(),
+                                 stream=st.cuda_stream, want_stats=stats is not None)
+        if stats is not None:
+            stats["rank_stats"] = es
+            stats["sectors"] = mine if mode != "rows" else f"rows {rank}/{world} of every sector"
+        dist.reduce(d_map, dst=0, op=dist.ReduceOp.SUM)
+        if rank != 0:
+            return None
+        if not raw:
+            ctx.scale(d_map.data_ptr(), dimy * dimx, cfg.ns, cellsize, int(cfg.units), st.cuda_stream)
+        return d_map.cpu().numpy()

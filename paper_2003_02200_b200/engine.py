@@ -55,20 +55,27 @@ class ScanDir(enum.IntEnum):
     Backward = 1
 
 
+ALL_GPUS = -1  # RunConfig.n_gpus: every visible GPU
+
+
 @dataclass
 class RunConfig:
-    """dem.hpp:40-46. ``workers`` is replaced by the CUDA ``device``."""
+    """dem.hpp:40-46. The reference's ``workers`` (host threads sharing one
+    call) becomes ``n_gpus`` (GPUs sharing one call: devices ``device`` ..
+    ``device + n_gpus - 1``, or ALL_GPUS), one NCCL reduce of the maps."""
     ns: int = 360
     h0: float = 1.5
     max_distance: Optional[float] = None
     units: Units = Units.SquareKilometers
     device: int = 0
+    n_gpus: int = 1
 
     def to_c(self) -> _lib.RunConfigC:
         md = 0.0 if self.max_distance is None else float(self.max_distance)
         if self.max_distance is not None and not md > 0.0:
             raise ValueError(f"invalid config: max distance must be a positive finite number, got {md}")
-        return _lib.RunConfigC(int(self.ns), float(self.h0), md, int(self.units), int(self.device))
+        return _lib.RunConfigC(int(self.ns), float(self.h0), md, int(self.units), int(self.device),
+                               int(self.n_gpus))
 
 
 @dataclass
@@ -350,6 +357,44 @@ def total_viewshed(dem: Dem, cfg: RunConfig, stats: Optional[EngineStats] = None
     if progress is not None:
         _report_progress(dem, cfg, st, progress)
     return VsGrid(out, Units(cfg.units))
+
+
+def total_viewshed_devices(dem: Dem, cfg: RunConfig, devices, raw: bool = False,
+                           stats: Optional[EngineStats] = None) -> np.ndarray:
+    """One total viewshed shared by the listed GPUs in this process (one host
+    thread per GPU, one NCCL reduce; repeated devices reduce by peer adds).
+    Returns the raw map if ``raw``, else the scaled areas."""
+    _require_no_nodata(dem, cfg)
+    devs = np.ascontiguousarray(devices, np.int32)
+    out = np.empty((dem.dimy(), dem.dimx()), np.float64)
+    c = cfg.to_c()
+    st = _lib.StatsC()
+    check(lib.sks_total_viewshed_devices(dem.values.ctypes.data, dem.dimy(), dem.dimx(), dem.cellsize, C.byref(c),
+                                         devs.ctypes.data, len(devs), int(raw), out.ctypes.data, C.byref(st)))
+    if stats is not None:
+        for k, v in st.as_dict().items():
+            setattr(stats, k, v)
+    return out
+
+
+def config_devices(cfg: RunConfig) -> list:
+    """The GPUs a run config names (device, n_gpus)."""
+    c = cfg.to_c()
+    buf = np.zeros(256, np.int32)
+    n = int(lib.sks_config_devices(C.byref(c), buf.ctypes.data, len(buf)))
+    return buf[:min(n, len(buf))].tolist()
+
+
+def row_cuts_update(cuts, times) -> np.ndarray:
+    """One measured-time rebalancing step of the row-block cuts (C++,
+    sks_row_cuts_update; distributed.RowBalancer wraps it)."""
+    c = np.ascontiguousarray(cuts, np.float64)
+    t = np.ascontiguousarray(times, np.float64)
+    if c.shape != (len(t) + 1,):
+        raise ValueError("cuts must hold len(times) + 1 fractions")
+    out = np.empty_like(c)
+    lib.sks_row_cuts_update(c.ctypes.data, t.ctypes.data, len(t), out.ctypes.data)
+    return out
 
 
 def sector_sweep(dem: Dem, cfg: RunConfig, k: int) -> SectorResult:
