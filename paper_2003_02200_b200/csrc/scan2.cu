@@ -41,6 +41,7 @@
 // no CTA-wide barrier after the start-up.
 #include <cuda_runtime.h>
 
+#include <algorithm>
 #include <cfloat>
 #include <climits>
 #include <cstdint>
@@ -84,7 +85,7 @@ constexpr int kSumShift = 22;
 constexpr int kSumMask = (1 << kSumShift) - 1;
 
 struct Layout2 {
-  int nc;     // fl(1/dd) table copies: 4 (quad loads) or 2 (pair loads, long rows)
+  int nc;     // fl(1/dd) table copies: 4 (quad loads), 2 (pair loads) or 1 (long rows)
   int lb;     // row buffer (floats) per direction
   int nw16, nw64;
   int T;      // table length per copy (floats, a multiple of 32)
@@ -352,13 +353,24 @@ __device__ __forceinline__ bool step_vis(float t, float& hi, float& lo, int& A, 
 // (still a bound: fl(1/d) is monotone); the N pair is ordered to match. A
 // dd <= 0 reads NaN and fails the test (never skipped: conservative).
 // Absent POVs have hf = +inf, so N = -inf and they never block a skip.
-template <bool kHl>
+// With one table copy (kNC == 1, long rows) tb addresses copy 0 with the
+// same element offset, where the pairs are not 8-B aligned: two scalar loads.
+template <bool kHl, int kNC = 2>
 __device__ __forceinline__ bool window_hidden(const Pov2& P, float2 em2, unsigned tb, int k0, int w) {
   float2 N = __fadd2_rn(em2, make_float2(-P.hf1, -P.hf0));
   if (kHl) N = __fadd2_rn(N, make_float2(-P.hl1, -P.hl0));
   const unsigned ra = tb + 4u * static_cast<unsigned>(k0);
-  const float2 b1 = __fmul2_rn(N, lds64(ra));
-  const float2 b2 = __fmul2_rn(N, lds64(ra + 4u * static_cast<unsigned>(w)));
+  float2 i1, i2;
+  if constexpr (kNC == 1) {
+    const unsigned rb = ra + 4u * static_cast<unsigned>(w);
+    i1 = make_float2(lds32(ra), lds32(ra + 4));
+    i2 = make_float2(lds32(rb), lds32(rb + 4));
+  } else {
+    i1 = lds64(ra);
+    i2 = lds64(ra + 4u * static_cast<unsigned>(w));
+  }
+  const float2 b1 = __fmul2_rn(N, i1);
+  const float2 b2 = __fmul2_rn(N, i2);
   const bool ok = (b1.x < P.lo1) & (b2.x < P.lo1) & (b1.y < P.lo0) & (b2.y < P.lo0);
   return __all_sync(0xffffffffu, ok);
 }
@@ -375,6 +387,13 @@ __device__ __forceinline__ void eval16(Pov2& P, unsigned sb, unsigned ivb0, unsi
     if (kNC == 4) {
       q0 = lds128(ivb0 + 4 * k);
       q1 = lds128(ivb1 + 4 * k);
+    } else if constexpr (kNC == 1) {
+      // one copy: the first POV's quad is pair-aligned, the second's starts
+      // one element off (a scalar, a pair, a scalar)
+      const float2 a0 = lds64(ivb0 + 4 * k), b0 = lds64(ivb0 + 4 * k + 8);
+      const float2 m1 = lds64(ivb1 + 4 * k + 4);
+      q0 = make_float4(a0.x, a0.y, b0.x, b0.y);
+      q1 = make_float4(lds32(ivb1 + 4 * k), m1.x, m1.y, lds32(ivb1 + 4 * k + 12));
     } else {
       const float2 a0 = lds64(ivb0 + 4 * k), b0 = lds64(ivb0 + 4 * k + 8);
       const float2 a1 = lds64(ivb1 + 4 * k), b1 = lds64(ivb1 + 4 * k + 8);
@@ -431,6 +450,13 @@ __device__ __forceinline__ void eval16_capped(Pov2& P, unsigned sb, unsigned ivb
     if (kNC == 4) {
       q0 = lds128(ivb0 + 4 * k);
       q1 = lds128(ivb1 + 4 * k);
+    } else if constexpr (kNC == 1) {
+      // one copy: the first POV's quad is pair-aligned, the second's starts
+      // one element off (a scalar, a pair, a scalar)
+      const float2 a0 = lds64(ivb0 + 4 * k), b0 = lds64(ivb0 + 4 * k + 8);
+      const float2 m1 = lds64(ivb1 + 4 * k + 4);
+      q0 = make_float4(a0.x, a0.y, b0.x, b0.y);
+      q1 = make_float4(lds32(ivb1 + 4 * k), m1.x, m1.y, lds32(ivb1 + 4 * k + 12));
     } else {
       const float2 a0 = lds64(ivb0 + 4 * k), b0 = lds64(ivb0 + 4 * k + 8);
       const float2 a1 = lds64(ivb1 + 4 * k), b1 = lds64(ivb1 + 4 * k + 8);
@@ -479,8 +505,10 @@ __device__ void run_task(const ScanArgs& a, const Layout2& lay, const Slot& sl, 
   const float2* W16 = dir ? sl.WR16 : sl.WS16;
   const float2* W64 = dir ? sl.WR64 : sl.WS64;
   const unsigned sb = smem_u32(B);
-  // copy 1 holds fl(1/d) at element d + kOff - 1 (window tests, pair loads)
-  const unsigned tb = smem_u32(IV + lay.copy(1)) + 4u * static_cast<unsigned>(kOff - 2 - P.y0);
+  // copy 1 holds fl(1/d) at element d + kOff - 1 (window tests, pair loads;
+  // one copy: copy 0 at element d + kOff)
+  const unsigned tb = kNC == 1 ? smem_u32(IV + lay.copy(0)) + 4u * static_cast<unsigned>(kOff - 1 - P.y0)
+                               : smem_u32(IV + lay.copy(1)) + 4u * static_cast<unsigned>(kOff - 2 - P.y0);
   // per POV: the table copy r with (k - y - r) % kNC == 0 for k % 4 == 0
   // (y0 is even: with 2 copies the first POV reads copy 0, the second copy 1)
   const int y1 = P.y0 + 1;
@@ -510,7 +538,7 @@ __device__ void run_task(const ScanArgs& a, const Layout2& lay, const Slot& sl, 
   while (k0 <= klast) {
     if (!kVis && k0 >= kctest && k0 + kH - 1 <= kmain) {
       const float2 em = lds64(w64a + 8u * (static_cast<unsigned>(k0) / kH));
-      if (window_hidden<kHl>(P, em, tb, k0, kH)) {
+      if (window_hidden<kHl, kNC>(P, em, tb, k0, kH)) {
         k0 += kH;
         nskip += kH;
         continue;
@@ -520,7 +548,7 @@ __device__ void run_task(const ScanArgs& a, const Layout2& lay, const Slot& sl, 
     while (k0 < kc && k0 <= klast && k0 + kW - 1 <= kmain) {
       if (!kVis && k0 >= ktest) {
         const float2 em = lds64(w16a + 8u * (static_cast<unsigned>(k0) / kW));
-        if (window_hidden<kHl>(P, em, tb, k0, kW)) {
+        if (window_hidden<kHl, kNC>(P, em, tb, k0, kW)) {
           k0 += kW;
           nskip += kW;
           continue;
@@ -546,7 +574,7 @@ __device__ void run_task(const ScanArgs& a, const Layout2& lay, const Slot& sl, 
     for (; k0 <= kt_end; k0 += kW) {
       if (k0 >= ktest) {  // the bound over the whole window also covers the masked targets
         const float2 em = lds64(w16a + 8u * (static_cast<unsigned>(k0) / kW));
-        if (window_hidden<kHl>(P, em, tb, k0, kW)) {
+        if (window_hidden<kHl, kNC>(P, em, tb, k0, kW)) {
           nskip += kW;
           continue;
         }
@@ -777,28 +805,38 @@ __global__ void __launch_bounds__(kThr, 1) scan2_kernel(const __grid_constant__ 
 }  // namespace
 
 // Table copies and slots that fit the opt-in shared memory for rows up to
-// lmax: 2 copies (4 with -DSKS_PREFER_NC4 where >= 2 slots fit) with >= 1
-// slot; 0 slots: the rows are too long for shared memory and go through the
-// fixup kernel whole (long rows, engine.cu).
+// lmax: 2 copies (pair loads) where >= 2 slots fit (rows up to ~8 000
+// cells; 4 copies with quad loads measured slower: the freed memory holds
+// more row slots, config 2 scan 59.7 -> 58.9 ms, -DSKS_PREFER_NC4 keeps
+// them); beyond, one copy if that fits more slots (config 5's 10 000-cell
+// rows: 2 slots instead of 1; the second POV's table quads and the window
+// tests then take scalar loads), else whichever holds one slot (rows up to
+// ~17 000 cells). 0 slots: the rows go through the fixup kernel whole (long
+// rows, engine.cu).
 static void scan2_config(int lmax, int* copies, int* slots) {
   *copies = 0;
   *slots = 0;
   if (lmax >= 32768 - 128) return;  // k < 2^15 keeps the flush sums exact
   const long long cap = 227 * 1024;
-#ifdef SKS_PREFER_NC4
-  for (int nc : {4, 2}) {
-#else
-  // 2 copies (pair loads) even where 4 would fit: the smem they free holds
-  // more row slots, which measured faster (config 2 scan 59.7 -> 58.9 ms)
-  for (int nc : {2}) {
-#endif
+  auto fit = [&](int nc) {
     const Layout2 lay(lmax, nc);
     const long long n = (cap - 4LL * lay.slots) / (4LL * lay.slot);
-    if (n >= (nc == 4 ? 2 : 1)) {
-      *copies = nc;
-      *slots = static_cast<int>(n > kMaxSlots ? kMaxSlots : n);
-      return;
-    }
+    return static_cast<int>(std::min<long long>(std::max<long long>(n, 0), kMaxSlots));
+  };
+#ifdef SKS_PREFER_NC4
+  if (fit(4) >= 2) {
+    *copies = 4;
+    *slots = fit(4);
+    return;
+  }
+#endif
+  const int n2 = fit(2), n1 = fit(1);
+  if (n2 >= 2 || (n2 >= 1 && n1 <= n2)) {
+    *copies = 2;
+    *slots = n2;
+  } else if (n1 >= 1) {
+    *copies = 1;
+    *slots = n1;
   }
 }
 
@@ -846,11 +884,13 @@ int launch_scan2(const ScanArgs& a, int nslots, void* stream) {
   if (copies == 0 || nslots < 1 || nslots > fit) return static_cast<int>(cudaErrorInvalidValue);
   cudaStream_t st = static_cast<cudaStream_t>(stream);
   if (a.any_capped) {
-    return copies == 4 ? launch_scan2_t<kThreads, 4, true>(a, nslots, sms, st)
-                       : launch_scan2_t<kThreads, 2, true>(a, nslots, sms, st);
+    return copies == 4   ? launch_scan2_t<kThreads, 4, true>(a, nslots, sms, st)
+           : copies == 2 ? launch_scan2_t<kThreads, 2, true>(a, nslots, sms, st)
+                         : launch_scan2_t<kThreads, 1, true>(a, nslots, sms, st);
   }
-  return copies == 4 ? launch_scan2_t<kThreads, 4, false>(a, nslots, sms, st)
-                     : launch_scan2_t<kThreads, 2, false>(a, nslots, sms, st);
+  return copies == 4   ? launch_scan2_t<kThreads, 4, false>(a, nslots, sms, st)
+         : copies == 2 ? launch_scan2_t<kThreads, 2, false>(a, nslots, sms, st)
+                       : launch_scan2_t<kThreads, 1, false>(a, nslots, sms, st);
 }
 
 }  // namespace sks

@@ -20,7 +20,8 @@ What is compared, per configuration (BASELINE.json configs):
     four whole sectors, bit for bit.
   * rows longer than the shared-memory scan holds (sks_scan_row_limit): the
     exact per-POV path, bit for bit, plus the same path forced at small
-    sizes (SKS_LONG_ROW) end to end.
+    sizes (SKS_LONG_ROW) end to end; rows of 9 000-14 000 cells on the
+    scan's one-table-copy layout.
 The reference runs on host threads in parallel (ctypes releases the GIL).
 """
 from concurrent.futures import ThreadPoolExecutor
@@ -166,22 +167,43 @@ def test_smoothed_noise_2000_whole_sectors_bitexact(ref):
 
 @pytest.mark.parametrize("max_dd", [NO_CAP, 5000])
 def test_rows_beyond_scan_slots_bitexact(ref, max_dd):
-    """Rows of 14 000 cells (above sks_scan_row_limit, ~13 300): the batch
+    """Rows of 19 000 cells (above sks_scan_row_limit, ~17 300): the batch
     routes them whole through the exact per-POV kernel (its fl(1/d) table in
-    global memory). Every POV of every row, both directions, ragged ranges,
-    with and without a distance cap."""
-    L = 14000
-    assert L > sk.scan_row_limit()
-    rows = 5
+    global memory); rows of 14 000 and 12 000 cells in the same batch go
+    through the shared-memory scan with ONE fl(1/d) table copy (the layout
+    that holds 2 slots of config 5's 10 000-cell rows). Every POV of every
+    row, both directions, ragged ranges, with and without a distance cap."""
+    L = 19000
+    assert 14000 < sk.scan_row_limit() < L
+    rows = 6
     g = sk.make_synthetic(sk.SyntheticKind.Fractal, rows, L, 10.0, 23).values
     vals = np.ascontiguousarray(g, np.float32)
     rr = np.zeros((rows, 2), np.int32)
     rr[:, 1] = L
     rr[1] = (7, L - 3)
-    rr[3] = (100, 13050)  # shorter than the limit: scanned by the shared-memory kernel
+    rr[2] = (100, 14100)   # 14 000 cells
+    rr[3] = (5, 12004)     # 11 999 cells
+    rr[4] = (3000, 17000)  # 14 000 cells
     theirs = ref.sector_viewshed(vals, rr, rows, 0, 0.0, 1.5, max_dd)
     ours = sk.sector_viewshed(sk.SkwGrid(vals, rr, 0, rows, 0.0), 1.5, max_dd)
     assert np.array_equal(b64(ours), b64(theirs))
+
+
+@pytest.mark.parametrize("h0", [0.0, 1.7])
+def test_one_table_copy_layout_observer_heights(ref, h0):
+    """Rows of 9 000-12 000 cells (the one-table-copy scan layout) with h0 = 0
+    (exact ties on the ramp rows) and a non-float h0 (1.7: the two-float
+    observer height, the kHl path, and POVs routed to the FP64 fixup)."""
+    rows, L = 4, 12000
+    g = sk.make_synthetic(sk.SyntheticKind.Fractal, rows, L, 10.0, 31).values.copy()
+    g[2] = np.linspace(0.0, 60.0, L, dtype=np.float32)  # a ramp row: collinear targets
+    rr = np.zeros((rows, 2), np.int32)
+    rr[:, 1] = L
+    rr[1] = (2500, 11500)
+    for max_dd in (NO_CAP, 3000):
+        theirs = ref.sector_viewshed(g, rr, rows, 0, 0.0, h0, max_dd)
+        ours = sk.sector_viewshed(sk.SkwGrid(g, rr, 0, rows, 0.0), h0, max_dd)
+        assert np.array_equal(b64(ours), b64(theirs)), max_dd
 
 
 @pytest.mark.parametrize("shape,kind,ns,maxd", [
