@@ -344,7 +344,7 @@ struct sks_context {
            std::unique_ptr<Plans>>
       cache;
   // work buffers
-  DevBuf sdem, cv, cvb, queue, fixcnt, fixoff, wm16, counters, dem, map, vis, check, ivt;
+  DevBuf sdem, cv, cvb, queue, fixcnt, fixoff, wm16, counters, dem, map, vis, check, ivt, dem_pitched;
   int ivt_len = 0;  // entries of the global fl(1/d) table computed so far
   unsigned long long* h_check = nullptr;  // pinned: device DEM scan result
   cudaEvent_t ev[8] = {};
@@ -396,6 +396,26 @@ struct sks_context {
     fixoff.ensure((b.items.size() + 1 + 1024) * sizeof(unsigned), device);  // + prefix block sums
     wm16.ensure(static_cast<size_t>(b.pool_elems / 16 + 1) * sizeof(float), device);
     counters.ensure(kCounterBytes, device);
+  }
+
+  // Relocation of a batch from a device DEM. The kernel's TMA tensor maps
+  // need a 16-byte aligned base and a row pitch of whole 16-byte units; a DEM
+  // without them (dimx not a multiple of 4) is first copied into a pitched
+  // buffer (one D2D copy of the DEM, microseconds).
+  void relocate(const float* d_dem, int dimy, int dimx, const BatchDev& bd, const Batch& b, cudaStream_t st) {
+    const int al = relocate_dem_align();
+    const float* src = d_dem;
+    long long pitch = dimx;
+    if ((reinterpret_cast<uintptr_t>(d_dem) & 15u) != 0 || dimx % al != 0) {
+      pitch = round_up(dimx, 32);
+      dem_pitched.ensure(static_cast<size_t>(pitch) * dimy * sizeof(float), device);
+      cuda_check(cudaMemcpy2DAsync(dem_pitched.p, pitch * sizeof(float), d_dem, dimx * sizeof(float),
+                                   dimx * sizeof(float), dimy, cudaMemcpyDeviceToDevice, st),
+                 "pitch DEM");
+      src = dem_pitched.as<float>();
+    }
+    cuda_check(launch_relocate_grid(src, dimy, dimx, pitch, bd, b.tiles_x, b.tiles_total, st), "launch relocate");
+    ++launches;
   }
 
   // Global fl(1/d) table for batches whose longest row exceeds the fixup's
@@ -558,10 +578,7 @@ void run_sectors(sks_context* ctx, const float* d_dem, int dimy, int dimx, doubl
     ScanArgs a = ctx->scan_args(b, bd, cfg->h0, st);
     a.force_exact = force_exact ? 1 : 0;
     if (stats) cuda_check(cudaEventRecord(ctx->ev[0], st), "event");
-    if (!fused) {
-      cuda_check(launch_relocate_grid(d_dem, bd, b.tiles_x, b.tiles_total, st), "launch relocate");
-      ++ctx->launches;
-    }
+    if (!fused) ctx->relocate(d_dem, dimy, dimx, bd, b, st);
     if (stats) cuda_check(cudaEventRecord(ctx->ev[1], st), "event");
     ctx->scan_batch(b, a, st, false, false);
     if (stats) cuda_check(cudaEventRecord(ctx->ev[2], st), "event");
@@ -972,8 +989,8 @@ void debug_relocate(sks_context* ctx, Batch& b, const float* grid, size_t grid_e
   cuda_check(cudaMemsetAsync(ctx->sdem.p, 0, static_cast<size_t>(b.pool_elems) * sizeof(float), st),
              "memset sdem");
   BatchDev bd = ctx->batch_dev(b, false);
-  cuda_check(launch_relocate_grid(ctx->dem.as<float>(), bd, b.tiles_x, b.tiles_total, st),
-             "launch relocate");
+  const SectorDev& s0 = b.sdev[0];
+  ctx->relocate(ctx->dem.as<float>(), s0.src_rows, s0.src_cols, bd, b, st);
   const SectorDev& sd = b.sdev[0];
   cuda_check(cudaMemcpy2DAsync(values, sizeof(float) * sd.cols, ctx->sdem.p, sizeof(float) * sd.pitch,
                                sizeof(float) * sd.cols, sd.skw_rows, cudaMemcpyDeviceToHost, st),

@@ -116,7 +116,10 @@ struct Layout2 {
 };
 
 // control block of one slot (ints)
-enum : int { kWord = 0, kRemaining, kDead, kS, kQ, kL, kFirst, kCap, kItem };
+// kBar: the slot's mbarrier (8-byte aligned: slot blocks are 64 B apart) for
+// the TMA bulk copy of its rows; kLoads: rows loaded into the slot so far
+// (the barrier phase parity)
+enum : int { kWord = 0, kRemaining, kDead, kS, kQ, kL, kFirst, kCap, kItem, kLoads, kBar = 10 };
 
 struct Slot {
   const float* S;
@@ -227,9 +230,33 @@ __device__ void load_slot(const ScanArgs& a, int* ctl, float* base, const Layout
       }
     }
   } else {
+#ifdef SKS_NO_TMA
     const float* src = a.b.sdem + row0;
 #pragma unroll 4
     for (int x = lane; x < lay.lb; x += 32) S[x] = x < L ? __ldg(src + x) : ninf;
+#else
+    // TMA bulk copy of the row into the R buffer (free: it is rebuilt from S
+    // below). The copy starts at the 16-byte boundary below the row start
+    // (sdem_off and pitch are multiples of 32 floats, so the shift is
+    // rg.x & 3) and ends at the next boundary after it: within the row's
+    // pitch in global memory and within lb >= lmax + 64 floats here. One
+    // lane issues it on the slot's mbarrier; the warp waits on the phase.
+    const int sh = rg.x & 3;
+    const unsigned bytes = static_cast<unsigned>(((sh + L + 3) & ~3) * 4);
+    uint64_t* bar = reinterpret_cast<uint64_t*>(ctl + kBar);
+    volatile int* vl = ctl;
+    const unsigned parity = static_cast<unsigned>(vl[kLoads]) & 1u;
+    __syncwarp();
+    if (lane == 0) {
+      vl[kLoads] = vl[kLoads] + 1;
+      // R was last read through the generic proxy (the previous row's tasks)
+      fence_proxy_async();
+      mbar_expect_tx(bar, bytes);
+      tma_bulk_g2s(R, a.b.sdem + (row0 - sh), bytes, bar);
+    }
+    mbar_wait(bar, parity);
+    for (int x = lane; x < lay.lb; x += 32) S[x] = x < L ? R[x + sh] : ninf;
+#endif
   }
   __syncwarp();
   for (int x = lane; x < lay.lb; x += 32) R[x] = x < L ? S[L - 1 - x] : ninf;
@@ -637,6 +664,8 @@ __global__ void __launch_bounds__(kThr, 1) scan2_kernel(const __grid_constant__ 
     smem[lay.copy(r) + j] = d >= 1 ? __frcp_rn(static_cast<float>(d)) : qnan;
   }
   for (int i = tid; i < kMaxSlots * kCtlInts; i += blockDim.x) ctl_all[i] = 0;
+  __syncthreads();
+  if (tid < nslots) mbar_init(reinterpret_cast<uint64_t*>(ctl_all + tid * kCtlInts + kBar), 1);
   __syncthreads();
   if (warp < nslots) load_slot(a, ctl_all + warp * kCtlInts, slots + warp * lay.slot, lay, lane);
 

@@ -100,8 +100,12 @@ __host__ __device__ inline unsigned pack_fix(unsigned dir, unsigned g) { return 
 
 // Kernel entry points (launch wrappers). All return the launch error.
 // grid: (tiles_total, n_sectors); tile t -> (t / tiles_x, t % tiles_x)
-int launch_relocate_grid(const float* dem, const BatchDev& b, int tiles_x,
-                         int tiles_total, void* stream);
+// dem: dem_rows x dem_cols floats with a row pitch of dem_pitch floats; the
+// base 16-byte aligned and dem_pitch a multiple of relocate_dem_align() (the
+// TMA tensor maps' stride rule); else cudaErrorMisalignedAddress.
+int launch_relocate_grid(const float* dem, int dem_rows, int dem_cols, long long dem_pitch,
+                         const BatchDev& b, int tiles_x, int tiles_total, void* stream);
+int relocate_dem_align();
 int relocate_tile_rows();
 int relocate_tile_cols();
 int launch_fixup(const ScanArgs& a, unsigned* off, void* stream);  // fixup.cu (off: n_items + 1)

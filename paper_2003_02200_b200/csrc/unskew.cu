@@ -90,6 +90,15 @@ constexpr int kTR = kUT + 1;  // staged source rows (the tile's rows + the row a
 #define SKS_UNSKEW_MINB 5  // CTAs per SM (48 registers)
 #endif
 
+// Per-sector constants of a staged buffer (written by thread 0 with the
+// staging, read as shared broadcasts).
+struct USect {
+  int iv[6];
+  int rows, i_lo, j_lo;
+  int fast;  // every cell of the tile is interior in pre_ops space (1 <= i <= rows-2)
+  double corr;
+};
+
 template <bool kBlocks>  // row-block sharding: some tiles own no row of a sector
 __global__ void __launch_bounds__(256, SKS_UNSKEW_MINB) unskew_pipe_kernel(BatchDev b, double* __restrict__ map, int dimy,
                                                               int dimx) {
@@ -97,39 +106,75 @@ __global__ void __launch_bounds__(256, SKS_UNSKEW_MINB) unskew_pipe_kernel(Batch
   __shared__ int sown[2];  // sector staged in the buffer has owned rows in the tile
   __shared__ int sdest[2][kUT];
   __shared__ double sfrac[2][kUT];
+  __shared__ USect ssec[2];
+  // ring of the next sectors' descriptors (SectorDev copied word by word):
+  // sector s sits in slot s % 3 from iteration s - 2 on
+  constexpr int kSecWords = static_cast<int>(sizeof(SectorDev) / 4);
+  static_assert(sizeof(SectorDev) % 8 == 0, "SectorDev copied as whole words");
+  __shared__ SectorDev sring[3];
+  auto load_sec = [&](int s) {
+    if (threadIdx.x < kSecWords) {
+      reinterpret_cast<int*>(sring + s % 3)[threadIdx.x] =
+          __ldg(reinterpret_cast<const int*>(b.sectors + s) + threadIdx.x);
+    }
+  };
   const int tx = threadIdx.x & 31;
   const int ty = threadIdx.x >> 5;  // 0..7
   const int y0 = blockIdx.y * kUT, x0 = blockIdx.x * kUT;
   const int ye = min(dimy, y0 + kUT) - 1, xe = min(dimx, x0 + kUT) - 1;
+  const bool full_tile = ye == y0 + kUT - 1 && xe == x0 + kUT - 1;
   const int sj = x0 + tx;
-  const unsigned scv_u32 = static_cast<unsigned>(__cvta_generic_to_shared(&scv[0][0][0]));
-  const unsigned sdest_u32 = static_cast<unsigned>(__cvta_generic_to_shared(&sdest[0][0]));
-  const unsigned sfrac_u32 = static_cast<unsigned>(__cvta_generic_to_shared(&sfrac[0][0]));
+  const int sy = y0 + 4 * ty;  // this thread's cells: (sy + u, sj), u = 0..3
   double acc[4];
 #pragma unroll
   for (int u = 0; u < 4; ++u) {
-    const int si = y0 + ty + 8 * u;
+    const int si = sy + u;
     acc[u] = (si < dimy && sj < dimx) ? map[static_cast<long long>(si) * dimx + sj] : 0.0;
   }
   // the tile's pre_ops box of a sector (axis permutations/flips: corners)
-  auto box = [&](const int* iv, int* i_lo, int* j_lo) {
+  auto box = [&](const int* iv, int* i_lo, int* j_lo, int* ni) {
     const int ia = iv[0] * y0 + iv[1] * x0 + iv[2], ib = iv[0] * ye + iv[1] * xe + iv[2];
     const int ja = iv[3] * y0 + iv[4] * x0 + iv[5], jb = iv[3] * ye + iv[4] * xe + iv[5];
     *i_lo = min(ia, ib);
     *j_lo = min(ja, jb);
+    *ni = max(ia, ib) - *i_lo + 1;
     return max(ja, jb) - *j_lo + 1;  // nj
   };
-  auto stage = [&](int s, int bf) {
-    const SectorDev* sdp = b.sectors + s;
+  // Staging is software-pipelined through registers: the loads of sector s+1
+  // are issued before sector s is computed and stored to shared memory after
+  // it, so one barrier per sector separates the stores from the reads.
+  // Thread (tx, ty) stages column tx, T rows ty + 8k (k < 4, plus row 32 for
+  // ty == 0).
+  // The sector constants, dest and frac of sector s go straight to buffer
+  // s & 1, last read while sector s-2 was computed, before the barrier that
+  // precedes this fetch; only the cv values wait in registers.
+  struct Pre {
+    int v[5];
+    int own;
+  };
+  auto fetch = [&](int s, Pre& P) {
+    const int bf = s & 1;
+    const SectorDev& sdp = sring[s % 3];
     int iv[6];
 #pragma unroll
-    for (int k = 0; k < 6; ++k) iv[k] = __ldg(sdp->inv + k);
-    const int base = __ldg(&sdp->base), q_lo = __ldg(&sdp->q_lo), q_hi = __ldg(&sdp->q_hi);
-    const int skw_rows = __ldg(&sdp->skw_rows), pitch = __ldg(&sdp->pitch), col_off = __ldg(&sdp->col_off);
-    const long long sdem_off = __ldg(&sdp->sdem_off);
-    const double tan = __ldg(&sdp->shear_tan);
-    int i_lo, j_lo;
-    const int nj = box(iv, &i_lo, &j_lo);
+    for (int k = 0; k < 6; ++k) iv[k] = sdp.inv[k];
+    const int base = sdp.base, q_lo = sdp.q_lo, q_hi = sdp.q_hi;
+    const int skw_rows = sdp.skw_rows, pitch = sdp.pitch, col_off = sdp.col_off;
+    const long long sdem_off = sdp.sdem_off;
+    const double tan = sdp.shear_tan;
+    int i_lo, j_lo, ni;
+    const int nj = box(iv, &i_lo, &j_lo, &ni);
+    if (threadIdx.x == 0) {
+      USect& c = ssec[bf];
+#pragma unroll
+      for (int k = 0; k < 6; ++k) c.iv[k] = iv[k];
+      const int rows = sdp.rows;
+      c.rows = rows;
+      c.i_lo = i_lo;
+      c.j_lo = j_lo;
+      c.fast = full_tile && i_lo >= 1 && i_lo + ni - 1 <= rows - 2;
+      c.corr = sdp.correction;
+    }
     bool own = true;
     if (kBlocks && !(q_lo <= 0 && q_hi >= skw_rows)) {
       // none of the skewed rows the tile reads may belong to this run
@@ -138,95 +183,129 @@ __global__ void __launch_bounds__(256, SKS_UNSKEW_MINB) unskew_pipe_kernel(Batch
       const int p_min = base + i_lo - 1 - d_hi, p_max = base + i_lo + kUT - 1 - d_lo;
       own = max(p_min, q_lo) <= min(p_max, q_hi - 1);
     }
+    P.own = own;
     if (kBlocks && threadIdx.x == 0) sown[bf] = own ? 1 : 0;
-    if (!own) return;
-    if (threadIdx.x < nj) {
-      asm volatile("cp.async.ca.shared.global [%0], [%1], 4;\n" ::"r"(sdest_u32 + 4u * (bf * kUT + threadIdx.x)),
-                   "l"(b.dest + col_off + j_lo + threadIdx.x));
-      asm volatile("cp.async.ca.shared.global [%0], [%1], 8;\n" ::"r"(sfrac_u32 + 8u * (bf * kUT + threadIdx.x)),
-                   "l"(b.fracd + col_off + j_lo + threadIdx.x));
+    if (threadIdx.x < nj && own) {
+      sdest[bf][threadIdx.x] = __ldg(b.dest + col_off + j_lo + threadIdx.x);
+      sfrac[bf][threadIdx.x] = __ldg(b.fracd + col_off + j_lo + threadIdx.x);
     }
-    if (tx < nj) {
+#pragma unroll
+    for (int k = 0; k < 5; ++k) P.v[k] = 0;
+    if (tx < nj && own) {
       const int j = j_lo + tx;
       const int dj = __double2int_rz(__dmul_rn(tan, static_cast<double>(j)));
-      const int* col = b.cv + sdem_off + j;
-      const int p0 = base + i_lo - 1 - dj;  // skewed row of T row 0
-      for (int ir = ty; ir < kTR; ir += 8) {
-        const int p = p0 + ir;
-        const unsigned dst = scv_u32 + 4u * ((bf * kTR + ir) * (kUT + 1) + tx);
-        if (p >= q_lo && p < q_hi && p >= 0 && p < skw_rows) {
-          asm volatile("cp.async.ca.shared.global [%0], [%1], 4;\n" ::"r"(dst), "l"(col + static_cast<long long>(p) * pitch));
-        } else {
-          scv[bf][ir][tx] = 0;  // outside the sector or another run's row
-        }
+      const int p0 = base + i_lo - 1 - dj + ty;  // skewed row of T row ty
+      const int plo = max(q_lo, 0), phi = min(q_hi, skw_rows);  // staged rows [plo, phi)
+      const int* col = b.cv + sdem_off + j + static_cast<long long>(p0) * pitch;
+      const int step = 8 * pitch;
+#pragma unroll
+      for (int k = 0; k < 5; ++k) {
+        const int p = p0 + 8 * k;
+        if ((k < 4 || ty == 0) && p >= plo && p < phi) P.v[k] = __ldg(col);
+        col += step;
       }
     }
   };
-  stage(0, 0);
-  asm volatile("cp.async.commit_group;\n" ::);
+  auto commit = [&](const Pre& P, int bf) {
+    if (!P.own) return;
+#pragma unroll
+    for (int k = 0; k < 5; ++k) {
+      if (k < 4 || ty == 0) scv[bf][ty + 8 * k][tx] = P.v[k];
+    }
+  };
+  Pre P;
+  load_sec(0);
+  if (b.n_sectors > 1) load_sec(1);
+  __syncthreads();
+  fetch(0, P);
   for (int s = 0; s < b.n_sectors; ++s) {
     const int bf = s & 1;
-    if (s + 1 < b.n_sectors) {
-      stage(s + 1, bf ^ 1);
-      asm volatile("cp.async.commit_group;\n" ::);
-      asm volatile("cp.async.wait_group 1;\n" ::: "memory");
-    } else {
-      asm volatile("cp.async.wait_group 0;\n" ::: "memory");
-    }
-    __syncthreads();  // sector s's buffer complete for every thread
-    if (kBlocks && sown[bf] == 0) {
-      __syncthreads();
-      continue;
-    }
-    const SectorDev* sdp = b.sectors + s;
-    int iv[6];
+    commit(P, bf);
+    __syncthreads();  // sector s staged; sector s-1's buffer (bf ^ 1) no longer read
+    // slot (s+2) % 3 held sector s-1, last read by fetch(s-1) before this barrier
+    if (s + 2 < b.n_sectors) load_sec(s + 2);
+    if (s + 1 < b.n_sectors) fetch(s + 1, P);
+    if (kBlocks && sown[bf] == 0) continue;
+    const USect& c = ssec[bf];
+    const int iv0 = c.iv[0], iv1 = c.iv[1], iv2 = c.iv[2], iv3 = c.iv[3], iv4 = c.iv[4], iv5 = c.iv[5];
+    const int i_lo = c.i_lo, j_lo = c.j_lo;
+    const double corr = c.corr;
+    const int i0 = iv0 * sy + iv1 * sj + iv2;  // pre_ops cell of (sy, sj); (sy + u, sj) adds u * (iv0, iv3)
+    const int j0 = iv3 * sy + iv4 * sj + iv5;
+    if (c.fast) {
+      // Interior cells: both covered() weights are fl(fl(1-r)+r), within
+      // 2^-52 of 1, so both flags hold (skew.cpp:233-240) and every cell
+      // interpolates v = fl(fl(omr*fl(cv_p*corr)) + fl(r*fl(cv_{p-1}*corr))).
+      if (iv0 != 0) {
+        // pre_ops row i = iv0*si + ..: the 4 cells are 4 consecutive rows of
+        // one column j, reading 5 consecutive staged rows
+        const int jl = j0 - j_lo;
+        const double r = sfrac[bf][jl];
+        const double omr = __dsub_rn(1.0, r);
+        const int ir0 = i0 - i_lo + 1;        // T row of cell 0's p
+        const int rb = min(ir0, ir0 + 3 * iv0) - 1;  // first of the 5 T rows
+        double va[5];
 #pragma unroll
-    for (int k = 0; k < 6; ++k) iv[k] = __ldg(sdp->inv + k);
-    const int rows = __ldg(&sdp->rows);
-    const double corr = __ldg(&sdp->correction);
-    int i_lo, j_lo;
-    box(iv, &i_lo, &j_lo);
-    // cell u of this thread: si = y0 + ty + 8u, sj fixed; (i, j) step by 8 * (iv[0], iv[3])
-    const int i0 = iv[0] * (y0 + ty) + iv[1] * sj + iv[2];
-    const int j0 = iv[3] * (y0 + ty) + iv[4] * sj + iv[5];
+        for (int k = 0; k < 5; ++k) va[k] = __dmul_rn(static_cast<double>(scv[bf][rb + k][jl]), corr);
 #pragma unroll
-    for (int u = 0; u < 4; ++u) {
-      const int si = y0 + ty + 8 * u;
-      if (si >= dimy || sj >= dimx) continue;
-      const int i = i0 + 8 * u * iv[0];
-      const int j = j0 + 8 * u * iv[3];
-      const int jl = j - j_lo;
-      const int ir = i - i_lo + 1;  // T row of p; p - 1 is T row ir - 1
-      const double r = sfrac[bf][jl];
-      const double omr = __dsub_rn(1.0, r);
-      const double w_p = (i + 1 < rows) ? __dadd_rn(omr, r) : omr;
-      const double w_m = (i >= 1) ? __dadd_rn(omr, r) : r;
-      const bool a = full_d(w_p);
-      const bool c = full_d(w_m);
-      double va = 0.0, vb = 0.0;
-      if (a) va = __dmul_rn(static_cast<double>(scv[bf][ir][jl]), corr);
-      if (!a || c) vb = __dmul_rn(static_cast<double>(scv[bf][ir - 1][jl]), corr);
-      if (!a && !c && b.dem != nullptr) {
-        const SectorDev& sd = b.sectors[s];
-        const int p = sd.base + i - sdest[bf][jl];
-        const int2 rg = (p >= 1 && p - 1 < sd.skw_rows) ? __ldg(b.ranges + sd.row_off + p - 1) : make_int2(0, 0);
-        if (j < rg.x || j >= rg.y) vb = 0.0;
-      }
-      double v;
-      if (a && c) {
-        v = __dadd_rn(__dmul_rn(omr, va), __dmul_rn(r, vb));
-      } else if (a) {
-        v = va;
+        for (int u = 0; u < 4; ++u) {
+          // T row of cell u's p relative to rb: ir0 + u*iv0 - rb (1..4)
+          const int ka = iv0 > 0 ? u + 1 : 4 - u;
+          acc[u] = __dadd_rn(acc[u], __dadd_rn(__dmul_rn(omr, va[ka]), __dmul_rn(r, va[ka - 1])));
+        }
       } else {
-        v = vb;
+        // transposed: the 4 cells are 4 consecutive columns of one row i
+        const int ir = i0 - i_lo + 1;
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+          const int jl = j0 + u * iv3 - j_lo;
+          const double r = sfrac[bf][jl];
+          const double omr = __dsub_rn(1.0, r);
+          const double va = __dmul_rn(static_cast<double>(scv[bf][ir][jl]), corr);
+          const double vb = __dmul_rn(static_cast<double>(scv[bf][ir - 1][jl]), corr);
+          acc[u] = __dadd_rn(acc[u], __dadd_rn(__dmul_rn(omr, va), __dmul_rn(r, vb)));
+        }
       }
-      acc[u] = __dadd_rn(acc[u], v);
+    } else {
+      const int rows = c.rows;
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        const int si = sy + u;
+        if (si >= dimy || sj >= dimx) continue;
+        const int i = i0 + u * iv0;
+        const int j = j0 + u * iv3;
+        const int jl = j - j_lo;
+        const int ir = i - i_lo + 1;  // T row of p; p - 1 is T row ir - 1
+        const double r = sfrac[bf][jl];
+        const double omr = __dsub_rn(1.0, r);
+        const double w_p = (i + 1 < rows) ? __dadd_rn(omr, r) : omr;
+        const double w_m = (i >= 1) ? __dadd_rn(omr, r) : r;
+        const bool a = full_d(w_p);
+        const bool cc = full_d(w_m);
+        double va = 0.0, vb = 0.0;
+        if (a) va = __dmul_rn(static_cast<double>(scv[bf][ir][jl]), corr);
+        if (!a || cc) vb = __dmul_rn(static_cast<double>(scv[bf][ir - 1][jl]), corr);
+        if (!a && !cc && b.dem != nullptr) {
+          const SectorDev& sd = b.sectors[s];
+          const int p = sd.base + i - sdest[bf][jl];
+          const int2 rg = (p >= 1 && p - 1 < sd.skw_rows) ? __ldg(b.ranges + sd.row_off + p - 1) : make_int2(0, 0);
+          if (j < rg.x || j >= rg.y) vb = 0.0;
+        }
+        double v;
+        if (a && cc) {
+          v = __dadd_rn(__dmul_rn(omr, va), __dmul_rn(r, vb));
+        } else if (a) {
+          v = va;
+        } else {
+          v = vb;
+        }
+        acc[u] = __dadd_rn(acc[u], v);
+      }
     }
-    __syncthreads();  // buffer bf free before sector s+2 is staged into it
   }
 #pragma unroll
   for (int u = 0; u < 4; ++u) {
-    const int si = y0 + ty + 8 * u;
+    const int si = sy + u;
     if (si < dimy && sj < dimx) map[static_cast<long long>(si) * dimx + sj] = acc[u];
   }
 }
