@@ -627,7 +627,8 @@ def make_bench_report(dataset: str, dimy: int, dimx: int, cfg: RunConfig, stats:
                     stats.reduce_seconds, stats.total_seconds)
     r.povs_per_second = float(dimy) * float(dimx) * float(cfg.ns // 2) / scan if scan > 0 else float("inf")
     if baseline_total_seconds > 0.0:
-        r.speedup = baseline_total_seconds / r.total_seconds
+        # C++ double division (bench.cpp:25): a zero total gives inf, not an exception
+        r.speedup = baseline_total_seconds / r.total_seconds if r.total_seconds != 0.0 else float("inf")
     return r
 
 

@@ -130,6 +130,9 @@ def test_bench_report_format_matches_reference_layout():
     assert "povs_per_second: %.17g" % (2000.0 * 2000.0 * 90 / 0.062) in text
     assert text.endswith("speedup: %.17g\n" % (70.0 / 0.07))
     assert "speedup" not in sk.format_bench_report(sk.make_bench_report("x", 2, 2, cfg, st))
+    # stats without a total (per-part runs): C++'s division gives inf, no exception
+    st.total_seconds = 0.0
+    assert sk.make_bench_report("x", 2, 2, cfg, st, baseline_total_seconds=1.0).speedup == float("inf")
 
 
 def test_cpp_facade_host_utilities(tmp_path):
