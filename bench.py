@@ -390,6 +390,7 @@ def run_ours(args, world, rank, local):
     total_ms = max_over_ranks(total_ms, world)
     scan_s = max_over_ranks(phases["scan"], world)
     skew_s = max_over_ranks(phases["skew"], world)
+    unskew_s = max_over_ranks(phases["unskew"], world)
     evals_all = sum_over_ranks(evals, world)
     launches_all = int(sum_over_ranks(launches, world))
     flagged_all = int(sum_over_ranks(flagged, world))
@@ -438,17 +439,24 @@ def run_ours(args, world, rank, local):
     fp32_peak = props.multi_processor_count * 128 * sm_max * 1e6  # lane-ops/s
     scan_achieved = 4.0 * evals_all / max(scan_s, 1e-12) if world == 1 else 4.0 * evals_all / max(scan_s * world, 1e-12)
     traffic = None
-    reloc_traffic = None
+    reloc_traffic = unskew_traffic = None
+    issue_active = None
     prof = os.path.join(ROOT, "profiles", "ncu_summary.json")
     if os.path.exists(prof):  # dram read+write bytes per launch from one ncu --set full capture
         try:
             with open(prof) as f:
                 nsum = json.load(f)
-            traffic = nsum.get("scan_kernel", {}).get("dram_bytes_per_launch")
-            reloc_traffic = nsum.get("relocate_kernel", {}).get("dram_bytes_per_launch")
+            same = nsum.get("config") == cfgid and nsum.get("terrain") == args.terrain
+            traffic = nsum.get("scan_kernel", {}).get("dram_bytes_per_launch") if same else None
+            issue_active = nsum.get("scan_kernel", {}).get("issue_active") if same else None
+            reloc_traffic = nsum.get("relocate_kernel", {}).get("dram_bytes_per_launch") if same else None
+            unskew_traffic = nsum.get("unskew_kernel", {}).get("dram_bytes_per_launch") if same else None
         except Exception:
-            traffic = reloc_traffic = None
+            traffic = reloc_traffic = unskew_traffic = issue_active = None
     reloc_bytes = 8.0 * n * n * (ns // 2) * args.steps / world
+    # unskew: 4 B of cv per cell and sector + the FP64 map read and written once
+    unskew_bytes = (4.0 * (ns // 2) + 16.0) * n * n * args.steps / world
+    executed = 4.0 * (evals_all - skipped_all) / max(scan_s * (world if world > 1 else 1), 1e-12)
     line = {
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": ms_per_step, "higher_is_better": True, "scaling": "strong",
@@ -464,12 +472,16 @@ def run_ours(args, world, rank, local):
         "roofline": {"kernel": "scan_kernel (FP32-issue bound)", "bound": "fp32",
                      "achieved": scan_achieved / 1e12, "peak": fp32_peak / 1e12, "unit": "TFLOP/s",
                      "frac": scan_achieved / fp32_peak, "traffic": traffic,
+                     "executed_frac": executed / fp32_peak,
+                     "issue_active": issue_active,
                      "note": (f"4 algorithmic FP32 ops per target evaluation (SURVEY 8d) x "
                               f"{evals_all / args.steps:.4g} evals/step / scan-kernel CUDA-event time; peak = "
                               f"{props.multi_processor_count} SMs x 128 lanes x {sm_max:g} MHz (sm_max). "
                               f"{100.0 * skipped_all / max(evals_all, 1):.1f}% of the evaluations were decided "
                               f"(hidden, certified) by the hidden-block skip test without per-target FP32 work; "
-                              f"they are counted as evaluated")},
+                              f"they are counted as evaluated. executed_frac counts only the evaluations the "
+                              f"kernel performed; issue_active is the scan kernel's smsp issue-active fraction "
+                              f"from the committed ncu capture of this workload (profiles/ncu_summary.json)")},
         "roofline_relocation": {"kernel": "relocate_kernel", "bound": "hbm",
                                 "achieved": reloc_bytes / max(skew_s, 1e-12) / 1e9,
                                 "peak": float(peaks.get("hbm_gbs", 6650.0)), "unit": "GB/s",
@@ -477,6 +489,13 @@ def run_ours(args, world, rank, local):
                                 "peak_kind": peak_kind, "traffic": reloc_traffic,
                                 "note": ("algorithmic 8N bytes per sector (read N, write N covered cells); the "
                                          "kernel also zeroes the N cv cells it covers (4N more written)")},
+        "roofline_unskew": {"kernel": "unskew_pipe_kernel", "bound": "hbm",
+                            "achieved": unskew_bytes / max(unskew_s, 1e-12) / 1e9,
+                            "peak": float(peaks.get("hbm_gbs", 6650.0)), "unit": "GB/s",
+                            "frac": unskew_bytes / max(unskew_s, 1e-12) / 1e9
+                            / float(peaks.get("hbm_gbs", 6650.0)),
+                            "peak_kind": peak_kind, "traffic": unskew_traffic,
+                            "note": "algorithmic 4 B of cv per cell and sector + 16 B of FP64 map per cell"},
         "phase_ms_per_step": {k: v * 1e3 / args.steps for k, v in phases.items()},
         "target_evals_per_s": evals_all / args.steps / (ms_per_step * 1e-3),
         "flagged_groups_per_step": flagged_all / args.steps,

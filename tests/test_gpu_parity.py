@@ -41,6 +41,8 @@ def b64(a):
     ((33, 33), sk.SyntheticKind.Cone, 360),
     ((2, 2), sk.SyntheticKind.Ramp, 8),
     ((130, 70), sk.SyntheticKind.Fractal, 24),
+    # interior and edge tiles of the TMA pipeline, an odd DEM width (pitched copy)
+    ((203, 181), sk.SyntheticKind.Fractal, 12),
 ])
 def test_relocation_bitexact_every_sector(ora, shape, kind, ns):
     dem = sk.make_synthetic(kind, *shape, 10.0, 7).values
