@@ -23,6 +23,8 @@
 #include <cuda_runtime.h>
 
 #include <cfloat>
+#include <cstdlib>
+#include <string>
 #include <algorithm>
 #include <cstdint>
 
@@ -386,6 +388,255 @@ __global__ void __launch_bounds__(kWarps * 32, SKS_FIX_MINB) fixup_kernel(ScanAr
   }
 }
 
+// ---------------------------------------------------------------------------
+// Warp-per-POV fixup (opt-in, SKS_FIXUP=warp; measured 2-3x slower than the
+// thread-per-POV kernel: config 2 fixup 3.79 vs 1.79 ms, config 4 65.9 vs
+// 30.1 ms, config 5 5.88 vs 2.01 s — each 32-target step is a chain of
+// shuffles plus an L2 round trip, and 32 warps per SM keep too few steps in
+// flight; the thread kernel's 512 independent POVs per SM hide the latency
+// better). The thread-per-POV kernel above keeps 512
+// POVs in flight per SM but its lanes diverge: each POV skips its own blocks,
+// so only ~11 of 32 lanes are busy in eval_block (ncu, round 1), and its cost
+// grows with the row length (config 5: 32 % of the step). Here a warp takes
+// one POV and walks its targets 32 at a time:
+//   * skip: each lane tests one 16-target window of the next 32 (512 targets)
+//     with the same exact bound as exact_pov; candidates are re-tested
+//     against lo as it rises and evaluated two windows per step;
+//   * step: lane i holds target i of the step (in scan order) and computes
+//     the certified FP32 t; the state before lane i is R_i = max(R, t of the
+//     lanes before i) (the FP32 value of the last record when every earlier
+//     decision was certain: a record's t exceeds the previous hi, a hidden
+//     target's t lies below lo), an exclusive warp max-scan; record if
+//     t > hi(R_i), hidden if t < lo(R_i), else the first such band lane is
+//     decided with the reference's FP64 operations against the exact max
+//     (theta of the last record, computed lazily) and the lanes after it are
+//     re-run from the resolved state.
+// Every decision that reaches cv is the reference's (scan.cpp:24-34), as in
+// exact_pov; POVs whose h does not split run the FP64 recurrence with an FP64
+// warp max-scan.
+__device__ __forceinline__ float warp_excl_max(float v, int lane) {
+  float incl = v;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const float u = __shfl_up_sync(0xffffffffu, incl, o);
+    if (lane >= o) incl = fmaxf(incl, u);
+  }
+  const float ex = __shfl_up_sync(0xffffffffu, incl, 1);
+  return lane == 0 ? -INFINITY : ex;
+}
+
+__device__ __forceinline__ double warp_excl_max_d(double v, int lane) {
+  double incl = v;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const double u = __shfl_up_sync(0xffffffffu, incl, o);
+    if (lane >= o) incl = fmax(incl, u);
+  }
+  const double ex = __shfl_up_sync(0xffffffffu, incl, 1);
+  return lane == 0 ? -INFINITY : ex;
+}
+
+struct WarpState {
+  float hf, hl;
+  double h;
+  float R;        // FP32 t of the last record (-inf: none yet)
+  int r;          // its dd (0: none)
+  double M;       // exact max theta when Mvalid
+  bool Mvalid;
+  int cv;         // this lane's share of the ring sum
+};
+
+__device__ __forceinline__ float lo_of(float R) { return R == -INFINITY ? -FLT_MAX : __fmaf_rn(fabsf(R), -kBand, R); }
+
+// One step: lane i holds target dd (valid: act), elevation e, certified t.
+__device__ __forceinline__ void warp_step(WarpState& S, const float* row, int x, int sg, bool act, int dd, float e,
+                                          float t, int lane) {
+  int start = 0;
+  for (;;) {
+    const bool mine = act && lane >= start;
+    const float Ri = fmaxf(S.R, warp_excl_max(mine ? t : -INFINITY, lane));
+    bool rec, band;
+    if (Ri == -INFINITY) {
+      rec = mine;  // nothing seen yet: every finite target is above -inf
+      band = false;
+    } else {
+      const float at = fabsf(Ri);
+      rec = mine && t > __fmaf_rn(at, kBand, Ri);
+      band = mine && !rec && t >= __fmaf_rn(at, -kBand, Ri);
+    }
+    const unsigned bm = __ballot_sync(0xffffffffu, band);
+    const int stop = bm ? __ffs(bm) - 1 : 32;
+    const bool take = rec && lane < stop;
+    const unsigned rm = __ballot_sync(0xffffffffu, take);
+    if (take) S.cv += 2 * dd + 1;
+    if (rm) {
+      const int last = 31 - __clz(rm);
+      S.R = __shfl_sync(0xffffffffu, t, last);
+      S.r = __shfl_sync(0xffffffffu, dd, last);
+      S.Mvalid = false;
+    }
+    if (stop == 32) return;
+    // the first band target, decided exactly (scan.cpp:24-25): theta against
+    // the exact running max, theta of the last record r
+    const float eb = __shfl_sync(0xffffffffu, e, stop);
+    const int db = __shfl_sync(0xffffffffu, dd, stop);
+    const float tb = __shfl_sync(0xffffffffu, t, stop);
+    const double th = __ddiv_rn(__dsub_rn(static_cast<double>(eb), S.h), static_cast<double>(db));
+    if (!S.Mvalid) {
+      S.M = S.r == 0 ? -INFINITY
+                     : __ddiv_rn(__dsub_rn(static_cast<double>(__ldg(row + x + sg * S.r)), S.h),
+                                 static_cast<double>(S.r));
+      S.Mvalid = true;
+    }
+    if (th > S.M) {
+      if (lane == stop) S.cv += 2 * db + 1;
+      S.M = th;
+      S.R = tb;
+      S.r = db;
+    }
+    start = stop + 1;
+  }
+}
+
+// cv of one POV (every lane returns the same value).
+__device__ int warp_pov(const float* row, const float* wm, const float* ivt, int x, int sg, int D, double h,
+                        bool force_exact, int lane) {
+  WarpState S;
+  S.h = h;
+  S.hf = __double2float_rn(h);
+  const double hld = __dsub_rn(h, static_cast<double>(S.hf));
+  S.hl = __double2float_rn(hld);
+  S.R = -INFINITY;
+  S.r = 0;
+  S.M = -INFINITY;
+  S.Mvalid = true;
+  S.cv = 0;
+  if (D < 1) return 0;
+  const bool exact_all = force_exact || static_cast<double>(S.hl) != hld || !(fabsf(S.hf) < 1e30f);
+  if (exact_all || wm == nullptr) {
+    // the FP64 recurrence, 32 targets per step (an FP64 max-scan)
+    double M = -INFINITY;
+    int cv = 0;
+    for (int d0 = 1; d0 <= D; d0 += 32) {
+      const int dd = d0 + lane;
+      const bool act = dd <= D;
+      const double th = act ? __ddiv_rn(__dsub_rn(static_cast<double>(__ldg(row + x + sg * dd)), h),
+                                        static_cast<double>(dd))
+                            : -INFINITY;
+      const double Mi = fmax(M, warp_excl_max_d(th, lane));
+      if (act && th > Mi) cv += 2 * dd + 1;
+      M = fmax(Mi, th);
+      M = __shfl_sync(0xffffffffu, M, 31);
+    }
+    return __reduce_add_sync(0xffffffffu, cv);
+  }
+  // 16-target windows in scan order (row positions 16w .. 16w+15)
+  const int pfirst = x + sg, plast = x + sg * D;
+  const int w0 = pfirst >> 4, w1 = plast >> 4;
+  const int nblk = (w1 - w0) * sg + 1;
+  for (int b0 = 0; b0 < nblk; b0 += 32) {
+    const int j = b0 + lane;
+    const bool valid = j < nblk;
+    float B = INFINITY;  // max slope bound of window j (+inf: not a window)
+    if (valid) {
+      const int w = w0 + sg * j;
+      const int da = max(1, sg > 0 ? 16 * w - x : x - (16 * w + 15));
+      const int db = min(D, sg > 0 ? 16 * w + 15 - x : x - 16 * w);
+      const float N = __fadd_rn(__fsub_rn(__ldg(wm + w), S.hf), -S.hl);
+      B = fmaxf(__fmul_rn(N, ivt[da]), __fmul_rn(N, ivt[db]));
+    }
+    unsigned pend = __ballot_sync(0xffffffffu, valid);
+    for (;;) {
+      // candidates against the current lo (it only rises: re-tested each step)
+      const unsigned cand = __ballot_sync(0xffffffffu, !(B < lo_of(S.R))) & pend;
+      if (cand == 0) break;
+      const int ja = __ffs(cand) - 1;
+      const unsigned rest = cand & (cand - 1);
+      const int jb = rest ? __ffs(rest) - 1 : -1;
+      pend &= ~(1u << ja);
+      if (jb >= 0) pend &= ~(1u << jb);
+      // lanes 0-15: window ja, 16-31: window jb (scan order within each)
+      const int jj = lane < 16 ? ja : jb;
+      const int w = w0 + sg * (b0 + jj);
+      const int pos = sg > 0 ? 16 * w + (lane & 15) : 16 * w + 15 - (lane & 15);
+      const int dd = sg * (pos - x);
+      const bool act = jj >= 0 && dd >= 1 && dd <= D;
+      const float e = act ? __ldg(row + pos) : 0.f;
+      const float t = act ? __fmul_rn(__fadd_rn(__fsub_rn(e, S.hf), -S.hl), ivt[dd]) : -INFINITY;
+      warp_step(S, row, x, sg, act, dd, e, t, lane);
+    }
+  }
+  return __reduce_add_sync(0xffffffffu, S.cv);
+}
+
+// the sequential form for the debug POV (outlined: keeps the warp kernel's registers)
+__device__ __noinline__ int exact_pov_dbg(const float* row, const float* wm, const float* ivt, int x, int sg, int D,
+                                          double h, bool force_exact, uint8_t* vis) {
+  return exact_pov(row, wm, ivt, x, sg, D, h, force_exact, vis);
+}
+
+#ifndef SKS_FIXW_MINB
+#define SKS_FIXW_MINB 4
+#endif
+template <bool kSmemTab>
+__global__ void __launch_bounds__(kWarps * 32, SKS_FIXW_MINB) fixup_warp_kernel(ScanArgs a, int tab_len,
+                                                                              const unsigned* off) {
+  extern __shared__ __align__(16) float ivt_s[];  // fl(1/d), d = 0 .. tab_len - 1
+  if (kSmemTab) {
+    for (int d = threadIdx.x; d < tab_len; d += blockDim.x) ivt_s[d] = __frcp_rn(static_cast<float>(d));
+    __syncthreads();
+  }
+  const float* ivt = kSmemTab ? ivt_s : a.ivt;
+  const int lane = threadIdx.x & 31;
+  const unsigned grp = static_cast<unsigned>(a.fix_group);
+  const unsigned total = off[a.n_items];
+  const unsigned nwarps = gridDim.x * (blockDim.x >> 5);
+  for (unsigned w = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5); w < total; w += nwarps) {
+    // item: the last it with off[it] <= w (warp-uniform)
+    int lo = 0, hi = a.n_items;
+    while (hi - lo > 1) {
+      const int mid = (lo + hi) >> 1;
+      if (__ldg(off + mid) <= w) lo = mid; else hi = mid;
+    }
+    const int it = lo;
+    const unsigned wj = w - __ldg(off + it);
+    const ScanItem item = a.items[it];
+    const SectorDev& sd = a.b.sectors[item.s];
+    const int2 rg = a.b.ranges[sd.row_off + item.q];
+    const int first = rg.x;
+    const int L = rg.y - rg.x;
+    const long long rowoff = sd.sdem_off + static_cast<long long>(item.q) * sd.pitch;
+    const float* row = a.b.sdem + rowoff + first;
+    const unsigned nf = __ldg(a.fix_cnt + it) & 0xffffu;
+    const unsigned e = wj / grp;
+    const unsigned ent = a.fix_queue[a.fix_off[it] + (e < nf ? e : static_cast<unsigned>(L) + (e - nf))];
+    const int dir = static_cast<int>(ent >> 31);
+    const int y = static_cast<int>((ent & 0x7fffffffu) * grp + wj % grp);
+    if (y >= L) continue;
+    const int x = dir ? (L - 1 - y) : y;
+    const int D = min(sd.max_dd, dir ? x : (L - 1 - x));
+    const bool dbg = a.dbg_j0 >= 0 && item.s == 0 && item.q == 0 && first + x == a.dbg_j0;
+    const double h = dbg ? a.dbg_h : __dadd_rn(static_cast<double>(row[x]), a.h0);
+    const float* wm = a.wm16 != nullptr ? a.wm16 + rowoff / 16 : nullptr;
+    int cv;
+    if (dbg) {
+      // debug capture of the per-target decisions: the sequential form
+      cv = 0;
+      if (lane == 0) {
+        cv = exact_pov_dbg(row, wm, ivt, x, dir ? -1 : 1, D, h, a.force_exact != 0,
+                           dir ? a.dbg_vis_bwd : a.dbg_vis_fwd);
+      }
+      cv = __shfl_sync(0xffffffffu, cv, 0);
+    } else {
+      cv = warp_pov(row, wm, ivt, x, dir ? -1 : 1, D, h, a.force_exact != 0, lane);
+    }
+    if (lane == 0 && cv != 0) {
+      int* dst = ((dir && a.b.cv_bwd) ? a.b.cv_bwd : a.b.cv) + rowoff + first;
+      atomicAdd(dst + x, cv);
+    }
+  }
+}
+
 // Long rows (items [0, n_long)): one CTA per row writes the row's 16-cell
 // window maxima (what scan2's row loader writes for the rows it scans) and
 // queues every POV in both directions (forward entries y = 0 .. L-1 at the
@@ -444,6 +695,23 @@ int launch_fixup(const ScanArgs& a, unsigned* off, void* stream) {
   }
   const int tab_len = ((std::max(a.lmax_all, a.lmax) + 31) / 32) * 32;
   const cudaStream_t st = static_cast<cudaStream_t>(stream);
+  // SKS_FIXUP=warp selects the warp-per-POV kernel (measured slower, kept
+  // for experiments)
+  const char* fx = std::getenv("SKS_FIXUP");
+  const bool thread_kernel = !(fx != nullptr && std::string(fx) == "warp");
+  if (!thread_kernel) {
+    const bool smem_tab = tab_len <= kSmemTabMax;
+    if (!smem_tab && a.ivt == nullptr) return static_cast<int>(cudaErrorInvalidValue);
+    const size_t smem = smem_tab ? static_cast<size_t>(tab_len) * sizeof(float) : 0;
+    auto kern = smem_tab ? fixup_warp_kernel<true> : fixup_warp_kernel<false>;
+    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
+    if (e != cudaSuccess) return static_cast<int>(e);
+    int per_sm = 0;
+    e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, kWarps * 32, smem);
+    if (e != cudaSuccess) return static_cast<int>(e);
+    kern<<<sms * (per_sm > 0 ? per_sm : 1), kWarps * 32, smem, st>>>(a, tab_len, off);
+    return static_cast<int>(cudaGetLastError());
+  }
   if (tab_len <= kSmemTabMax) {
     const size_t smem = static_cast<size_t>(tab_len) * sizeof(float);
     cudaError_t e = cudaFuncSetAttribute(fixup_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,

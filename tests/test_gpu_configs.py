@@ -246,3 +246,37 @@ def test_rows_beyond_int32_ring_sums_rejected():
     dem = sk.Dem(np.zeros((2, 46341), np.float32), 10.0)
     with pytest.raises(ValueError, match="46340"):
         sk.total_viewshed_raw(dem, sk.RunConfig(ns=2))
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("shape,kind,ns,maxd", [
+    ((90, 70), sk.SyntheticKind.Fractal, 36, None),
+    ((64, 80), sk.SyntheticKind.SmoothedNoise, 24, 250.0),
+    ((40, 60), sk.SyntheticKind.Ramp, 8, None),
+])
+def test_warp_fixup_kernel_bitexact(ref, shape, kind, ns, maxd, monkeypatch):
+    """The opt-in warp-per-POV fixup (SKS_FIXUP=warp), fed every POV of the
+    long rows (SKS_LONG_ROW=48) plus the scan's flagged ones: bit-identical
+    raw maps."""
+    monkeypatch.setenv("SKS_FIXUP", "warp")
+    monkeypatch.setenv("SKS_LONG_ROW", "48")
+    dem = sk.make_synthetic(kind, *shape, 10.0, 19)
+    cfg = sk.RunConfig(ns=ns, h0=1.5, max_distance=maxd, units=sk.Units.SquareMeters)
+    theirs = ref.total_viewshed(dem.values, 10.0, ns, 1.5, max_distance=maxd or 0.0, raw=True)
+    ctx = sk.Context(0)
+    ours = ctx.total_viewshed(dem.values, 10.0, cfg, raw=True)
+    assert np.array_equal(b64(ours), b64(theirs))
+    ctx.close()
+
+
+@pytest.mark.gpu
+def test_warp_fixup_kernel_exact_mode(ref, monkeypatch):
+    """SKS_FIXUP=warp on elevations outside the FP32 filter's range: every
+    POV takes the kernel's FP64 path (warp max-scan in FP64), bit-identical."""
+    monkeypatch.setenv("SKS_FIXUP", "warp")
+    base = sk.make_synthetic(sk.SyntheticKind.Fractal, 30, 26, 10.0, 5).values
+    vals = np.ascontiguousarray(base * np.float32(3.0e12), np.float32)
+    cfg = sk.RunConfig(ns=16, h0=0.0, units=sk.Units.SquareMeters)
+    theirs = ref.total_viewshed(vals, 10.0, 16, 0.0, raw=True)
+    ours = sk.total_viewshed_raw(sk.Dem(vals, 10.0), cfg)
+    assert np.array_equal(b64(ours), b64(theirs))
