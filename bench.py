@@ -446,11 +446,11 @@ def run_ours(args, world, rank, local):
         try:
             with open(prof) as f:
                 nsum = json.load(f)
-            same = nsum.get("config") == cfgid and nsum.get("terrain") == args.terrain
-            traffic = nsum.get("scan_kernel", {}).get("dram_bytes_per_launch") if same else None
-            issue_active = nsum.get("scan_kernel", {}).get("issue_active") if same else None
-            reloc_traffic = nsum.get("relocate_kernel", {}).get("dram_bytes_per_launch") if same else None
-            unskew_traffic = nsum.get("unskew_kernel", {}).get("dram_bytes_per_launch") if same else None
+            wl = nsum.get("workloads", {}).get(f"{cfgid}/{args.terrain}", {})
+            traffic = wl.get("scan_kernel", {}).get("dram_bytes_per_launch")
+            issue_active = wl.get("scan_kernel", {}).get("issue_active")
+            reloc_traffic = wl.get("relocate_kernel", {}).get("dram_bytes_per_launch")
+            unskew_traffic = wl.get("unskew_kernel", {}).get("dram_bytes_per_launch")
         except Exception:
             traffic = reloc_traffic = unskew_traffic = issue_active = None
     reloc_bytes = 8.0 * n * n * (ns // 2) * args.steps / world

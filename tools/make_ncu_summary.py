@@ -1,6 +1,6 @@
-"""Writes profiles/ncu_summary.json from one `ncu --set full` capture of a bench
-workload (the per-launch DRAM traffic and issue-active figures bench.py reports
-beside its rooflines).
+"""Merges one `ncu --set full` capture of a bench workload into
+profiles/ncu_summary.json (per config and terrain: the per-launch DRAM traffic
+and issue-active figures bench.py reports beside its rooflines).
 
   python tools/make_ncu_summary.py REPORT.ncu-rep CONFIG TERRAIN "source note"
 """
@@ -28,7 +28,7 @@ def val(d, k):
 
 names = {"scan2_kernel": "scan_kernel", "relocate_kernel": "relocate_kernel", "unskew_pipe_kernel": "unskew_kernel",
          "fixup_kernel": "fixup_kernel"}
-out = {"source": note, "config": cfg, "terrain": terrain}
+out = {"source": note}
 for d in data:
     full = d[hdr.index("Kernel Name")]
     for key, name in names.items():
@@ -51,6 +51,15 @@ for k, v in out.items():
         for kk, vv in v.items():
             if isinstance(vv, float) and math.isnan(vv):
                 v[kk] = None
-with open(os.path.join(ROOT, "profiles", "ncu_summary.json"), "w") as f:
-    json.dump(out, f, indent=1)
+path = os.path.join(ROOT, "profiles", "ncu_summary.json")
+try:
+    with open(path) as f:
+        allsum = json.load(f)
+    if "workloads" not in allsum:
+        allsum = {"workloads": {}}
+except (OSError, ValueError):
+    allsum = {"workloads": {}}
+allsum["workloads"][f"{cfg}/{terrain}"] = out
+with open(path, "w") as f:
+    json.dump(allsum, f, indent=1)
 print(json.dumps(out, indent=1))
