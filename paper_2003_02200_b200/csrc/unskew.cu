@@ -86,8 +86,14 @@ constexpr int kUT = 32;           // tile edge (cells)
 // cp.async into the second buffer while sector s is computed.
 constexpr int kTR = kUT + 1;  // staged source rows (the tile's rows + the row above)
 
+#ifndef SKS_UNSKEW_CPT
+#define SKS_UNSKEW_CPT 8  // cells per thread (8: 128 threads per tile; measured 0.79 ms vs 0.91 with 4, config 2)
+#endif
+constexpr int kCPT = SKS_UNSKEW_CPT;
+constexpr int kNW = kUT / kCPT;                 // warps per CTA (cell rows of kCPT)
+constexpr int kNV = (kTR + kNW - 1) / kNW;     // staged T rows per thread
 #ifndef SKS_UNSKEW_MINB
-#define SKS_UNSKEW_MINB 5  // CTAs per SM (48 registers)
+#define SKS_UNSKEW_MINB (kCPT == 4 ? 5 : 8)  // CTAs per SM (4: 48 registers, 8: 64)
 #endif
 
 // Per-sector constants of a staged buffer (written by thread 0 with the
@@ -100,7 +106,7 @@ struct USect {
 };
 
 template <bool kBlocks>  // row-block sharding: some tiles own no row of a sector
-__global__ void __launch_bounds__(256, SKS_UNSKEW_MINB) unskew_pipe_kernel(BatchDev b, double* __restrict__ map, int dimy,
+__global__ void __launch_bounds__(32 * kNW, SKS_UNSKEW_MINB) unskew_pipe_kernel(BatchDev b, double* __restrict__ map, int dimy,
                                                               int dimx) {
   __shared__ int scv[2][kTR][kUT + 1];
   __shared__ int sown[2];  // sector staged in the buffer has owned rows in the tile
@@ -119,15 +125,15 @@ __global__ void __launch_bounds__(256, SKS_UNSKEW_MINB) unskew_pipe_kernel(Batch
     }
   };
   const int tx = threadIdx.x & 31;
-  const int ty = threadIdx.x >> 5;  // 0..7
+  const int ty = threadIdx.x >> 5;  // 0 .. kNW-1
   const int y0 = blockIdx.y * kUT, x0 = blockIdx.x * kUT;
   const int ye = min(dimy, y0 + kUT) - 1, xe = min(dimx, x0 + kUT) - 1;
   const bool full_tile = ye == y0 + kUT - 1 && xe == x0 + kUT - 1;
   const int sj = x0 + tx;
-  const int sy = y0 + 4 * ty;  // this thread's cells: (sy + u, sj), u = 0..3
-  double acc[4];
+  const int sy = y0 + kCPT * ty;  // this thread's cells: (sy + u, sj), u < kCPT
+  double acc[kCPT];
 #pragma unroll
-  for (int u = 0; u < 4; ++u) {
+  for (int u = 0; u < kCPT; ++u) {
     const int si = sy + u;
     acc[u] = (si < dimy && sj < dimx) ? map[static_cast<long long>(si) * dimx + sj] : 0.0;
   }
@@ -143,13 +149,12 @@ __global__ void __launch_bounds__(256, SKS_UNSKEW_MINB) unskew_pipe_kernel(Batch
   // Staging is software-pipelined through registers: the loads of sector s+1
   // are issued before sector s is computed and stored to shared memory after
   // it, so one barrier per sector separates the stores from the reads.
-  // Thread (tx, ty) stages column tx, T rows ty + 8k (k < 4, plus row 32 for
-  // ty == 0).
+  // Thread (tx, ty) stages column tx, T rows ty + kNW*k (< kTR).
   // The sector constants, dest and frac of sector s go straight to buffer
   // s & 1, last read while sector s-2 was computed, before the barrier that
   // precedes this fetch; only the cv values wait in registers.
   struct Pre {
-    int v[5];
+    int v[kNV];
     int own;
   };
   auto fetch = [&](int s, Pre& P) {
@@ -190,27 +195,31 @@ __global__ void __launch_bounds__(256, SKS_UNSKEW_MINB) unskew_pipe_kernel(Batch
       sfrac[bf][threadIdx.x] = __ldg(b.fracd + col_off + j_lo + threadIdx.x);
     }
 #pragma unroll
-    for (int k = 0; k < 5; ++k) P.v[k] = 0;
+    for (int k = 0; k < kNV; ++k) P.v[k] = 0;
     if (tx < nj && own) {
       const int j = j_lo + tx;
       const int dj = __double2int_rz(__dmul_rn(tan, static_cast<double>(j)));
       const int p0 = base + i_lo - 1 - dj + ty;  // skewed row of T row ty
       const int plo = max(q_lo, 0), phi = min(q_hi, skw_rows);  // staged rows [plo, phi)
-      const int* col = b.cv + sdem_off + j + static_cast<long long>(p0) * pitch;
-      const int step = 8 * pitch;
+      // one 64-bit base per column (T row ty), 32-bit byte offsets from it
+      const char* col = reinterpret_cast<const char*>(b.cv + sdem_off + j + static_cast<long long>(p0) * pitch);
+      unsigned off = 0;
+      const unsigned step = static_cast<unsigned>(kNW * pitch) * 4u;
 #pragma unroll
-      for (int k = 0; k < 5; ++k) {
-        const int p = p0 + 8 * k;
-        if ((k < 4 || ty == 0) && p >= plo && p < phi) P.v[k] = __ldg(col);
-        col += step;
+      for (int k = 0; k < kNV; ++k) {
+        const int p = p0 + kNW * k;
+        if (ty + kNW * k < kTR && static_cast<unsigned>(p - plo) < static_cast<unsigned>(phi - plo)) {
+          P.v[k] = __ldg(reinterpret_cast<const int*>(col + off));
+        }
+        off += step;
       }
     }
   };
   auto commit = [&](const Pre& P, int bf) {
     if (!P.own) return;
 #pragma unroll
-    for (int k = 0; k < 5; ++k) {
-      if (k < 4 || ty == 0) scv[bf][ty + 8 * k][tx] = P.v[k];
+    for (int k = 0; k < kNV; ++k) {
+      if (ty + kNW * k < kTR) scv[bf][ty + kNW * k][tx] = P.v[k];
     }
   };
   Pre P;
@@ -237,27 +246,30 @@ __global__ void __launch_bounds__(256, SKS_UNSKEW_MINB) unskew_pipe_kernel(Batch
       // 2^-52 of 1, so both flags hold (skew.cpp:233-240) and every cell
       // interpolates v = fl(fl(omr*fl(cv_p*corr)) + fl(r*fl(cv_{p-1}*corr))).
       if (iv0 != 0) {
-        // pre_ops row i = iv0*si + ..: the 4 cells are 4 consecutive rows of
-        // one column j, reading 5 consecutive staged rows
+        // pre_ops row i = iv0*si + ..: the cells are consecutive rows of one
+        // column j; each group of 4 reads 5 consecutive staged rows
         const int jl = j0 - j_lo;
         const double r = sfrac[bf][jl];
         const double omr = __dsub_rn(1.0, r);
         const int ir0 = i0 - i_lo + 1;        // T row of cell 0's p
-        const int rb = min(ir0, ir0 + 3 * iv0) - 1;  // first of the 5 T rows
-        double va[5];
 #pragma unroll
-        for (int k = 0; k < 5; ++k) va[k] = __dmul_rn(static_cast<double>(scv[bf][rb + k][jl]), corr);
+        for (int h = 0; h < kCPT / 4; ++h) {
+          const int rb = min(ir0 + 4 * h * iv0, ir0 + (4 * h + 3) * iv0) - 1;  // first of the 5 T rows
+          double va[5];
 #pragma unroll
-        for (int u = 0; u < 4; ++u) {
-          // T row of cell u's p relative to rb: ir0 + u*iv0 - rb (1..4)
-          const int ka = iv0 > 0 ? u + 1 : 4 - u;
-          acc[u] = __dadd_rn(acc[u], __dadd_rn(__dmul_rn(omr, va[ka]), __dmul_rn(r, va[ka - 1])));
+          for (int k = 0; k < 5; ++k) va[k] = __dmul_rn(static_cast<double>(scv[bf][rb + k][jl]), corr);
+#pragma unroll
+          for (int u = 0; u < 4; ++u) {
+            // T row of cell 4h+u's p relative to rb (1..4)
+            const int ka = iv0 > 0 ? u + 1 : 4 - u;
+            acc[4 * h + u] = __dadd_rn(acc[4 * h + u], __dadd_rn(__dmul_rn(omr, va[ka]), __dmul_rn(r, va[ka - 1])));
+          }
         }
       } else {
-        // transposed: the 4 cells are 4 consecutive columns of one row i
+        // transposed: the cells are consecutive columns of one row i
         const int ir = i0 - i_lo + 1;
 #pragma unroll
-        for (int u = 0; u < 4; ++u) {
+        for (int u = 0; u < kCPT; ++u) {
           const int jl = j0 + u * iv3 - j_lo;
           const double r = sfrac[bf][jl];
           const double omr = __dsub_rn(1.0, r);
@@ -269,7 +281,7 @@ __global__ void __launch_bounds__(256, SKS_UNSKEW_MINB) unskew_pipe_kernel(Batch
     } else {
       const int rows = c.rows;
 #pragma unroll
-      for (int u = 0; u < 4; ++u) {
+      for (int u = 0; u < kCPT; ++u) {
         const int si = sy + u;
         if (si >= dimy || sj >= dimx) continue;
         const int i = i0 + u * iv0;
@@ -304,7 +316,7 @@ __global__ void __launch_bounds__(256, SKS_UNSKEW_MINB) unskew_pipe_kernel(Batch
     }
   }
 #pragma unroll
-  for (int u = 0; u < 4; ++u) {
+  for (int u = 0; u < kCPT; ++u) {
     const int si = sy + u;
     if (si < dimy && sj < dimx) map[static_cast<long long>(si) * dimx + sj] = acc[u];
   }
@@ -348,9 +360,9 @@ int launch_unskew(const BatchDev& b, const float*, double* map, int dimy, int di
                   void* stream) {
   dim3 grid((dimx + kUT - 1) / kUT, (dimy + kUT - 1) / kUT);
   if (b.row_blocks) {
-    unskew_pipe_kernel<true><<<grid, 256, 0, static_cast<cudaStream_t>(stream)>>>(b, map, dimy, dimx);
+    unskew_pipe_kernel<true><<<grid, 32 * kNW, 0, static_cast<cudaStream_t>(stream)>>>(b, map, dimy, dimx);
   } else {
-    unskew_pipe_kernel<false><<<grid, 256, 0, static_cast<cudaStream_t>(stream)>>>(b, map, dimy, dimx);
+    unskew_pipe_kernel<false><<<grid, 32 * kNW, 0, static_cast<cudaStream_t>(stream)>>>(b, map, dimy, dimx);
   }
   return static_cast<int>(cudaGetLastError());
 }
