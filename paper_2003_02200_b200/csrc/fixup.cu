@@ -49,7 +49,18 @@ struct ExactState {
   double M;       // exact max theta when Mvalid
   bool Mvalid;
   int cv;
+#ifdef SKS_EXP_BANDHIST
+  int first_band;  // dd of the first band target (-1: none)
+  int gap;         // its distance to the last record
+  int blk_before, blk_after;
+#endif
 };
+
+#ifdef SKS_EXP_BANDHIST
+// experiment build (tools/bandhist.py): where the first band target of each
+// re-run POV falls and how the evaluated blocks split around it
+__device__ unsigned long long g_bandhist[64];
+#endif
 
 // One target, every case handled (filter + exact FP64 inside the band).
 __device__ __forceinline__ bool exact_step(ExactState& S, const float* row, int x, int sg, int dd,
@@ -60,6 +71,12 @@ __device__ __forceinline__ bool exact_step(ExactState& S, const float* row, int 
     above = true;
     S.Mvalid = false;
   } else if (t >= S.lo) {
+#ifdef SKS_EXP_BANDHIST
+    if (S.first_band < 0) {
+      S.first_band = dd;
+      S.gap = dd - S.r;
+    }
+#endif
     const double th = __ddiv_rn(__dsub_rn(static_cast<double>(e), S.h), static_cast<double>(dd));
     if (!S.Mvalid) {
       S.M = __ddiv_rn(__dsub_rn(static_cast<double>(row[x + sg * S.r]), S.h), static_cast<double>(S.r));
@@ -201,6 +218,11 @@ __device__ int exact_pov(const float* row, const float* wm, const float* ivt, in
   S.M = -INFINITY;
   S.Mvalid = true;
   S.cv = 0;
+#ifdef SKS_EXP_BANDHIST
+  S.first_band = -1;
+  S.gap = 0;
+  S.blk_before = S.blk_after = 0;
+#endif
   const bool exact_all = force_exact || static_cast<double>(S.hl) != hld || !(fabsf(S.hf) < 1e30f);
   if (exact_all) {
     double M = -INFINITY;
@@ -251,10 +273,28 @@ __device__ int exact_pov(const float* row, const float* wm, const float* ivt, in
       const int db = min(D, sg > 0 ? 16 * w + 15 - x : x - 16 * w);
       const float N = __fadd_rn(__fsub_rn(__ldg(wm + w), S.hf), -S.hl);  // L1 hit
       if (!(__fmul_rn(N, ivt[da]) < S.lo && __fmul_rn(N, ivt[db]) < S.lo)) {
+#ifdef SKS_EXP_BANDHIST
+        if (S.first_band < 0) ++S.blk_before; else ++S.blk_after;
+#endif
         eval_block(S, row, ivt, x, sg, da, db);
       }
     }
   }
+#ifdef SKS_EXP_BANDHIST
+  {
+    auto lg = [](int v) { int b = 0; while (v > 1 && b < 15) { v >>= 1; ++b; } return b; };
+    atomicAdd(&g_bandhist[44], 1ull);
+    if (S.first_band < 0) {
+      atomicAdd(&g_bandhist[45], 1ull);
+    } else {
+      atomicAdd(&g_bandhist[min(9, static_cast<int>(10.0 * S.first_band / (D + 1)))], 1ull);
+      atomicAdd(&g_bandhist[10 + lg(S.first_band)], 1ull);
+      atomicAdd(&g_bandhist[26 + lg(S.gap + 1)], 1ull);
+    }
+    atomicAdd(&g_bandhist[42], static_cast<unsigned long long>(S.blk_before));
+    atomicAdd(&g_bandhist[43], static_cast<unsigned long long>(S.blk_after));
+  }
+#endif
   return S.cv;
 }
 
@@ -743,5 +783,16 @@ int launch_ivt_table(float* ivt, int n, void* stream) {
 }
 
 int fixup_smem_table_max() { return kSmemTabMax; }
+
+#ifdef SKS_EXP_BANDHIST
+extern "C" int sks_exp_bandhist(unsigned long long* out, int reset) {
+  cudaError_t e = cudaMemcpyFromSymbol(out, g_bandhist, sizeof(g_bandhist));
+  if (reset) {
+    static const unsigned long long z[64] = {};
+    cudaMemcpyToSymbol(g_bandhist, z, sizeof(z));
+  }
+  return static_cast<int>(e);
+}
+#endif
 
 }  // namespace sks
