@@ -498,10 +498,25 @@ struct sks_context {
     launches += 3;
   }
 
+  // Host entry point: the last batch's map pass runs in row chunks and each
+  // chunk's D2H starts on copy_stream while the next chunk is computed.
+  cudaStream_t copy_stream = nullptr;
+  cudaEvent_t chunk_ev[4] = {};
+
+  void ensure_copy_stream() {
+    if (copy_stream) return;
+    cuda_check(cudaStreamCreateWithFlags(&copy_stream, cudaStreamNonBlocking), "copy stream");
+    for (cudaEvent_t& e : chunk_ev) cuda_check(cudaEventCreateWithFlags(&e, cudaEventDisableTiming), "event");
+  }
+
   ~sks_context() {
     for (cudaEvent_t& e : ev) {
       if (e) cudaEventDestroy(e);
     }
+    for (cudaEvent_t& e : chunk_ev) {
+      if (e) cudaEventDestroy(e);
+    }
+    if (copy_stream) cudaStreamDestroy(copy_stream);
     if (own_stream) cudaStreamDestroy(own_stream);
     if (h_check) cudaFreeHost(h_check);
   }
@@ -559,7 +574,7 @@ double elapsed(cudaEvent_t a, cudaEvent_t b) {
 void run_sectors(sks_context* ctx, const float* d_dem, int dimy, int dimx, double cellsize,
                  const sks_run_config* cfg, std::vector<int> sectors, double* d_map,
                  cudaStream_t st, sks_stats* stats, bool force_exact, int part = 0, int nparts = 1,
-                 const std::vector<double>& cuts = {}) {
+                 const std::vector<double>& cuts = {}, BatchDev* defer_last = nullptr) {
   std::sort(sectors.begin(), sectors.end());
   sectors.erase(std::unique(sectors.begin(), sectors.end()), sectors.end());
   for (int k : sectors) {
@@ -584,6 +599,10 @@ void run_sectors(sks_context* ctx, const float* d_dem, int dimy, int dimx, doubl
     if (stats) cuda_check(cudaEventRecord(ctx->ev[2], st), "event");
     ctx->fixup_batch(a, st);
     if (stats) cuda_check(cudaEventRecord(ctx->ev[3], st), "event");
+    if (defer_last != nullptr && !stats && &bp == &P.batches.back()) {
+      *defer_last = bd;  // the caller runs this batch's map pass (chunked)
+      continue;
+    }
     cuda_check(launch_unskew(bd, nullptr, d_map, dimy, dimx, st), "launch unskew");
     ++ctx->launches;
     if (stats) {
@@ -696,16 +715,44 @@ void total_host(sks_context* ctx, const float* dem, int dimy, int dimx, double c
   std::iota(all.begin(), all.end(), 0);
   sks_stats local{};
   local.kernel_launches += 1;  // dem_check
+  // Without stats, the last batch's unskew + scale run in row chunks and each
+  // chunk's D2H overlaps the next chunk's compute (the map rows a chunk of
+  // DEM tiles writes are final once that chunk's unskew and scale are done).
+  BatchDev last{};
+  last.n_sectors = -1;
   run_sectors(ctx, ctx->dem.as<float>(), dimy, dimx, cellsize, cfg, all, ctx->map.as<double>(), st,
-              stats ? &local : nullptr, exact);
-  if (!raw) {
-    cuda_check(launch_scale(ctx->map.as<double>(), static_cast<long long>(n),
-                            area_scale_factor(cfg->ns, cellsize, cfg->units), st),
-               "launch scale");
-    ++ctx->launches;
-    local.kernel_launches += 1;
+              stats ? &local : nullptr, exact, 0, 1, {}, stats ? nullptr : &last);
+  const double factor = area_scale_factor(cfg->ns, cellsize, cfg->units);
+  double* map = ctx->map.as<double>();
+  if (last.n_sectors >= 0) {
+    ctx->ensure_copy_stream();
+    const int tr = unskew_tile_rows();
+    const int tiles = (dimy + tr - 1) / tr;
+    const int nch = std::min(4, tiles);
+    for (int c = 0; c < nch; ++c) {
+      const int t0 = tiles * c / nch, t1 = tiles * (c + 1) / nch;
+      const int y0 = t0 * tr, y1 = std::min(dimy, t1 * tr);
+      const size_t off = static_cast<size_t>(y0) * dimx, cnt = static_cast<size_t>(y1 - y0) * dimx;
+      cuda_check(launch_unskew(last, nullptr, map, dimy, dimx, st, t0, t1 - t0), "launch unskew");
+      ++ctx->launches;
+      if (!raw) {
+        cuda_check(launch_scale(map + off, static_cast<long long>(cnt), factor, st), "launch scale");
+        ++ctx->launches;
+      }
+      cuda_check(cudaEventRecord(ctx->chunk_ev[c], st), "event");
+      cuda_check(cudaStreamWaitEvent(ctx->copy_stream, ctx->chunk_ev[c], 0), "wait");
+      cuda_check(cudaMemcpyAsync(out + off, map + off, cnt * sizeof(double), cudaMemcpyDeviceToHost, ctx->copy_stream),
+                 "D2H map");
+    }
+    cuda_check(cudaStreamSynchronize(ctx->copy_stream), "sync");
+  } else {
+    if (!raw) {
+      cuda_check(launch_scale(map, static_cast<long long>(n), factor, st), "launch scale");
+      ++ctx->launches;
+      local.kernel_launches += 1;
+    }
+    cuda_check(cudaMemcpyAsync(out, ctx->map.p, n * sizeof(double), cudaMemcpyDeviceToHost, st), "D2H map");
   }
-  cuda_check(cudaMemcpyAsync(out, ctx->map.p, n * sizeof(double), cudaMemcpyDeviceToHost, st), "D2H map");
   cuda_check(cudaStreamSynchronize(st), "sync");
   if (stats) {
     local.h2d_bytes = static_cast<long long>(n * sizeof(float));

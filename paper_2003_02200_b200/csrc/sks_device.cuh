@@ -118,8 +118,11 @@ int scan2_slots(int lmax);  // 0: rows too long for the target-lockstep kernel
 int scan2_max_row();        // longest row scan2 can hold (>= 1 slot)
 size_t scan2_smem_bytes(int lmax, int nslots);
 int launch_scan2(const ScanArgs& a, int nslots, void* stream);
+// tile rows [tile_row0, tile_row0 + tile_rows) of the map (32 DEM rows each;
+// tile_rows < 0: to the end)
 int launch_unskew(const BatchDev& b, const float* unused, double* map,
-                  int dimy, int dimx, void* stream);
+                  int dimy, int dimx, void* stream, int tile_row0 = 0, int tile_rows = -1);
+int unskew_tile_rows();
 int launch_unskew_from_vs(const BatchDev& b, const double* skw_vs,
                           double* map, int dimy, int dimx, void* stream);
 int launch_scale(double* map, long long n, double factor, void* stream);

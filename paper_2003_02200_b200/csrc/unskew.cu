@@ -107,7 +107,7 @@ struct USect {
 
 template <bool kBlocks>  // row-block sharding: some tiles own no row of a sector
 __global__ void __launch_bounds__(32 * kNW, SKS_UNSKEW_MINB) unskew_pipe_kernel(BatchDev b, double* __restrict__ map, int dimy,
-                                                              int dimx) {
+                                                              int dimx, int tile_row0) {
   __shared__ int scv[2][kTR][kUT + 1];
   __shared__ int sown[2];  // sector staged in the buffer has owned rows in the tile
   __shared__ int sdest[2][kUT];
@@ -126,7 +126,7 @@ __global__ void __launch_bounds__(32 * kNW, SKS_UNSKEW_MINB) unskew_pipe_kernel(
   };
   const int tx = threadIdx.x & 31;
   const int ty = threadIdx.x >> 5;  // 0 .. kNW-1
-  const int y0 = blockIdx.y * kUT, x0 = blockIdx.x * kUT;
+  const int y0 = (tile_row0 + blockIdx.y) * kUT, x0 = blockIdx.x * kUT;
   const int ye = min(dimy, y0 + kUT) - 1, xe = min(dimx, x0 + kUT) - 1;
   const bool full_tile = ye == y0 + kUT - 1 && xe == x0 + kUT - 1;
   const int sj = x0 + tx;
@@ -357,15 +357,20 @@ __global__ void cv_to_vs_kernel(const int* cvf, const int* cvb, double* out, lon
 }  // namespace
 
 int launch_unskew(const BatchDev& b, const float*, double* map, int dimy, int dimx,
-                  void* stream) {
-  dim3 grid((dimx + kUT - 1) / kUT, (dimy + kUT - 1) / kUT);
+                  void* stream, int tile_row0, int tile_rows) {
+  const int all_rows = (dimy + kUT - 1) / kUT;
+  if (tile_rows < 0) tile_rows = all_rows - tile_row0;
+  if (tile_rows <= 0) return 0;
+  dim3 grid((dimx + kUT - 1) / kUT, tile_rows);
   if (b.row_blocks) {
-    unskew_pipe_kernel<true><<<grid, 32 * kNW, 0, static_cast<cudaStream_t>(stream)>>>(b, map, dimy, dimx);
+    unskew_pipe_kernel<true><<<grid, 32 * kNW, 0, static_cast<cudaStream_t>(stream)>>>(b, map, dimy, dimx, tile_row0);
   } else {
-    unskew_pipe_kernel<false><<<grid, 32 * kNW, 0, static_cast<cudaStream_t>(stream)>>>(b, map, dimy, dimx);
+    unskew_pipe_kernel<false><<<grid, 32 * kNW, 0, static_cast<cudaStream_t>(stream)>>>(b, map, dimy, dimx, tile_row0);
   }
   return static_cast<int>(cudaGetLastError());
 }
+
+int unskew_tile_rows() { return kUT; }
 
 int launch_unskew_from_vs(const BatchDev& b, const double* skw_vs, double* map, int dimy,
                           int dimx, void* stream) {
