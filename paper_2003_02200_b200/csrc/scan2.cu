@@ -153,12 +153,7 @@ __device__ void load_slot(const ScanArgs& a, int* ctl, float* base, const Layout
 }
 __device__ void load_slot_(const ScanArgs& a, int* ctl, float* base, const Layout2& lay, int lane) {
 #else
-#ifdef SKS_LOADER_NOINLINE
-__device__ __noinline__
-#else
-__device__
-#endif
-void load_slot(const ScanArgs& a, int* ctl, float* base, const Layout2& lay, int lane) {
+__device__ void load_slot(const ScanArgs& a, int* ctl, float* base, const Layout2& lay, int lane) {
 #endif
   int it = 0;
   if (lane == 0) it = static_cast<int>(atomicAdd(a.item_counter, 1u));
@@ -262,41 +257,12 @@ void load_slot(const ScanArgs& a, int* ctl, float* base, const Layout2& lay, int
     if (lane == 0) {
       vl[kLoads] = vl[kLoads] + 1;
       // R was last read through the generic proxy (the previous row's tasks)
-#ifndef SKS_EXP_NOFENCE
       fence_proxy_async();
-#endif
       mbar_expect_tx(bar, bytes);
       tma_bulk_g2s(R, a.b.sdem + (row0 - sh), bytes, bar);
     }
     mbar_wait(bar, parity);
-#ifdef SKS_VEC_SHIFT
-    {
-      const unsigned ra = smem_u32(R), sa = smem_u32(S);
-      for (int qi = lane; qi < lay.lb / 4; qi += 32) {
-        const int x = 4 * qi;
-        const float4 u = lds128(ra + 16u * qi);
-        const float4 w = lds128(ra + 16u * qi + 16u);
-        float4 v;
-        switch (sh) {
-          case 0: v = u; break;
-          case 1: v = make_float4(u.y, u.z, u.w, w.x); break;
-          case 2: v = make_float4(u.z, u.w, w.x, w.y); break;
-          default: v = make_float4(u.w, w.x, w.y, w.z); break;
-        }
-        if (x + 3 >= L) {
-          if (x >= L) v.x = ninf;
-          if (x + 1 >= L) v.y = ninf;
-          if (x + 2 >= L) v.z = ninf;
-          v.w = ninf;
-        }
-        asm volatile("st.shared.v4.f32 [%0], {%1, %2, %3, %4};" ::"r"(sa + 16u * qi), "f"(v.x), "f"(v.y), "f"(v.z),
-                     "f"(v.w)
-                     : "memory");
-      }
-    }
-#else
     for (int x = lane; x < lay.lb; x += 32) S[x] = x < L ? R[x + sh] : ninf;
-#endif
 #endif
   }
   __syncwarp();
@@ -350,12 +316,6 @@ void load_slot(const ScanArgs& a, int* ctl, float* base, const Layout2& lay, int
   }
   __syncwarp();
 }
-
-#ifdef SKS_LOADER_NOINLINE2
-__device__ __noinline__ void load_slot_ni(const ScanArgs& a, int* ctl, float* base, const Layout2& lay, int lane) {
-  load_slot(a, ctl, base, lay, lane);
-}
-#endif
 
 // Per-lane state of one task (two POVs).
 struct Pov2 {
@@ -862,11 +822,7 @@ __global__ void __launch_bounds__(kThr, 1) scan2_kernel(const __grid_constant__ 
     __syncwarp();
     int last = 0;
     if (lane == 0) last = atomicSub(ctl + kRemaining, 1) == 1;
-#ifdef SKS_LOADER_NOINLINE2
-    if (__shfl_sync(0xffffffffu, last, 0)) load_slot_ni(a, ctl, slots + sl * lay.slot, lay, lane);
-#else
     if (__shfl_sync(0xffffffffu, last, 0)) load_slot(a, ctl, slots + sl * lay.slot, lay, lane);
-#endif
   }
   if (a.skipped != nullptr && lane == 0 && skipped != 0) {
     atomicAdd(a.skipped, 64ull * skipped);
