@@ -125,7 +125,10 @@ struct Batch {
   int tiles_x = 0, tiles_total = 0;
   long long target_evals = 0;
   // device copies
-  DevBuf d_sectors, d_dest, d_fracf, d_fracd, d_ranges, d_items, d_fix_off;
+  // scan3 row pairs over the scanned items [n_long, n_items) (indices relative
+  // to n_long): (sector slot, item of row 2m, item of row 2m+1 or -1, 0)
+  std::vector<int4> pairs;
+  DevBuf d_sectors, d_dest, d_fracf, d_fracd, d_ranges, d_items, d_fix_off, d_pairs;
 };
 
 struct Plans {
@@ -256,6 +259,34 @@ std::unique_ptr<Batch> make_batch(const std::vector<SectorPlanH>& plans,
     const int L = item_len(it);
     if (L > limit) ++b->n_long; else if (L >= 2 && b->sdev[it.s].max_dd > 0) b->lmax = std::max(b->lmax, L);
   }
+  // scan3 pairs: rows 2m and 2m+1 of a sector (whichever are scanned items),
+  // longest pair first
+  {
+    std::map<std::pair<int, int>, int> pos;  // (sector slot, row) -> relative item
+    for (size_t i = b->n_long; i < b->items.size(); ++i) {
+      pos[{b->items[i].s, b->items[i].q}] = static_cast<int>(i) - b->n_long;
+    }
+    std::vector<char> done(b->items.size() - b->n_long, 0);
+    std::vector<std::pair<int, int4>> pl;  // (max L, pair)
+    for (size_t i = b->n_long; i < b->items.size(); ++i) {
+      const int rel = static_cast<int>(i) - b->n_long;
+      if (done[rel]) continue;
+      const ScanItem& it = b->items[i];
+      const int q0 = it.q & ~1;
+      auto a_it = pos.find({it.s, q0});
+      auto b_it = pos.find({it.s, q0 + 1});
+      int ia = a_it != pos.end() ? a_it->second : -1;
+      int ib = b_it != pos.end() ? b_it->second : -1;
+      if (ia < 0) std::swap(ia, ib);  // a single odd row goes in slot a
+      done[ia] = 1;
+      if (ib >= 0) done[ib] = 1;
+      const int la = item_len(b->items[b->n_long + ia]);
+      const int lb = ib >= 0 ? item_len(b->items[b->n_long + ib]) : 0;
+      pl.push_back({std::max(la, lb), make_int4(it.s, ia, ib, 0)});
+    }
+    std::stable_sort(pl.begin(), pl.end(), [](const auto& x, const auto& y) { return x.first > y.first; });
+    for (const auto& p : pl) b->pairs.push_back(p.second);
+  }
   // fixup queue segments, in item order: one entry per POV and direction,
   // the exact bound
   b->fix_off.resize(b->items.size());
@@ -290,6 +321,7 @@ std::unique_ptr<Batch> make_batch(const std::vector<SectorPlanH>& plans,
   up(b->d_ranges, b->ranges.data(), b->ranges.size() * sizeof(int2));
   up(b->d_items, b->items.data(), b->items.size() * sizeof(ScanItem));
   up(b->d_fix_off, b->fix_off.data(), b->fix_off.size() * sizeof(unsigned));
+  up(b->d_pairs, b->pairs.data(), b->pairs.size() * sizeof(int4));
   return b;
 }
 
@@ -463,7 +495,20 @@ struct sks_context {
   // zero_cv: the cv pool must be cleared here (debug paths that upload an
   // sDEM directly); after relocate_kernel it already is (the kernel zeroes
   // the cv cells of every tile it writes).
-  void scan_batch(const Batch& b, const ScanArgs& a, cudaStream_t st, bool split_bwd, bool zero_cv) {
+  // Scan kernel choice per workload shape (dims, ns, max_distance, row
+  // block): scan3 (row pairs) evaluates fewer windows on rough terrain and
+  // more on near-flat terrain (fractal 2000^2: scan 58.9 -> 53.0 ms;
+  // SmoothedNoise: 123.2 -> 135.2 ms), so the first call of a shape runs
+  // scan3 and the second scan2, each timed on the device, and the faster
+  // one is kept. Both give identical results. SKS_SCAN3=0/1 forces a kernel.
+  struct ScanTune {
+    float t3 = -1.f, t2 = -1.f;
+    int choice = 0;  // 0: undecided, 2 or 3
+  };
+  std::map<std::tuple<int, int, int, double, int, int>, ScanTune> tune;
+
+  void scan_batch(const Batch& b, const ScanArgs& a, cudaStream_t st, bool split_bwd, bool zero_cv,
+                  int mode = 0) {
     if (zero_cv) {
       cuda_check(cudaMemsetAsync(cv.p, 0, static_cast<size_t>(b.pool_elems) * sizeof(int), st),
                  "memset cv");
@@ -487,9 +532,32 @@ struct sks_context {
       s2.n_items -= b.n_long;
       s2.fix_off += b.n_long;
       s2.fix_cnt += b.n_long;
-      cuda_check(launch_scan2(s2, scan2_slots(s2.lmax), st), "launch scan2");
+      s2.pairs = b.d_pairs.as<int4>();
+      s2.n_pairs = static_cast<int>(b.pairs.size());
+      if (use_scan3(b, s2.lmax, mode)) {
+        cuda_check(launch_scan3(s2, scan3_slots(s2.lmax), st), "launch scan3");
+      } else {
+        cuda_check(launch_scan2(s2, scan2_slots(s2.lmax), st), "launch scan2");
+      }
       ++launches;
     }
+  }
+
+  // scan3 (row pairs) where at least 2 pair slots fit and the
+  // relocation is not fused into the loader; SKS_SCAN3=0 keeps scan2 (read
+  // per launch)
+  static bool scan3_fits(const Batch& b, int lmax) { return !b.fused && scan3_slots(lmax) >= 2; }
+  static int forced_scan() {
+    const char* v = std::getenv("SKS_SCAN3");
+    if (v == nullptr) return 0;
+    return std::string(v) == "0" ? 2 : 3;
+  }
+  // mode: 2 or 3 (the tuned or forced choice), 0: scan3 where it fits
+  static bool use_scan3(const Batch& b, int lmax, int mode) {
+    if (!scan3_fits(b, lmax)) return false;
+    const int f = forced_scan();
+    if (f != 0) return f == 3;
+    return mode != 2;
   }
 
   void fixup_batch(const ScanArgs& a, cudaStream_t st) {
@@ -583,6 +651,22 @@ void run_sectors(sks_context* ctx, const float* d_dem, int dimy, int dimx, doubl
   Plans& P = ctx->plans_for(dimy, dimx, cfg->ns, cellsize, cfg->max_distance, sectors, part, nparts, cuts);
   const long long launches0 = ctx->launches;
   double t_skew = 0, t_scan = 0, t_fix = 0, t_unskew = 0;
+  // scan kernel choice (sks_context::ScanTune): time one call of each where
+  // scan3 fits, then keep the faster
+  auto& tn = ctx->tune[std::make_tuple(dimy, dimx, cfg->ns, cfg->max_distance, part, nparts)];
+  int mode = tn.choice;
+  bool timing = false;
+  if (mode == 0 && sks_context::forced_scan() == 0) {
+    bool fits = false;
+    for (auto& bp : P.batches) fits |= sks_context::scan3_fits(*bp, std::max(bp->lmax, 4));
+    if (fits) {
+      mode = tn.t3 < 0.f ? 3 : 2;
+      timing = true;
+    } else {
+      tn.choice = mode = 2;
+    }
+  }
+  float t_tune = 0.f;
   long long flagged = 0, evals = 0, skipped = 0;
   for (auto& bp : P.batches) {
     Batch& b = *bp;
@@ -595,7 +679,15 @@ void run_sectors(sks_context* ctx, const float* d_dem, int dimy, int dimx, doubl
     if (stats) cuda_check(cudaEventRecord(ctx->ev[0], st), "event");
     if (!fused) ctx->relocate(d_dem, dimy, dimx, bd, b, st);
     if (stats) cuda_check(cudaEventRecord(ctx->ev[1], st), "event");
-    ctx->scan_batch(b, a, st, false, false);
+    if (timing) cuda_check(cudaEventRecord(ctx->ev[5], st), "event");
+    ctx->scan_batch(b, a, st, false, false, mode);
+    if (timing) {
+      cuda_check(cudaEventRecord(ctx->ev[6], st), "event");
+      cuda_check(cudaEventSynchronize(ctx->ev[6]), "sync");
+      float ms = 0.f;
+      cuda_check(cudaEventElapsedTime(&ms, ctx->ev[5], ctx->ev[6]), "elapsed");
+      t_tune += ms;
+    }
     if (stats) cuda_check(cudaEventRecord(ctx->ev[2], st), "event");
     ctx->fixup_batch(a, st);
     if (stats) cuda_check(cudaEventRecord(ctx->ev[3], st), "event");
@@ -644,6 +736,10 @@ void run_sectors(sks_context* ctx, const float* d_dem, int dimy, int dimx, doubl
       skipped += static_cast<long long>(sk);
     }
     evals += b.target_evals;
+  }
+  if (timing) {
+    (mode == 3 ? tn.t3 : tn.t2) = t_tune;
+    if (tn.t3 >= 0.f && tn.t2 >= 0.f) tn.choice = tn.t3 <= tn.t2 ? 3 : 2;
   }
   if (stats) {
     stats->skew_seconds += t_skew;
