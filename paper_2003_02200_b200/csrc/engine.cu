@@ -125,10 +125,10 @@ struct Batch {
   int tiles_x = 0, tiles_total = 0;
   long long target_evals = 0;
   // device copies
-  // scan3 row pairs over the scanned items [n_long, n_items) (indices relative
-  // to n_long): (sector slot, item of row 2m, item of row 2m+1 or -1, 0)
-  std::vector<int4> pairs;
-  DevBuf d_sectors, d_dest, d_fracf, d_fracd, d_ranges, d_items, d_fix_off, d_pairs;
+  // scan3 row groups (pairs, quads) over the scanned items [n_long, n_items)
+  // (indices relative to n_long)
+  std::vector<int4> pairs, quads;
+  DevBuf d_sectors, d_dest, d_fracf, d_fracd, d_ranges, d_items, d_fix_off, d_pairs, d_quads;
 };
 
 struct Plans {
@@ -259,33 +259,25 @@ std::unique_ptr<Batch> make_batch(const std::vector<SectorPlanH>& plans,
     const int L = item_len(it);
     if (L > limit) ++b->n_long; else if (L >= 2 && b->sdev[it.s].max_dd > 0) b->lmax = std::max(b->lmax, L);
   }
-  // scan3 pairs: rows 2m and 2m+1 of a sector (whichever are scanned items),
-  // longest pair first
-  {
-    std::map<std::pair<int, int>, int> pos;  // (sector slot, row) -> relative item
+  // scan3 row groups of kR = 2 and 4: rows q0 .. q0+kR-1 (q0 = q & ~(kR-1))
+  // of a sector, each a scanned item or -1, longest group first
+  for (int kR : {2, 4}) {
+    std::map<std::pair<int, int>, int4> groups;  // (sector slot, q0) -> items
+    std::map<std::pair<int, int>, int> glen;
     for (size_t i = b->n_long; i < b->items.size(); ++i) {
-      pos[{b->items[i].s, b->items[i].q}] = static_cast<int>(i) - b->n_long;
-    }
-    std::vector<char> done(b->items.size() - b->n_long, 0);
-    std::vector<std::pair<int, int4>> pl;  // (max L, pair)
-    for (size_t i = b->n_long; i < b->items.size(); ++i) {
-      const int rel = static_cast<int>(i) - b->n_long;
-      if (done[rel]) continue;
       const ScanItem& it = b->items[i];
-      const int q0 = it.q & ~1;
-      auto a_it = pos.find({it.s, q0});
-      auto b_it = pos.find({it.s, q0 + 1});
-      int ia = a_it != pos.end() ? a_it->second : -1;
-      int ib = b_it != pos.end() ? b_it->second : -1;
-      if (ia < 0) std::swap(ia, ib);  // a single odd row goes in slot a
-      done[ia] = 1;
-      if (ib >= 0) done[ib] = 1;
-      const int la = item_len(b->items[b->n_long + ia]);
-      const int lb = ib >= 0 ? item_len(b->items[b->n_long + ib]) : 0;
-      pl.push_back({std::max(la, lb), make_int4(it.s, ia, ib, 0)});
+      const int q0 = it.q & ~(kR - 1);
+      auto key = std::make_pair(it.s, q0);
+      auto [g, fresh] = groups.try_emplace(key, make_int4(-1, -1, -1, -1));
+      int* slot = &g->second.x;
+      slot[it.q - q0] = static_cast<int>(i) - b->n_long;
+      glen[key] = std::max(glen[key], item_len(it));
     }
+    std::vector<std::pair<int, int4>> pl;
+    for (const auto& [key, g] : groups) pl.push_back({glen[key], g});
     std::stable_sort(pl.begin(), pl.end(), [](const auto& x, const auto& y) { return x.first > y.first; });
-    for (const auto& p : pl) b->pairs.push_back(p.second);
+    auto& out = kR == 2 ? b->pairs : b->quads;
+    for (const auto& pg : pl) out.push_back(pg.second);
   }
   // fixup queue segments, in item order: one entry per POV and direction,
   // the exact bound
@@ -322,6 +314,7 @@ std::unique_ptr<Batch> make_batch(const std::vector<SectorPlanH>& plans,
   up(b->d_items, b->items.data(), b->items.size() * sizeof(ScanItem));
   up(b->d_fix_off, b->fix_off.data(), b->fix_off.size() * sizeof(unsigned));
   up(b->d_pairs, b->pairs.data(), b->pairs.size() * sizeof(int4));
+  up(b->d_quads, b->quads.data(), b->quads.size() * sizeof(int4));
   return b;
 }
 
@@ -496,14 +489,15 @@ struct sks_context {
   // sDEM directly); after relocate_kernel it already is (the kernel zeroes
   // the cv cells of every tile it writes).
   // Scan kernel choice per workload shape (dims, ns, max_distance, row
-  // block): scan3 (row pairs) evaluates fewer windows on rough terrain and
-  // more on near-flat terrain (fractal 2000^2: scan 58.9 -> 53.0 ms;
-  // SmoothedNoise: 123.2 -> 135.2 ms), so the first call of a shape runs
-  // scan3 and the second scan2, each timed on the device, and the faster
-  // one is kept. Both give identical results. SKS_SCAN3=0/1 forces a kernel.
+  // block): scan3 over groups of adjacent rows evaluates fewer windows on
+  // rough terrain and more on near-flat terrain (config 2 scan: fractal
+  // 58.9 ms scan2, 52.9 pairs, 50.2 quads; SmoothedNoise 123.1, 135.6,
+  // 155.4), so the first calls of a shape try quads, pairs and scan2 (each
+  // timed on the device) and the fastest is kept. All give identical
+  // results. SKS_SCAN3 = 0 / 1 / 4 forces scan2 / pairs / quads.
   struct ScanTune {
-    float t3 = -1.f, t2 = -1.f;
-    int choice = 0;  // 0: undecided, 2 or 3
+    float t[5] = {-1.f, -1.f, -1.f, -1.f, -1.f};  // device time per mode (2, 3, 4)
+    int choice = 0;  // 0: undecided, else the mode
   };
   std::map<std::tuple<int, int, int, double, int, int>, ScanTune> tune;
 
@@ -532,10 +526,11 @@ struct sks_context {
       s2.n_items -= b.n_long;
       s2.fix_off += b.n_long;
       s2.fix_cnt += b.n_long;
-      s2.pairs = b.d_pairs.as<int4>();
-      s2.n_pairs = static_cast<int>(b.pairs.size());
-      if (use_scan3(b, s2.lmax, mode)) {
-        cuda_check(launch_scan3(s2, scan3_slots(s2.lmax), st), "launch scan3");
+      const int rows = scan3_rows(b, s2.lmax, mode);
+      if (rows > 0) {
+        s2.pairs = rows == 4 ? b.d_quads.as<int4>() : b.d_pairs.as<int4>();
+        s2.n_pairs = static_cast<int>(rows == 4 ? b.quads.size() : b.pairs.size());
+        cuda_check(launch_scan3(s2, scan3_slots(s2.lmax, rows), rows, st), "launch scan3");
       } else {
         cuda_check(launch_scan2(s2, scan2_slots(s2.lmax), st), "launch scan2");
       }
@@ -546,18 +541,28 @@ struct sks_context {
   // scan3 (row pairs) where at least 2 pair slots fit and the
   // relocation is not fused into the loader; SKS_SCAN3=0 keeps scan2 (read
   // per launch)
-  static bool scan3_fits(const Batch& b, int lmax) { return !b.fused && scan3_slots(lmax) >= 2; }
-  static int forced_scan() {
-    const char* v = std::getenv("SKS_SCAN3");
-    if (v == nullptr) return 0;
-    return std::string(v) == "0" ? 2 : 3;
+  // kernel modes: 2 = scan2 (64 positions of one row per task), 3 = scan3
+  // over row pairs, 4 = scan3 over row quads; a group mode
+  // needs >= 2 slots of its size
+  static bool mode_fits(const Batch& b, int lmax, int mode) {
+    if (mode == 2) return true;
+    return !b.fused && scan3_slots(lmax, mode == 4 ? 4 : 2) >= 2;
   }
-  // mode: 2 or 3 (the tuned or forced choice), 0: scan3 where it fits
-  static bool use_scan3(const Batch& b, int lmax, int mode) {
-    if (!scan3_fits(b, lmax)) return false;
+  static int forced_scan() {
+    const char* v = std::getenv("SKS_SCAN3");  // 0: scan2, 1 / 2: pairs, 4: quads
+    if (v == nullptr) return 0;
+    const std::string m(v);
+    return m == "0" ? 2 : m == "4" ? 4 : 3;
+  }
+  // rows per group of the scan3 launch for `mode` (0: scan2)
+  static int scan3_rows(const Batch& b, int lmax, int mode) {
     const int f = forced_scan();
-    if (f != 0) return f == 3;
-    return mode != 2;
+    if (f != 0) mode = f;
+    if (mode == 0) mode = 3;
+    if (mode == 2 || !mode_fits(b, lmax, mode)) {
+      return mode == 4 && mode_fits(b, lmax, 3) ? 2 : 0;
+    }
+    return mode == 4 ? 4 : 2;
   }
 
   void fixup_batch(const ScanArgs& a, cudaStream_t st) {
@@ -657,13 +662,22 @@ void run_sectors(sks_context* ctx, const float* d_dem, int dimy, int dimx, doubl
   int mode = tn.choice;
   bool timing = false;
   if (mode == 0 && sks_context::forced_scan() == 0) {
-    bool fits = false;
-    for (auto& bp : P.batches) fits |= sks_context::scan3_fits(*bp, std::max(bp->lmax, 4));
-    if (fits) {
-      mode = tn.t3 < 0.f ? 3 : 2;
-      timing = true;
-    } else {
+    // candidate modes in trial order: quads, pairs, scan2 (those that fit)
+    auto fits = [&](int m) {
+      bool ok = false;
+      for (auto& bp : P.batches) ok |= sks_context::mode_fits(*bp, std::max(bp->lmax, 4), m);
+      return ok;
+    };
+    for (int m : {4, 3, 2}) {
+      if (tn.t[m] < 0.f && fits(m)) {
+        mode = m;
+        break;
+      }
+    }
+    if (mode == 0 || !fits(3)) {
       tn.choice = mode = 2;
+    } else {
+      timing = true;
     }
   }
   float t_tune = 0.f;
@@ -738,8 +752,17 @@ void run_sectors(sks_context* ctx, const float* d_dem, int dimy, int dimx, doubl
     evals += b.target_evals;
   }
   if (timing) {
-    (mode == 3 ? tn.t3 : tn.t2) = t_tune;
-    if (tn.t3 >= 0.f && tn.t2 >= 0.f) tn.choice = tn.t3 <= tn.t2 ? 3 : 2;
+    tn.t[mode] = t_tune;
+    bool done = true;
+    int best = 0;
+    for (int m : {4, 3, 2}) {
+      bool ok = false;
+      for (auto& bp : P.batches) ok |= sks_context::mode_fits(*bp, std::max(bp->lmax, 4), m);
+      if (!ok) continue;
+      if (tn.t[m] < 0.f) done = false;
+      else if (best == 0 || tn.t[m] < tn.t[best]) best = m;
+    }
+    if (done) tn.choice = best;
   }
   if (stats) {
     stats->skew_seconds += t_skew;

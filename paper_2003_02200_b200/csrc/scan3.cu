@@ -37,26 +37,33 @@ namespace sks {
 
 namespace {
 
-constexpr int kTaskPos = 32;  // POV positions per task (x 2 rows)
 constexpr int kW = 16;        // fine window (targets)
 constexpr int kH = 64;        // coarse window (targets)
-#ifndef SKS3_NEAR_NOTEST
-#define SKS3_NEAR_NOTEST 48
-#endif
 constexpr int kOff = 128;  // table index offset (dd >= -kOff + 1 addressable)
 constexpr int kThreads = 768;
 constexpr int kMaxSlots = 8;
-constexpr int kCtlInts = 16;
+constexpr int kCtlInts = 32;
 constexpr float kBand = 5.9604644775390625e-07f;  // 10 * 2^-24
 constexpr int kSumShift = 22;
 constexpr int kSumMask = (1 << kSumShift) - 1;
 constexpr int kCopy1Shift = 18;  // copy 1's bank offset (floats) against copy 0
 
+// kR rows per task group (2: row pairs, 4: row quads); a task covers
+// kP = 64 / kR consecutive positions of every row of its group. Lane l owns
+// position y = kP c + (l mod kP) of rows 2 ph and 2 ph + 1, ph = l / kP.
+template <int kR>
+struct Geo {
+  static constexpr int kP = 64 / kR;
+  static constexpr int kNear = kP + 16;  // no skip tests in a task's first kNear targets
+};
+
+template <int kR>
 struct Layout3 {
   int lb;      // row buffer (floats) per row and direction
   int nw16, nw64;
   int T;       // table length per copy (floats, a multiple of 32)
-  int slot;    // floats per slot (a pair of rows)
+  int wpair;   // floats of window maxima per row pair
+  int slot;    // floats per slot (kR rows)
   int tables;  // offset of table copy 0
   int slots;   // offset of slot 0
   __host__ __device__ explicit Layout3(int lmax) {
@@ -64,7 +71,8 @@ struct Layout3 {
     nw16 = lb / kW;
     nw64 = lb / kH;
     T = ((kOff + lb + 16 + 31) / 32) * 32;
-    slot = 4 * lb + 4 * nw16 + 4 * nw64;
+    wpair = 4 * nw16 + 4 * nw64;
+    slot = 2 * kR * lb + (kR / 2) * wpair;
     tables = kMaxSlots * kCtlInts;
     slots = tables + 2 * T + kCopy1Shift + 14;  // 14: keeps the slots 16-byte aligned
   }
@@ -72,32 +80,39 @@ struct Layout3 {
   __host__ __device__ int total(int nslots) const { return slots + nslots * slot; }
 };
 
-// control block of one slot (ints)
-enum : int { kWord = 0, kRemaining, kDead, kS, kLA, kLB, kFirstA, kFirstB, kQA, kItA, kItB, kCap };
+// control block of one slot (ints): per row r < kR: L, first, item
+enum : int { kWord = 0, kRemaining, kDead, kS, kQ0, kCap, kRowL = 8, kRowFirst = 12, kRowItem = 16 };
 
+template <int kR>
 struct Slot3 {
-  float* S[2];  // forward copies of rows a, b
-  float* R[2];  // reversed copies
-  float2* W16S; float2* W16R;  // (m_b, m_a) per 16-target window
-  float2* W64S; float2* W64R;
+  float* S[kR];  // forward copies
+  float* R[kR];  // reversed copies
+  float2* W16S[kR / 2]; float2* W16R[kR / 2];  // per row pair: (m(row 2ph+1), m(row 2ph)) per window
+  float2* W64S[kR / 2]; float2* W64R[kR / 2];
 };
 
-__device__ __forceinline__ Slot3 slot_ptrs(float* base, const Layout3& lay) {
-  Slot3 s;
-  s.S[0] = base;
-  s.S[1] = base + lay.lb;
-  s.R[0] = base + 2 * lay.lb;
-  s.R[1] = base + 3 * lay.lb;
-  float2* w = reinterpret_cast<float2*>(base + 4 * lay.lb);
-  s.W16S = w;
-  s.W16R = w + lay.nw16;
-  s.W64S = w + 2 * lay.nw16;
-  s.W64R = w + 2 * lay.nw16 + lay.nw64;
+template <int kR>
+__device__ __forceinline__ Slot3<kR> slot_ptrs(float* base, const Layout3<kR>& lay) {
+  Slot3<kR> s;
+#pragma unroll
+  for (int r = 0; r < kR; ++r) {
+    s.S[r] = base + r * lay.lb;
+    s.R[r] = base + (kR + r) * lay.lb;
+  }
+#pragma unroll
+  for (int ph = 0; ph < kR / 2; ++ph) {
+    float2* w = reinterpret_cast<float2*>(base + 2 * kR * lay.lb + ph * lay.wpair);
+    s.W16S[ph] = w;
+    s.W16R[ph] = w + lay.nw16;
+    s.W64S[ph] = w + 2 * lay.nw16;
+    s.W64R[ph] = w + 2 * lay.nw16 + lay.nw64;
+  }
   return s;
 }
 
-// Loads the next row pair (longest first) into slot `base`; one warp.
-__device__ void load_pair(const ScanArgs& a, int* ctl, float* base, const Layout3& lay, int lane) {
+// Loads the next row group (longest first) into slot `base`; one warp.
+template <int kR>
+__device__ void load_group(const ScanArgs& a, int* ctl, float* base, const Layout3<kR>& lay, int lane) {
   int it = 0;
   if (lane == 0) it = static_cast<int>(atomicAdd(a.item_counter, 1u));
   it = __shfl_sync(0xffffffffu, it, 0);
@@ -105,82 +120,100 @@ __device__ void load_pair(const ScanArgs& a, int* ctl, float* base, const Layout
     if (lane == 0) atomicExch(ctl + kDead, 1);
     return;
   }
-  const int4 pr = a.pairs[it];  // (sector slot, item a, item b or -1, -)
-  const SectorDev& sd = a.b.sectors[pr.x];
-  const Slot3 sp = slot_ptrs(base, lay);
-  const float ninf = -INFINITY;
-  int Ls[2] = {0, 0}, firsts[2] = {0, 0}, qs[2] = {0, 0};
+  const int4 gi = a.pairs[it];  // items of rows q0 .. q0 + kR - 1 (-1: not scanned)
+  const int its[4] = {gi.x, gi.y, gi.z, gi.w};
+  int s = 0, q0 = 0;
 #pragma unroll
-  for (int r = 0; r < 2; ++r) {
-    const int itr = r ? pr.z : pr.y;
+  for (int r = kR - 1; r >= 0; --r) {
+    if (its[r] >= 0) {
+      const ScanItem item = a.items[its[r]];
+      s = item.s;
+      q0 = item.q - r;
+    }
+  }
+  const SectorDev& sd = a.b.sectors[s];
+  const Slot3<kR> sp = slot_ptrs<kR>(base, lay);
+  const float ninf = -INFINITY;
+  int Ls[kR], firsts[kR];
+#pragma unroll
+  for (int r = 0; r < kR; ++r) {
     float* S = sp.S[r];
     float* R = sp.R[r];
-    if (itr < 0) {
+    Ls[r] = 0;
+    firsts[r] = 0;
+    if (its[r] < 0) {
       for (int x = lane; x < lay.lb; x += 32) S[x] = R[x] = ninf;
       continue;
     }
-    const ScanItem item = a.items[itr];
-    const int2 rg = a.b.ranges[sd.row_off + item.q];
+    const int2 rg = a.b.ranges[sd.row_off + q0 + r];
     const int L = rg.y - rg.x;
     Ls[r] = L;
     firsts[r] = rg.x;
-    qs[r] = item.q;
-    const float* src = a.b.sdem + sd.sdem_off + static_cast<long long>(item.q) * sd.pitch + rg.x;
+    const float* src = a.b.sdem + sd.sdem_off + static_cast<long long>(q0 + r) * sd.pitch + rg.x;
 #pragma unroll 4
     for (int x = lane; x < lay.lb; x += 32) S[x] = x < L ? __ldg(src + x) : ninf;
     __syncwarp();
     for (int x = lane; x < lay.lb; x += 32) R[x] = x < L ? S[L - 1 - x] : ninf;
   }
   __syncwarp();
-  // window maxima, interleaved (row b, row a); the 16-cell forward maxima of
-  // each row also go to wm16 for the fixup's per-POV skip
-  const unsigned sa0 = smem_u32(sp.S[0]), sa1 = smem_u32(sp.S[1]);
-  const unsigned ra0 = smem_u32(sp.R[0]), ra1 = smem_u32(sp.R[1]);
-  for (int w = lane; w < lay.nw16; w += 32) {
-    float ms0 = -INFINITY, ms1 = -INFINITY, mr0 = -INFINITY, mr1 = -INFINITY;
+  // window maxima per row pair, interleaved (row 2ph+1, row 2ph); the 16-cell
+  // forward maxima of each row also go to wm16 for the fixup's per-POV skip
 #pragma unroll
-    for (int u = 0; u < kW / 4; ++u) {
-      const unsigned o = 4 * kW * w + 16 * u;
-      const float4 a0 = lds128(sa0 + o), a1 = lds128(sa1 + o);
-      const float4 b0 = lds128(ra0 + o), b1 = lds128(ra1 + o);
-      ms0 = fmaxf(ms0, fmaxf(fmaxf(a0.x, a0.y), fmaxf(a0.z, a0.w)));
-      ms1 = fmaxf(ms1, fmaxf(fmaxf(a1.x, a1.y), fmaxf(a1.z, a1.w)));
-      mr0 = fmaxf(mr0, fmaxf(fmaxf(b0.x, b0.y), fmaxf(b0.z, b0.w)));
-      mr1 = fmaxf(mr1, fmaxf(fmaxf(b1.x, b1.y), fmaxf(b1.z, b1.w)));
-    }
-    sp.W16S[w] = make_float2(ms1, ms0);
-    sp.W16R[w] = make_float2(mr1, mr0);
-    if (a.wm16 != nullptr) {
-      if (16 * w < Ls[0]) a.wm16[(sd.sdem_off + static_cast<long long>(qs[0]) * sd.pitch) / 16 + w] = ms0;
-      if (16 * w < Ls[1]) a.wm16[(sd.sdem_off + static_cast<long long>(qs[1]) * sd.pitch) / 16 + w] = ms1;
+  for (int ph = 0; ph < kR / 2; ++ph) {
+    const unsigned sa0 = smem_u32(sp.S[2 * ph]), sa1 = smem_u32(sp.S[2 * ph + 1]);
+    const unsigned ra0 = smem_u32(sp.R[2 * ph]), ra1 = smem_u32(sp.R[2 * ph + 1]);
+    for (int w = lane; w < lay.nw16; w += 32) {
+      float ms0 = -INFINITY, ms1 = -INFINITY, mr0 = -INFINITY, mr1 = -INFINITY;
+#pragma unroll
+      for (int u = 0; u < kW / 4; ++u) {
+        const unsigned o = 4 * kW * w + 16 * u;
+        const float4 a0 = lds128(sa0 + o), a1 = lds128(sa1 + o);
+        const float4 b0 = lds128(ra0 + o), b1 = lds128(ra1 + o);
+        ms0 = fmaxf(ms0, fmaxf(fmaxf(a0.x, a0.y), fmaxf(a0.z, a0.w)));
+        ms1 = fmaxf(ms1, fmaxf(fmaxf(a1.x, a1.y), fmaxf(a1.z, a1.w)));
+        mr0 = fmaxf(mr0, fmaxf(fmaxf(b0.x, b0.y), fmaxf(b0.z, b0.w)));
+        mr1 = fmaxf(mr1, fmaxf(fmaxf(b1.x, b1.y), fmaxf(b1.z, b1.w)));
+      }
+      sp.W16S[ph][w] = make_float2(ms1, ms0);
+      sp.W16R[ph][w] = make_float2(mr1, mr0);
+      if (a.wm16 != nullptr) {
+        const long long r0 = sd.sdem_off + static_cast<long long>(q0 + 2 * ph) * sd.pitch;
+        if (16 * w < Ls[2 * ph]) a.wm16[r0 / 16 + w] = ms0;
+        if (16 * w < Ls[2 * ph + 1]) a.wm16[(r0 + sd.pitch) / 16 + w] = ms1;
+      }
     }
   }
   __syncwarp();
-  for (int w = lane; w < lay.nw64; w += 32) {
-    float2 ms = make_float2(-INFINITY, -INFINITY), mr = make_float2(-INFINITY, -INFINITY);
 #pragma unroll
-    for (int u = 0; u < kH / kW; ++u) {
-      const float2 s2 = sp.W16S[(kH / kW) * w + u], r2 = sp.W16R[(kH / kW) * w + u];
-      ms = make_float2(fmaxf(ms.x, s2.x), fmaxf(ms.y, s2.y));
-      mr = make_float2(fmaxf(mr.x, r2.x), fmaxf(mr.y, r2.y));
+  for (int ph = 0; ph < kR / 2; ++ph) {
+    for (int w = lane; w < lay.nw64; w += 32) {
+      float2 ms = make_float2(-INFINITY, -INFINITY), mr = make_float2(-INFINITY, -INFINITY);
+#pragma unroll
+      for (int u = 0; u < kH / kW; ++u) {
+        const float2 s2 = sp.W16S[ph][(kH / kW) * w + u], r2 = sp.W16R[ph][(kH / kW) * w + u];
+        ms = make_float2(fmaxf(ms.x, s2.x), fmaxf(ms.y, s2.y));
+        mr = make_float2(fmaxf(mr.x, r2.x), fmaxf(mr.y, r2.y));
+      }
+      sp.W64S[ph][w] = ms;
+      sp.W64R[ph][w] = mr;
     }
-    sp.W64S[w] = ms;
-    sp.W64R[w] = mr;
   }
   __syncwarp();
   if (lane == 0) {
-    const int L = max(Ls[0], Ls[1]);
-    const int ntasks = 2 * ((L + kTaskPos - 1) / kTaskPos);
+    int L = 0;
+#pragma unroll
+    for (int r = 0; r < kR; ++r) L = max(L, Ls[r]);
+    const int ntasks = 2 * ((L + Geo<kR>::kP - 1) / Geo<kR>::kP);
     volatile int* v = ctl;
-    v[kS] = pr.x;
-    v[kLA] = Ls[0];
-    v[kLB] = Ls[1];
-    v[kFirstA] = firsts[0];
-    v[kFirstB] = firsts[1];
-    v[kQA] = qs[0];
-    v[kItA] = pr.y;
-    v[kItB] = pr.z;
+    v[kS] = s;
+    v[kQ0] = q0;
     v[kCap] = sd.max_dd;
+#pragma unroll
+    for (int r = 0; r < kR; ++r) {
+      v[kRowL + r] = Ls[r];
+      v[kRowFirst + r] = firsts[r];
+      v[kRowItem + r] = its[r];
+    }
     __threadfence_block();
     atomicExch(ctl + kRemaining, ntasks);
     __threadfence_block();
@@ -351,27 +384,29 @@ __device__ __forceinline__ void eval16_capped(PovP& P, unsigned sa, unsigned sb,
   }
 }
 
-template <bool kHl, bool kVis, bool kCapped>
-__device__ void run_task(const Layout3& lay, const Slot3& sl, const float* IV, int dir, int chunk, int L,
-                         int cap, PovP& P, int vis_p, uint8_t* vis, int vis_D, unsigned long long& skipped) {
-  const unsigned sa = smem_u32(dir ? sl.R[0] : sl.S[0]);
-  const unsigned sb = smem_u32(dir ? sl.R[1] : sl.S[1]);
-  const float2* W16 = dir ? sl.W16R : sl.W16S;
-  const float2* W64 = dir ? sl.W64R : sl.W64S;
+template <int kR, bool kHl, bool kVis, bool kCapped>
+__device__ void run_task(const Layout3<kR>& lay, const Slot3<kR>& sl, const float* IV, int dir, int chunk, int L,
+                         int cap, int ph, PovP& P, int vis_p, uint8_t* vis, int vis_D,
+                         unsigned long long& skipped) {
+  const unsigned sa = smem_u32(dir ? sl.R[2 * ph] : sl.S[2 * ph]);
+  const unsigned sb = smem_u32(dir ? sl.R[2 * ph + 1] : sl.S[2 * ph + 1]);
+  const float2* W16 = dir ? sl.W16R[ph] : sl.W16S[ph];
+  const float2* W64 = dir ? sl.W64R[ph] : sl.W64S[ph];
   // copy r with (k - y - r) even for k % 4 == 0: r = y & 1; the window
   // tests read copy 0 at element d + kOff
   const int r = P.y & 1;
   const unsigned ivb = smem_u32(IV + lay.copy(r)) + 4u * static_cast<unsigned>(kOff - r - P.y);
   const unsigned tb = smem_u32(IV + lay.copy(0)) + 4u * static_cast<unsigned>(kOff - P.y);
   const unsigned w16a = smem_u32(W16), w64a = smem_u32(W64);
-  const int ymin = chunk * kTaskPos;
+  constexpr int kP = Geo<kR>::kP;
+  const int ymin = chunk * kP;
   const bool capped = cap < L - 1;
   const int kmain = capped ? ymin + cap : INT_MAX / 2;
   const int klast = L - 1;
   int k0 = ymin;
   unsigned long long nskip = 0;
   int nev = 0;  // flush after 32 evaluated windows (A stays exact: scan2's bound)
-  const int ktest = ymin + SKS3_NEAR_NOTEST;
+  const int ktest = ymin + Geo<kR>::kNear;
   while (k0 <= klast) {
     // coarse 64-target windows where k0 is 64-aligned; fine windows up to
     // the next 64-aligned position
@@ -405,7 +440,7 @@ __device__ void run_task(const Layout3& lay, const Slot3& sl, const float* IV, i
   flush(P);
   if (kCapped && capped) {
     // masked tail (both POVs share dd, so one mask)
-    const int ylast = ymin + kTaskPos - 1;
+    const int ylast = ymin + kP - 1;
     const int kt_end = min(klast, ylast + cap);
     const int kcap = P.y + cap;
     int cnt = 0;
@@ -425,8 +460,8 @@ __device__ void run_task(const Layout3& lay, const Slot3& sl, const float* IV, i
           const bool m = d >= 1 && d <= cap;
           const float qn = __int_as_float(0x7fc00000);
           const float ivd = m ? IVf[d] : qn;
-          const float ea = dir ? sl.R[0][k] : sl.S[0][k];
-          const float eb = dir ? sl.R[1][k] : sl.S[1][k];
+          const float ea = dir ? sl.R[2 * ph][k] : sl.S[2 * ph][k];
+          const float eb = dir ? sl.R[2 * ph + 1][k] : sl.S[2 * ph + 1][k];
           const float t0 = __fmul_rn(__fadd_rn(__fadd_rn(ea, -P.hf0), -P.hl0), ivd);
           const float t1 = __fmul_rn(__fadd_rn(__fadd_rn(eb, -P.hf1), -P.hl1), ivd);
           const int kb = k + (1 << kSumShift);
@@ -447,16 +482,19 @@ __device__ void run_task(const Layout3& lay, const Slot3& sl, const float* IV, i
   skipped += nskip;
 }
 
-template <bool kCapped>
+template <int kR, bool kCapped>
 __global__ void __launch_bounds__(kThreads, 1) scan3_kernel(const __grid_constant__ ScanArgs a, int nslots, int lmax) {
   extern __shared__ __align__(16) float smem[];
-  const Layout3 lay(lmax);
+  const Layout3<kR> lay(lmax);
   int* ctl_all = reinterpret_cast<int*>(smem);
   float* IV = smem;
   float* slots = smem + lay.slots;
   const int tid = threadIdx.x;
   const int lane = tid & 31;
   const int warp = tid >> 5;
+  constexpr int kP = Geo<kR>::kP;
+  const int ph = lane / kP;    // row pair of this lane
+  const int yl = lane % kP;    // position within the task
 
   // fl(1/d) tables, 2 copies shifted by r: IV[r][i] = fl(1/(i - kOff + r)),
   // NaN for d <= 0 (a no-op target)
@@ -468,7 +506,7 @@ __global__ void __launch_bounds__(kThreads, 1) scan3_kernel(const __grid_constan
   }
   for (int i = tid; i < kMaxSlots * kCtlInts; i += blockDim.x) ctl_all[i] = 0;
   __syncthreads();
-  if (warp < nslots) load_pair(a, ctl_all + warp * kCtlInts, slots + warp * lay.slot, lay, lane);
+  if (warp < nslots) load_group<kR>(a, ctl_all + warp * kCtlInts, slots + warp * lay.slot, lay, lane);
 
   unsigned long long skipped = 0;
   int cur = warp % nslots;
@@ -507,17 +545,19 @@ __global__ void __launch_bounds__(kThreads, 1) scan3_kernel(const __grid_constan
     __threadfence_block();
     int* ctl = ctl_all + sl * kCtlInts;
     const volatile int* vc = ctl;
-    const int s = vc[kS], cap = vc[kCap];
-    const int Lr[2] = {vc[kLA], vc[kLB]};
-    const int firstr[2] = {vc[kFirstA], vc[kFirstB]};
-    const int itr[2] = {vc[kItA], vc[kItB]};
-    const int qa = vc[kQA];
-    const int L = max(Lr[0], Lr[1]);
-    const Slot3 sp = slot_ptrs(slots + sl * lay.slot, lay);
+    const int s = vc[kS], cap = vc[kCap], q0 = vc[kQ0];
+    int L = 0;
+#pragma unroll
+    for (int r = 0; r < kR; ++r) L = max(L, vc[kRowL + r]);
+    // this lane's two rows
+    const int Lr[2] = {vc[kRowL + 2 * ph], vc[kRowL + 2 * ph + 1]};
+    const int firstr[2] = {vc[kRowFirst + 2 * ph], vc[kRowFirst + 2 * ph + 1]};
+    const int itr[2] = {vc[kRowItem + 2 * ph], vc[kRowItem + 2 * ph + 1]};
+    const Slot3<kR> sp = slot_ptrs<kR>(slots + sl * lay.slot, lay);
     const int dir = task & 1, chunk = task >> 1;
 
     PovP P;
-    P.y = chunk * kTaskPos + lane;
+    P.y = chunk * kP + yl;
     P.v0 = P.y < Lr[0];
     P.v1 = P.y < Lr[1];
 #pragma unroll
@@ -534,9 +574,9 @@ __global__ void __launch_bounds__(kThreads, 1) scan3_kernel(const __grid_constan
       hl[p] = 0.f;
       if (y < Lr[p]) {
         const int x = dir ? (Lr[p] - 1 - y) : y;
-        const float* B = dir ? sp.R[p] : sp.S[p];
+        const float* B = dir ? sp.R[2 * ph + p] : sp.S[2 * ph + p];
         double h;
-        if (a.dbg_j0 >= 0 && s == 0 && qa + p == 0 && firstr[p] + x == a.dbg_j0) {
+        if (a.dbg_j0 >= 0 && s == 0 && q0 + 2 * ph + p == 0 && firstr[p] + x == a.dbg_j0) {
           h = a.dbg_h;
           vis_p = p;
           vis_D = min(cap, Lr[p] - 1 - y);
@@ -567,14 +607,16 @@ __global__ void __launch_bounds__(kThreads, 1) scan3_kernel(const __grid_constan
     const bool any_hl = __any_sync(0xffffffffu, P.hl0 != 0.f || P.hl1 != 0.f);
     if (vis_mode) {
       if (any_hl) {
-        run_task<true, true, kCapped>(lay, sp, IV, dir, chunk, L, cap, P, vis ? vis_p : -1, vis, vis_D, skipped);
+        run_task<kR, true, true, kCapped>(lay, sp, IV, dir, chunk, L, cap, ph, P, vis ? vis_p : -1, vis, vis_D,
+                                          skipped);
       } else {
-        run_task<false, true, kCapped>(lay, sp, IV, dir, chunk, L, cap, P, vis ? vis_p : -1, vis, vis_D, skipped);
+        run_task<kR, false, true, kCapped>(lay, sp, IV, dir, chunk, L, cap, ph, P, vis ? vis_p : -1, vis, vis_D,
+                                           skipped);
       }
     } else if (any_hl) {
-      run_task<true, false, kCapped>(lay, sp, IV, dir, chunk, L, cap, P, -1, nullptr, 0, skipped);
+      run_task<kR, true, false, kCapped>(lay, sp, IV, dir, chunk, L, cap, ph, P, -1, nullptr, 0, skipped);
     } else {
-      run_task<false, false, kCapped>(lay, sp, IV, dir, chunk, L, cap, P, -1, nullptr, 0, skipped);
+      run_task<kR, false, false, kCapped>(lay, sp, IV, dir, chunk, L, cap, ph, P, -1, nullptr, 0, skipped);
     }
 
     {
@@ -597,7 +639,7 @@ __global__ void __launch_bounds__(kThreads, 1) scan3_kernel(const __grid_constan
           a.fix_queue[a.fix_off[item] + slot] = pack_fix(static_cast<unsigned>(dir), static_cast<unsigned>(y));
         } else if (cvp != 0) {
           int* dst = ((dir && a.b.cv_bwd) ? a.b.cv_bwd : a.b.cv) + sd.sdem_off +
-                     static_cast<long long>(qa + p) * sd.pitch + firstr[p];
+                     static_cast<long long>(q0 + 2 * ph + p) * sd.pitch + firstr[p];
           atomicAdd(dst + (dir ? Lp - 1 - y : y), cvp);
         }
       }
@@ -605,7 +647,7 @@ __global__ void __launch_bounds__(kThreads, 1) scan3_kernel(const __grid_constan
     __syncwarp();
     int last = 0;
     if (lane == 0) last = atomicSub(ctl + kRemaining, 1) == 1;
-    if (__shfl_sync(0xffffffffu, last, 0)) load_pair(a, ctl, slots + sl * lay.slot, lay, lane);
+    if (__shfl_sync(0xffffffffu, last, 0)) load_group<kR>(a, ctl, slots + sl * lay.slot, lay, lane);
   }
   if (a.skipped != nullptr && lane == 0 && skipped != 0) {
     atomicAdd(a.skipped, 64ull * skipped);
@@ -614,27 +656,36 @@ __global__ void __launch_bounds__(kThreads, 1) scan3_kernel(const __grid_constan
 
 }  // namespace
 
-int scan3_slots(int lmax) {
+int scan3_slots(int lmax, int rows) {
   if (lmax >= 32768 - 128) return 0;
-  const Layout3 lay(lmax);
   const long long cap = 227 * 1024;
-  const long long n = (cap - 4LL * lay.slots) / (4LL * lay.slot);
-  return static_cast<int>(std::min<long long>(std::max<long long>(n, 0), kMaxSlots));
+  auto fit = [&](auto lay) {
+    const long long n = (cap - 4LL * lay.slots) / (4LL * lay.slot);
+    return static_cast<int>(std::min<long long>(std::max<long long>(n, 0), kMaxSlots));
+  };
+  return rows == 4 ? fit(Layout3<4>(lmax)) : fit(Layout3<2>(lmax));
 }
 
-int launch_scan3(const ScanArgs& a, int nslots, void* stream) {
-  int dev = 0;
-  cudaGetDevice(&dev);
-  int sms = 0;
-  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-  if (nslots < 1 || nslots > scan3_slots(a.lmax)) return static_cast<int>(cudaErrorInvalidValue);
-  const size_t smem = static_cast<size_t>(Layout3(a.lmax).total(nslots)) * sizeof(float);
-  cudaStream_t st = static_cast<cudaStream_t>(stream);
-  auto kern = a.any_capped ? scan3_kernel<true> : scan3_kernel<false>;
+template <int kR>
+static int launch_scan3_t(const ScanArgs& a, int nslots, int sms, cudaStream_t st) {
+  const size_t smem = static_cast<size_t>(Layout3<kR>(a.lmax).total(nslots)) * sizeof(float);
+  auto kern = a.any_capped ? scan3_kernel<kR, true> : scan3_kernel<kR, false>;
   cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
   if (e != cudaSuccess) return static_cast<int>(e);
   kern<<<sms, kThreads, smem, st>>>(a, nslots, a.lmax);
   return static_cast<int>(cudaGetLastError());
+}
+
+int launch_scan3(const ScanArgs& a, int nslots, int rows, void* stream) {
+  int dev = 0;
+  cudaGetDevice(&dev);
+  int sms = 0;
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  if ((rows != 2 && rows != 4) || nslots < 1 || nslots > scan3_slots(a.lmax, rows)) {
+    return static_cast<int>(cudaErrorInvalidValue);
+  }
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  return rows == 4 ? launch_scan3_t<4>(a, nslots, sms, st) : launch_scan3_t<2>(a, nslots, sms, st);
 }
 
 }  // namespace sks

@@ -94,8 +94,9 @@ struct ScanArgs {
   int lmax_all;           // longest row of the batch incl. long rows (fixup table)
   const float* ivt;       // global fl(1/d) table (lmax_all + 32 entries) when the
                           // fixup's shared-memory table would not fit; else nullptr
-  // scan3 (row pairs): pairs[i] = (sector slot, item of row q, item of row
-  // q+1 or -1, unused), longest first; the items index `items`/fix_off/fix_cnt
+  // scan3 (row groups of 2 or 4 adjacent skewed rows q0 .. q0+kR-1 of one
+  // sector): pairs[i] = the rows' items (-1: not scanned), longest group
+  // first; the items index `items`/fix_off/fix_cnt
   const int4* pairs;
   int n_pairs;
 };
@@ -122,8 +123,8 @@ int scan2_slots(int lmax);  // 0: rows too long for the target-lockstep kernel
 int scan2_max_row();        // longest row scan2 can hold (>= 1 slot)
 size_t scan2_smem_bytes(int lmax, int nslots);
 int launch_scan2(const ScanArgs& a, int nslots, void* stream);
-int scan3_slots(int lmax);  // row-pair slots that fit (0: rows too long)
-int launch_scan3(const ScanArgs& a, int nslots, void* stream);
+int scan3_slots(int lmax, int rows);  // row-group slots that fit (rows 2 or 4; 0: rows too long)
+int launch_scan3(const ScanArgs& a, int nslots, int rows, void* stream);
 // tile rows [tile_row0, tile_row0 + tile_rows) of the map (32 DEM rows each;
 // tile_rows < 0: to the end)
 int launch_unskew(const BatchDev& b, const float* unused, double* map,
