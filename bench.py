@@ -4,8 +4,10 @@
 Workload (BASELINE.json configs[1], "config 2"): synthetic 2000x2000 fractal
 DEM at 10 m (seed 7), 180 sectors, observer height 1.5 m, unlimited radius.
 A step is one full total viewshed: relocation + scan + fixup + unskew of all
-90 sector axes (sharded over ranks, LPT on exact work) + the reduce of the
-maps to rank 0 + area scaling, with the DEM resident in HBM.
+90 sector axes (N > 1: every rank runs its block of every sector's skewed
+rows, cuts rebalanced from measured times during warm-up) + the reduce of the
+maps to rank 0 + area scaling, with the DEM resident in HBM. The warm-up
+steps also cover the engine's scan-kernel autotune.
 
   python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
                   [--config 1..5] [--terrain fractal|smooth]

@@ -910,6 +910,26 @@ static int launch_scan2_t(const ScanArgs& a, int nslots, int sms, cudaStream_t s
   return static_cast<int>(cudaGetLastError());
 }
 
+// Shared-memory attribute of the instance launch_scan2 would use (loads its
+// module under lazy loading; the engine calls it before a timed launch).
+int prepare_scan2(int lmax, int any_capped) {
+  int copies = 0, fit = 0;
+  scan2_config(lmax, &copies, &fit);
+  if (copies == 0 || fit < 1) return 0;
+  const size_t smem = static_cast<size_t>(Layout2(lmax, copies).total(fit)) * sizeof(float);
+  auto set = [&](auto kern) {
+    return static_cast<int>(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
+  };
+  if (any_capped) {
+    return copies == 4 ? set(scan2_kernel<kThreads, 4, true>)
+           : copies == 2 ? set(scan2_kernel<kThreads, 2, true>)
+                         : set(scan2_kernel<kThreads, 1, true>);
+  }
+  return copies == 4 ? set(scan2_kernel<kThreads, 4, false>)
+         : copies == 2 ? set(scan2_kernel<kThreads, 2, false>)
+                       : set(scan2_kernel<kThreads, 1, false>);
+}
+
 int launch_scan2(const ScanArgs& a, int nslots, void* stream) {
   int dev = 0;
   cudaGetDevice(&dev);

@@ -125,6 +125,8 @@ size_t scan2_smem_bytes(int lmax, int nslots);
 int launch_scan2(const ScanArgs& a, int nslots, void* stream);
 int scan3_slots(int lmax, int rows);  // row-group slots that fit (rows 2 or 4; 0: rows too long)
 int launch_scan3(const ScanArgs& a, int nslots, int rows, void* stream);
+int prepare_scan2(int lmax, int any_capped);             // kernel attributes only (before a timed launch)
+int prepare_scan3(int lmax, int rows, int any_capped);
 // tile rows [tile_row0, tile_row0 + tile_rows) of the map (32 DEM rows each;
 // tile_rows < 0: to the end)
 int launch_unskew(const BatchDev& b, const float* unused, double* map,

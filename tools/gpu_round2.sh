@@ -12,10 +12,11 @@ timeout 300 python bench.py --no-cpu-baseline --terrain smooth > $OUT/bench_smoo
 if [ "$2" != "skip_ref" ]; then
   timeout 600 python bench.py --impl reference > $OUT/bench_ref.json 2> $OUT/bench_ref.err
 fi
-timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file $OUT/launches.csv \
+# prof_step runs one step: pin the kernel the autotune keeps for each terrain
+SKS_SCAN3=4 timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file $OUT/launches.csv \
   python tools/prof_step.py --steps 1 > $OUT/launches.log 2>&1
-timeout 900 ncu --set full --clock-control none --import-source on -k regex:"scan2_kernel|relocate_kernel|fixup_kernel|unskew_pipe_kernel" -c 4 \
+SKS_SCAN3=4 timeout 900 ncu --set full --clock-control none --import-source on -k regex:"scan[23]_kernel|relocate_kernel|fixup_kernel|unskew_pipe_kernel" -c 4 \
   -o $OUT/full python tools/prof_step.py --steps 1 > $OUT/ncu_full.log 2>&1
-timeout 900 ncu --set full --clock-control none -k regex:"scan2_kernel" -c 1 \
+SKS_SCAN3=0 timeout 900 ncu --set full --clock-control none -k regex:"scan2_kernel" -c 1 \
   -o $OUT/scan_smooth python tools/prof_step.py --steps 1 --terrain smooth > $OUT/ncu_smooth.log 2>&1
 echo done

@@ -26,7 +26,8 @@ def val(d, k):
     return v * scale if scale else v
 
 
-names = {"scan2_kernel": "scan_kernel", "relocate_kernel": "relocate_kernel", "unskew_pipe_kernel": "unskew_kernel",
+names = {"scan2_kernel": "scan_kernel", "scan3_kernel": "scan_kernel", "relocate_kernel": "relocate_kernel",
+         "unskew_pipe_kernel": "unskew_kernel",
          "fixup_kernel": "fixup_kernel"}
 out = {"source": note}
 for d in data:
