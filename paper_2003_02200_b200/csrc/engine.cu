@@ -492,9 +492,12 @@ struct sks_context {
   // block): scan3 over groups of adjacent rows evaluates fewer windows on
   // rough terrain and more on near-flat terrain (config 2 scan: fractal
   // 58.9 ms scan2, 52.9 pairs, 50.2 quads; SmoothedNoise 123.1, 135.6,
-  // 155.4), so the first calls of a shape try quads, pairs and scan2 (each
-  // timed on the device) and the fastest is kept. All give identical
-  // results. SKS_SCAN3 = 0 / 1 / 4 forces scan2 / pairs / quads.
+  // 155.4), so the first call of a shape scans its first batch with scan2,
+  // pairs and quads (each timed on the device, the cv pool re-zeroed in
+  // between) and the fastest is kept for every later batch and call; all
+  // give identical results. Tuning inside one call keeps later calls
+  // uniform (the row-block rebalancers measure them). SKS_SCAN3 = 0 / 1 / 4
+  // forces scan2 / pairs / quads.
   struct ScanTune {
     float t[5] = {-1.f, -1.f, -1.f, -1.f, -1.f};  // device time per mode (2, 3, 4)
     int choice = 0;  // 0: undecided, else the mode
@@ -659,28 +662,7 @@ void run_sectors(sks_context* ctx, const float* d_dem, int dimy, int dimx, doubl
   // scan kernel choice (sks_context::ScanTune): time one call of each where
   // scan3 fits, then keep the faster
   auto& tn = ctx->tune[std::make_tuple(dimy, dimx, cfg->ns, cfg->max_distance, part, nparts)];
-  int mode = tn.choice;
-  bool timing = false;
-  if (mode == 0 && sks_context::forced_scan() == 0) {
-    // candidate modes in trial order: quads, pairs, scan2 (those that fit)
-    auto fits = [&](int m) {
-      bool ok = false;
-      for (auto& bp : P.batches) ok |= sks_context::mode_fits(*bp, std::max(bp->lmax, 4), m);
-      return ok;
-    };
-    for (int m : {4, 3, 2}) {
-      if (tn.t[m] < 0.f && fits(m)) {
-        mode = m;
-        break;
-      }
-    }
-    if (mode == 0 || !fits(3)) {
-      tn.choice = mode = 2;
-    } else {
-      timing = true;
-    }
-  }
-  float t_tune = 0.f;
+  const bool tune_now = tn.choice == 0 && sks_context::forced_scan() == 0;
   long long flagged = 0, evals = 0, skipped = 0;
   for (auto& bp : P.batches) {
     Batch& b = *bp;
@@ -693,21 +675,40 @@ void run_sectors(sks_context* ctx, const float* d_dem, int dimy, int dimx, doubl
     if (stats) cuda_check(cudaEventRecord(ctx->ev[0], st), "event");
     if (!fused) ctx->relocate(d_dem, dimy, dimx, bd, b, st);
     if (stats) cuda_check(cudaEventRecord(ctx->ev[1], st), "event");
-    if (timing) {
-      // module loads and attribute calls stay outside the timed region
-      const int lm = std::max(b.lmax, 4);
-      const int rows = sks_context::scan3_rows(b, lm, mode);
-      cuda_check(rows > 0 ? prepare_scan3(lm, rows, b.any_capped ? 1 : 0) : prepare_scan2(lm, b.any_capped ? 1 : 0),
-                 "prepare scan");
-      cuda_check(cudaEventRecord(ctx->ev[5], st), "event");
-    }
-    ctx->scan_batch(b, a, st, false, false, mode);
-    if (timing) {
-      cuda_check(cudaEventRecord(ctx->ev[6], st), "event");
-      cuda_check(cudaEventSynchronize(ctx->ev[6]), "sync");
-      float ms = 0.f;
-      cuda_check(cudaEventElapsedTime(&ms, ctx->ev[5], ctx->ev[6]), "elapsed");
-      t_tune += ms;
+    if (tune_now && tn.choice == 0) {
+      // first call of the shape: scan this batch with every kernel mode that
+      // fits (each timed on the device, the cv pool re-zeroed in between:
+      // every trial leaves the same cv, queue and window maxima), keep the
+      // fastest for every later batch and call
+      int best = 0;
+      float best_ms = 0.f;
+      int ntrial = 0;
+      for (int m : {2, 3, 4}) {
+        const int lm = std::max(b.lmax, 4);
+        if (!sks_context::mode_fits(b, lm, m)) continue;
+        if (ntrial++ > 0) {
+          cuda_check(cudaMemsetAsync(ctx->cv.p, 0, static_cast<size_t>(b.pool_elems) * sizeof(int), st),
+                     "memset cv");
+        }
+        // module loads and attribute calls stay outside the timed region
+        const int rows = sks_context::scan3_rows(b, lm, m);
+        cuda_check(rows > 0 ? prepare_scan3(lm, rows, b.any_capped ? 1 : 0) : prepare_scan2(lm, b.any_capped ? 1 : 0),
+                   "prepare scan");
+        cuda_check(cudaEventRecord(ctx->ev[5], st), "event");
+        ctx->scan_batch(b, a, st, false, false, m);
+        cuda_check(cudaEventRecord(ctx->ev[6], st), "event");
+        cuda_check(cudaEventSynchronize(ctx->ev[6]), "sync");
+        float ms = 0.f;
+        cuda_check(cudaEventElapsedTime(&ms, ctx->ev[5], ctx->ev[6]), "elapsed");
+        tn.t[m] = ms;
+        if (best == 0 || ms < best_ms) {
+          best = m;
+          best_ms = ms;
+        }
+      }
+      tn.choice = best;  // the pool holds the last trial's state (the same for every mode)
+    } else {
+      ctx->scan_batch(b, a, st, false, false, tn.choice);
     }
     if (stats) cuda_check(cudaEventRecord(ctx->ev[2], st), "event");
     ctx->fixup_batch(a, st);
@@ -757,19 +758,6 @@ void run_sectors(sks_context* ctx, const float* d_dem, int dimy, int dimx, doubl
       skipped += static_cast<long long>(sk);
     }
     evals += b.target_evals;
-  }
-  if (timing) {
-    tn.t[mode] = t_tune;
-    bool done = true;
-    int best = 0;
-    for (int m : {4, 3, 2}) {
-      bool ok = false;
-      for (auto& bp : P.batches) ok |= sks_context::mode_fits(*bp, std::max(bp->lmax, 4), m);
-      if (!ok) continue;
-      if (tn.t[m] < 0.f) done = false;
-      else if (best == 0 || tn.t[m] < tn.t[best]) best = m;
-    }
-    if (done) tn.choice = best;
   }
   if (stats) {
     stats->skew_seconds += t_skew;
