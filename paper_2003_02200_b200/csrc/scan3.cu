@@ -40,7 +40,10 @@ namespace {
 constexpr int kW = 16;        // fine window (targets)
 constexpr int kH = 64;        // coarse window (targets)
 constexpr int kOff = 128;  // table index offset (dd >= -kOff + 1 addressable)
-constexpr int kThreads = 768;
+#ifndef SKS3_THREADS
+#define SKS3_THREADS 768
+#endif
+constexpr int kThreads = SKS3_THREADS;
 constexpr int kMaxSlots = 8;
 constexpr int kCtlInts = 32;
 constexpr float kBand = 5.9604644775390625e-07f;  // 10 * 2^-24
