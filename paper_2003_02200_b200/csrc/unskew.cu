@@ -118,9 +118,16 @@ __global__ void __launch_bounds__(32 * kNW, SKS_UNSKEW_MINB) unskew_pipe_kernel(
   constexpr int kSecWords = static_cast<int>(sizeof(SectorDev) / 4);
   static_assert(sizeof(SectorDev) % 8 == 0, "SectorDev copied as whole words");
   __shared__ SectorDev sring[3];
-  auto load_sec = [&](int s) {
+  // Row-block runs (kBlocks): the sectors with a skewed row of this run in
+  // the tile, compacted in ascending order at the start, so the loop below
+  // (one barrier per sector) walks only those (8 ranks: ~1/8 of them).
+  constexpr int kMaxList = 2048;
+  __shared__ short slist[kBlocks ? kMaxList : 1];
+  __shared__ int nlist_s;
+  auto load_sec = [&](int idx) {
+    const int s = (kBlocks && nlist_s >= 0) ? slist[idx] : idx;
     if (threadIdx.x < kSecWords) {
-      reinterpret_cast<int*>(sring + s % 3)[threadIdx.x] =
+      reinterpret_cast<int*>(sring + idx % 3)[threadIdx.x] =
           __ldg(reinterpret_cast<const int*>(b.sectors + s) + threadIdx.x);
     }
   };
@@ -222,18 +229,55 @@ __global__ void __launch_bounds__(32 * kNW, SKS_UNSKEW_MINB) unskew_pipe_kernel(
       if (ty + kNW * k < kTR) scv[bf][ty + kNW * k][tx] = P.v[k];
     }
   };
+  int nsec = b.n_sectors;
+  if (kBlocks) {
+    if (threadIdx.x == 0) nlist_s = b.n_sectors <= kMaxList ? 0 : -1;
+    __syncthreads();
+    if (nlist_s >= 0) {
+      // same test as fetch's: some skewed row the tile reads is this run's
+      for (int c0 = 0; c0 < b.n_sectors; c0 += blockDim.x) {
+        const int s = c0 + threadIdx.x;
+        bool own = false;
+        if (s < b.n_sectors) {
+          const SectorDev& sd = b.sectors[s];
+          int iv[6];
+#pragma unroll
+          for (int k = 0; k < 6; ++k) iv[k] = sd.inv[k];
+          int i_lo, j_lo, ni;
+          const int nj = box(iv, &i_lo, &j_lo, &ni);
+          own = true;
+          if (!(sd.q_lo <= 0 && sd.q_hi >= sd.skw_rows)) {
+            const double tan = sd.shear_tan;
+            const int d_lo = __double2int_rz(__dmul_rn(tan, static_cast<double>(j_lo)));
+            const int d_hi = __double2int_rz(__dmul_rn(tan, static_cast<double>(j_lo + nj - 1)));
+            const int p_min = sd.base + i_lo - 1 - d_hi, p_max = sd.base + i_lo + kUT - 1 - d_lo;
+            own = max(p_min, sd.q_lo) <= min(p_max, sd.q_hi - 1);
+          }
+        }
+        // ordered compaction: warp ballots, then the warps in turn
+        const unsigned m = __ballot_sync(0xffffffffu, own);
+        for (int w = 0; w < kNW; ++w) {
+          if (ty == w && own) slist[nlist_s + __popc(m & ((1u << tx) - 1u))] = static_cast<short>(s);
+          __syncthreads();
+          if (ty == w && tx == 0) nlist_s += __popc(m);
+          __syncthreads();
+        }
+      }
+      nsec = nlist_s;
+    }
+  }
   Pre P;
-  load_sec(0);
-  if (b.n_sectors > 1) load_sec(1);
+  if (nsec > 0) load_sec(0);
+  if (nsec > 1) load_sec(1);
   __syncthreads();
-  fetch(0, P);
-  for (int s = 0; s < b.n_sectors; ++s) {
+  if (nsec > 0) fetch(0, P);
+  for (int s = 0; s < nsec; ++s) {
     const int bf = s & 1;
     commit(P, bf);
     __syncthreads();  // sector s staged; sector s-1's buffer (bf ^ 1) no longer read
     // slot (s+2) % 3 held sector s-1, last read by fetch(s-1) before this barrier
-    if (s + 2 < b.n_sectors) load_sec(s + 2);
-    if (s + 1 < b.n_sectors) fetch(s + 1, P);
+    if (s + 2 < nsec) load_sec(s + 2);
+    if (s + 1 < nsec) fetch(s + 1, P);
     if (kBlocks && sown[bf] == 0) continue;
     const USect& c = ssec[bf];
     const int iv0 = c.iv[0], iv1 = c.iv[1], iv2 = c.iv[2], iv3 = c.iv[3], iv4 = c.iv[4], iv5 = c.iv[5];
@@ -298,7 +342,7 @@ __global__ void __launch_bounds__(32 * kNW, SKS_UNSKEW_MINB) unskew_pipe_kernel(
         if (a) va = __dmul_rn(static_cast<double>(scv[bf][ir][jl]), corr);
         if (!a || cc) vb = __dmul_rn(static_cast<double>(scv[bf][ir - 1][jl]), corr);
         if (!a && !cc && b.dem != nullptr) {
-          const SectorDev& sd = b.sectors[s];
+          const SectorDev& sd = b.sectors[(kBlocks && nlist_s >= 0) ? slist[s] : s];
           const int p = sd.base + i - sdest[bf][jl];
           const int2 rg = (p >= 1 && p - 1 < sd.skw_rows) ? __ldg(b.ranges + sd.row_off + p - 1) : make_int2(0, 0);
           if (j < rg.x || j >= rg.y) vb = 0.0;
