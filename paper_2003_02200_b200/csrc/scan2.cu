@@ -66,10 +66,11 @@ constexpr int kW = SKS_FINE_W;  // fine window (targets): 8 or 16
 #define SKS_COARSE_NOTEST SKS_NEAR_NOTEST
 #endif
 #ifndef SKS_COARSE_W
-#define SKS_COARSE_W 64
+#define SKS_COARSE_W 128  // round 2: 128 vs 64: SmoothedNoise 122.1 vs 123.1 ms, config 5 3764 vs 3878 ms (fractal config 2 59.3 vs 58.9, where scan3 runs)
 #endif
 constexpr int kH = SKS_COARSE_W;  // coarse window (targets)
-static_assert(kTaskPovs % kH == 0, "task starts must be aligned to coarse windows");
+// coarse windows longer than a task: tested only where k0 is kH-aligned
+constexpr bool kCoarseAligned = kTaskPovs % kH == 0;
 constexpr int kOff = 128;  // table index offset (dd >= -kOff + 1 addressable)
 #ifndef SKS_SCAN_THREADS
 #define SKS_SCAN_THREADS 768
@@ -570,7 +571,7 @@ __device__ void run_task(const ScanArgs& a, const Layout2& lay, const Slot& sl, 
   const int ktest = ymin + SKS_NEAR_NOTEST;
   const int kctest = ymin + SKS_COARSE_NOTEST;  // coarse tests only from here
   while (k0 <= klast) {
-    if (!kVis && k0 >= kctest && k0 + kH - 1 <= kmain) {
+    if (!kVis && (kCoarseAligned || (k0 & (kH - 1)) == 0) && k0 >= kctest && k0 + kH - 1 <= kmain) {
       const float2 em = lds64(w64a + 8u * (static_cast<unsigned>(k0) / kH));
       if (window_hidden<kHl, kNC>(P, em, tb, k0, kH)) {
         k0 += kH;
@@ -578,7 +579,7 @@ __device__ void run_task(const ScanArgs& a, const Layout2& lay, const Slot& sl, 
         continue;
       }
     }
-    const int kc = k0 + kH;
+    const int kc = kCoarseAligned ? k0 + kH : (k0 & ~(kH - 1)) + kH;
     while (k0 < kc && k0 <= klast && k0 + kW - 1 <= kmain) {
       if (!kVis && k0 >= ktest) {
         const float2 em = lds64(w16a + 8u * (static_cast<unsigned>(k0) / kW));

@@ -38,7 +38,10 @@ namespace sks {
 namespace {
 
 constexpr int kW = 16;        // fine window (targets)
-constexpr int kH = 64;        // coarse window (targets)
+#ifndef SKS3_COARSE
+#define SKS3_COARSE 128  // measured (quads, config 2): 32: 54.3 ms scan, 64: 50.2, 128: 49.7, 256: 51.4
+#endif
+constexpr int kH = SKS3_COARSE;  // coarse window (targets)
 constexpr int kOff = 128;  // table index offset (dd >= -kOff + 1 addressable)
 #ifndef SKS3_THREADS
 #define SKS3_THREADS 768
