@@ -368,6 +368,7 @@ def run_ours(args, world, rank, local):
     flagged = 0
     evals = 0
     skipped = 0
+    scan_kernel = 0
     for _ in range(args.steps):
         flush.fill_(1)  # evict L2 (126 MB) between steps, outside the timed region
         torch.cuda.synchronize()
@@ -388,6 +389,7 @@ def run_ours(args, world, rank, local):
         flagged += st.flagged_groups
         evals += st.target_evals
         skipped += st.skipped_target_slots
+        scan_kernel = st.scan_kernel
     sampler.stop()
     total_ms = max_over_ranks(total_ms, world)
     scan_s = max_over_ranks(phases["scan"], world)
@@ -471,7 +473,10 @@ def run_ours(args, world, rank, local):
                          "last_warmup_rank_ms": [round(x, 3) for x in rank_ms],
                          "note": "row-block cuts moved from measured per-rank times during warm-up, then frozen"}
                         if world > 1 else None),
-        "roofline": {"kernel": "scan_kernel (FP32-issue bound)", "bound": "fp32",
+        "scan_kernel": {2: "scan2 (one row x 64 positions per task)", 3: "scan3 row pairs",
+                        4: "scan3 row quads"}.get(scan_kernel, str(scan_kernel)),
+        "roofline": {"kernel": ({2: "scan2_kernel", 3: "scan3_kernel<2>", 4: "scan3_kernel<4>"}.get(scan_kernel, "scan")
+                                + " (FP32-issue bound)"), "bound": "fp32",
                      "achieved": scan_achieved / 1e12, "peak": fp32_peak / 1e12, "unit": "TFLOP/s",
                      "frac": scan_achieved / fp32_peak, "traffic": traffic,
                      "executed_frac": executed / fp32_peak,

@@ -75,6 +75,10 @@ typedef struct {
   long long d2h_bytes;
   long long skipped_target_slots; /* lane-target slots decided by the
                                      certified hidden-block skip */
+  int scan_kernel;  /* scan kernel of the call's last batch: 2 = one row x 64
+                       positions per task, 3 = row pairs, 4 = row quads
+                       (autotuned per shape) */
+  int pad_;
 } sks_stats;
 
 /* SectorPlan, skew.hpp:29-41. ops: 0 Transpose, 1 FlipCols, 2 FlipRows. */

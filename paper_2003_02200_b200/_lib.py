@@ -46,7 +46,8 @@ class StatsC(C.Structure):
                 ("sectors", C.c_int), ("batches", C.c_int),
                 ("kernel_launches", C.c_longlong), ("target_evals", C.c_longlong),
                 ("flagged_groups", C.c_longlong), ("h2d_bytes", C.c_longlong),
-                ("d2h_bytes", C.c_longlong), ("skipped_target_slots", C.c_longlong)]
+                ("d2h_bytes", C.c_longlong), ("skipped_target_slots", C.c_longlong),
+                ("scan_kernel", C.c_int), ("pad_", C.c_int)]
 
     def as_dict(self) -> dict:
         return {name: getattr(self, name) for name, _ in self._fields_}

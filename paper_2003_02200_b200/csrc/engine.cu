@@ -770,6 +770,11 @@ void run_sectors(sks_context* ctx, const float* d_dem, int dimy, int dimx, doubl
     stats->target_evals += evals;
     stats->flagged_groups += flagged;
     stats->skipped_target_slots += skipped;
+    if (!P.batches.empty()) {
+      const Batch& lb = *P.batches.back();
+      const int rows = sks_context::scan3_rows(lb, std::max(lb.lmax, 4), tn.choice);
+      stats->scan_kernel = rows == 4 ? 4 : rows == 2 ? 3 : 2;
+    }
   }
 }
 

@@ -318,6 +318,7 @@ void total_multi(const float* dem, int dimy, int dimx, double cellsize, const sk
       total.target_evals += s.target_evals;
       total.flagged_groups += s.flagged_groups;
       total.skipped_target_slots += s.skipped_target_slots;
+      total.scan_kernel = s.scan_kernel;
       total.batches += s.batches;
     }
     total.sectors = cfg->ns / 2;

@@ -42,6 +42,11 @@ constexpr int kW = 16;        // fine window (targets)
 #define SKS3_COARSE 128  // measured (quads, config 2): 32: 54.3 ms scan, 64: 50.2, 128: 49.7, 256: 51.4
 #endif
 constexpr int kH = SKS3_COARSE;  // coarse window (targets)
+#ifndef SKS3_TOP
+#define SKS3_TOP 0  // third level (targets, a multiple of kH; 0: two levels)
+#endif
+constexpr int kTop = SKS3_TOP;
+constexpr int kTopN = kTop > 0 ? kTop / kH : 1;  // coarse windows per top window
 constexpr int kOff = 128;  // table index offset (dd >= -kOff + 1 addressable)
 #ifndef SKS3_THREADS
 #define SKS3_THREADS 768
@@ -70,7 +75,7 @@ struct Geo {
 template <int kR>
 struct Layout3 {
   int lb;      // row buffer (floats) per row and direction
-  int nw16, nw64;
+  int nw16, nw64, nwt;  // nw64 rounded up to kTopN (padding windows are -inf)
   int T;       // table length per copy (floats, a multiple of 32)
   int wpair;   // floats of window maxima per row pair
   int slot;    // floats per slot (kR rows)
@@ -79,9 +84,10 @@ struct Layout3 {
   __host__ __device__ explicit Layout3(int lmax) {
     lb = ((lmax + kH + kH - 1) / kH) * kH;
     nw16 = lb / kW;
-    nw64 = lb / kH;
+    nw64 = ((lb / kH + kTopN - 1) / kTopN) * kTopN;
+    nwt = kTop > 0 ? nw64 / kTopN : 0;
     T = ((kOff + lb + 16 + 31) / 32) * 32;
-    wpair = 4 * nw16 + 4 * nw64;
+    wpair = 4 * nw16 + 4 * nw64 + 4 * nwt;
     slot = 2 * kR * lb + (kR / 2) * wpair;
     tables = kMaxSlots * kCtlInts;
     slots = tables + 2 * T + kCopy1Shift + 14;  // 14: keeps the slots 16-byte aligned
@@ -99,6 +105,7 @@ struct Slot3 {
   float* R[kR];  // reversed copies
   float2* W16S[kR / 2]; float2* W16R[kR / 2];  // per row pair: (m(row 2ph+1), m(row 2ph)) per window
   float2* W64S[kR / 2]; float2* W64R[kR / 2];
+  float2* WTS[kR / 2]; float2* WTR[kR / 2];  // top level (kTop > 0)
 };
 
 template <int kR>
@@ -116,6 +123,8 @@ __device__ __forceinline__ Slot3<kR> slot_ptrs(float* base, const Layout3<kR>& l
     s.W16R[ph] = w + lay.nw16;
     s.W64S[ph] = w + 2 * lay.nw16;
     s.W64R[ph] = w + 2 * lay.nw16 + lay.nw64;
+    s.WTS[ph] = w + 2 * lay.nw16 + 2 * lay.nw64;
+    s.WTR[ph] = w + 2 * lay.nw16 + 2 * lay.nw64 + lay.nwt;
   }
   return s;
 }
@@ -198,17 +207,36 @@ __device__ void load_group(const ScanArgs& a, int* ctl, float* base, const Layou
   for (int ph = 0; ph < kR / 2; ++ph) {
     for (int w = lane; w < lay.nw64; w += 32) {
       float2 ms = make_float2(-INFINITY, -INFINITY), mr = make_float2(-INFINITY, -INFINITY);
+      if ((kH / kW) * w < lay.nw16) {
 #pragma unroll
-      for (int u = 0; u < kH / kW; ++u) {
-        const float2 s2 = sp.W16S[ph][(kH / kW) * w + u], r2 = sp.W16R[ph][(kH / kW) * w + u];
-        ms = make_float2(fmaxf(ms.x, s2.x), fmaxf(ms.y, s2.y));
-        mr = make_float2(fmaxf(mr.x, r2.x), fmaxf(mr.y, r2.y));
+        for (int u = 0; u < kH / kW; ++u) {
+          const float2 s2 = sp.W16S[ph][(kH / kW) * w + u], r2 = sp.W16R[ph][(kH / kW) * w + u];
+          ms = make_float2(fmaxf(ms.x, s2.x), fmaxf(ms.y, s2.y));
+          mr = make_float2(fmaxf(mr.x, r2.x), fmaxf(mr.y, r2.y));
+        }
       }
       sp.W64S[ph][w] = ms;
       sp.W64R[ph][w] = mr;
     }
   }
   __syncwarp();
+  if (kTop > 0) {
+#pragma unroll
+    for (int ph = 0; ph < kR / 2; ++ph) {
+      for (int w = lane; w < lay.nwt; w += 32) {
+        float2 ms = make_float2(-INFINITY, -INFINITY), mr = make_float2(-INFINITY, -INFINITY);
+#pragma unroll
+        for (int u = 0; u < kTopN; ++u) {
+          const float2 s2 = sp.W64S[ph][kTopN * w + u], r2 = sp.W64R[ph][kTopN * w + u];
+          ms = make_float2(fmaxf(ms.x, s2.x), fmaxf(ms.y, s2.y));
+          mr = make_float2(fmaxf(mr.x, r2.x), fmaxf(mr.y, r2.y));
+        }
+        sp.WTS[ph][w] = ms;
+        sp.WTR[ph][w] = mr;
+      }
+    }
+    __syncwarp();
+  }
   if (lane == 0) {
     int L = 0;
 #pragma unroll
@@ -402,6 +430,7 @@ __device__ void run_task(const Layout3<kR>& lay, const Slot3<kR>& sl, const floa
   const unsigned sb = smem_u32(dir ? sl.R[2 * ph + 1] : sl.S[2 * ph + 1]);
   const float2* W16 = dir ? sl.W16R[ph] : sl.W16S[ph];
   const float2* W64 = dir ? sl.W64R[ph] : sl.W64S[ph];
+  const unsigned wta = kTop > 0 ? smem_u32(dir ? sl.WTR[ph] : sl.WTS[ph]) : 0u;
   // copy r with (k - y - r) even for k % 4 == 0: r = y & 1; the window
   // tests read copy 0 at element d + kOff
   const int r = P.y & 1;
@@ -418,8 +447,16 @@ __device__ void run_task(const Layout3<kR>& lay, const Slot3<kR>& sl, const floa
   int nev = 0;  // flush after 32 evaluated windows (A stays exact: scan2's bound)
   const int ktest = ymin + Geo<kR>::kNear;
   while (k0 <= klast) {
-    // coarse 64-target windows where k0 is 64-aligned; fine windows up to
-    // the next 64-aligned position
+    // top windows (kTop > 0) and coarse windows where k0 is aligned to them;
+    // fine windows up to the next coarse-aligned position
+    if (kTop > 0 && !kVis && (k0 & (kTop - 1)) == 0 && k0 >= ktest && k0 + kTop - 1 <= kmain) {
+      const float2 em = lds64(wta + 8u * (static_cast<unsigned>(k0) / kTop));
+      if (window_hidden<kHl>(P, em, tb, k0, kTop)) {
+        k0 += kTop;
+        nskip += kTop;
+        continue;
+      }
+    }
     if (!kVis && (k0 & (kH - 1)) == 0 && k0 >= ktest && k0 + kH - 1 <= kmain) {
       const float2 em = lds64(w64a + 8u * (static_cast<unsigned>(k0) / kH));
       if (window_hidden<kHl>(P, em, tb, k0, kH)) {

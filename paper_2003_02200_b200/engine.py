@@ -162,10 +162,13 @@ class EngineStats:
     h2d_bytes: int = 0
     d2h_bytes: int = 0
     skipped_target_slots: int = 0
+    scan_kernel: int = 0  # 2: one row x 64 positions, 3: row pairs, 4: row quads
 
     @classmethod
     def from_c(cls, s: _lib.StatsC) -> "EngineStats":
-        return cls(**s.as_dict())
+        d = s.as_dict()
+        d.pop("pad_", None)
+        return cls(**d)
 
 
 @dataclass
