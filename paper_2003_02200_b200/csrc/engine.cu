@@ -413,7 +413,8 @@ struct sks_context {
   }
 
   void ensure_pools(const Batch& b, bool split_bwd) {
-    sdem.ensure(static_cast<size_t>(b.pool_elems) * sizeof(float), device);
+    // + slack: the fixup reads whole 16-position blocks past a row end
+    sdem.ensure(static_cast<size_t>(b.pool_elems + 64) * sizeof(float), device);
     cv.ensure(static_cast<size_t>(b.pool_elems) * sizeof(int), device);
     if (split_bwd) cvb.ensure(static_cast<size_t>(b.pool_elems) * sizeof(int), device);
     queue.ensure(static_cast<size_t>(b.fix_cap) * sizeof(unsigned), device);

@@ -39,6 +39,12 @@ constexpr float kBand = 5.9604644775390625e-07f;  // 10 * 2^-24, as in the scan 
 #define SKS_FIX_WARPS 8
 #endif
 constexpr int kWarps = SKS_FIX_WARPS;
+#ifndef SKS_FIX_FULL16
+#define SKS_FIX_FULL16 1  // candidate blocks through eval16 (eval_block only for band blocks)
+#endif
+#ifndef SKS_FIX_COARSE
+#define SKS_FIX_COARSE 1  // one bound test per batch of kWm windows before the per-window tests
+#endif
 
 // Exact state of one POV scan (the reference recurrence under the filter).
 struct ExactState {
@@ -196,6 +202,65 @@ __device__ __forceinline__ void eval_range(ExactState& S, const float* row, cons
   for (; dd <= db; ++dd) exact_step(S, row, x, sg, dd, row[x + sg * dd], ivt[dd]);
 }
 
+// The targets of block w (positions 16w .. 16w+15) with dd in [da, db], in
+// scan order: target i of the block has dd = d0 + i (d0 = 16w - x forward,
+// x - 16w - 15 backward) and elevation e[i] (e[15 - i] backward); targets
+// outside [da, db] get a NaN 1/d and are no-ops. Branch-free certified pass
+// (predicated updates, ring sums as one packed accumulator, a near-hit count);
+// returns false with S untouched when a target fell in the band (the caller
+// re-runs the block with eval_block). The row is read at positions up to
+// 16 ceil(L / 16) - 1 (the sdem pool has slack for the last row).
+__device__ __forceinline__ bool eval16(ExactState& S, const float* row, const float* ivt, int w, int sg, int d0,
+                                       int da, int db) {
+  float e[16], q[16];
+  const float* pb = row + 16 * w;
+#pragma unroll
+  for (int i = 0; i < 16; ++i) e[i] = __ldg(pb + i);
+  if (db - da == 15) {
+    const float* iv = ivt + da;
+#pragma unroll
+    for (int i = 0; i < 16; ++i) q[i] = iv[i];
+  } else {
+#pragma unroll
+    for (int i = 0; i < 16; ++i) {
+      const int dd = d0 + i;
+      const int idx = min(max(dd, da), db);
+      const float v = ivt[idx];
+      q[i] = dd == idx ? v : __int_as_float(0x7fc00000);
+    }
+  }
+  int A = 0, rr = 0;
+  float G = 0.f;
+  float hi = S.hi, lo = S.lo;
+#pragma unroll
+  for (int i = 0; i < 16; ++i) {
+    const float ev = sg > 0 ? e[i] : e[15 - i];
+    const float t = __fmul_rn(__fadd_rn(__fsub_rn(ev, S.hf), -S.hl), q[i]);
+    const int kb = (1 << 22) + i;
+    asm("{\n\t.reg .pred pa, pg;\n\t.reg .f32 at;\n\t"
+        "setp.gt.f32 pa, %5, %0;\n\t"
+        "setp.ge.f32 pg, %5, %1;\n\t"
+        "abs.f32 at, %5;\n\t"
+        "@pa fma.rn.f32 %0, at, %8, %5;\n\t"
+        "@pa fma.rn.f32 %1, at, %9, %5;\n\t"
+        "@pa add.s32 %2, %2, %6;\n\t"
+        "@pa mov.b32 %3, %7;\n\t"
+        "@pg add.rn.f32 %4, %4, 0f3F800000;\n\t}"
+        : "+f"(hi), "+f"(lo), "+r"(A), "+r"(rr), "+f"(G)
+        : "f"(t), "r"(kb), "r"(i), "f"(kBand), "f"(-kBand));
+  }
+  const int n = A >> 22;
+  if (__float2int_rn(G) != n) return false;
+  if (n != 0) {
+    S.hi = hi;
+    S.lo = lo;
+    S.cv += 2 * (n * d0 + (A & ((1 << 22) - 1))) + n;
+    S.r = d0 + rr;
+    S.Mvalid = false;
+  }
+  return true;
+}
+
 // One POV: row (row coordinates), observer at x, direction sg (+1 forward,
 // -1 backward), D targets, ivt[d] = fl(1/d), wm[w] = max(row[16w .. 16w+15])
 // (or nullptr). Returns cv = sum (2dd+1) over the visible targets; writes
@@ -253,16 +318,35 @@ __device__ int exact_pov(const float* row, const float* wm, const float* ivt, in
   const int pfirst = x + sg, plast = x + sg * D;
   const int w0 = pfirst >> 4, w1 = plast >> 4;
   const int nblk = (w1 - w0) * sg + 1;
-  constexpr int kWm = 8;
+#ifndef SKS_FIX_WM
+#define SKS_FIX_WM 8
+#endif
+  constexpr int kWm = SKS_FIX_WM;
   for (int b0 = 0; b0 < nblk; b0 += kWm) {
+    float wv[kWm];
+#pragma unroll
+    for (int u = 0; u < kWm; ++u) wv[u] = b0 + u < nblk ? __ldg(wm + w0 + sg * (b0 + u)) : -INFINITY;
+#if SKS_FIX_COARSE
+    {
+      // the kWm windows at once: the same bound over their whole dd span
+      // with the maximum of their maxima (monotone rounding, both signs of N)
+      float m = wv[0];
+#pragma unroll
+      for (int u = 1; u < kWm; ++u) m = fmaxf(m, wv[u]);
+      const int wf = w0 + sg * b0, wl = w0 + sg * min(b0 + kWm - 1, nblk - 1);
+      const int da = max(1, sg > 0 ? 16 * wf - x : x - (16 * wf + 15));
+      const int db = min(D, sg > 0 ? 16 * wl + 15 - x : x - 16 * wl);
+      const float N = __fadd_rn(__fsub_rn(m, S.hf), -S.hl);
+      if (__fmul_rn(N, ivt[da]) < S.lo && __fmul_rn(N, ivt[db]) < S.lo) continue;
+    }
+#endif
     unsigned cand = 0;
 #pragma unroll
     for (int u = 0; u < kWm; ++u) {
       const int w = w0 + sg * (b0 + u);
-      const float wv = b0 + u < nblk ? __ldg(wm + w) : -INFINITY;
       const int da = max(1, sg > 0 ? 16 * w - x : x - (16 * w + 15));
       const int db = min(D, sg > 0 ? 16 * w + 15 - x : x - 16 * w);
-      const float N = __fadd_rn(__fsub_rn(wv, S.hf), -S.hl);
+      const float N = __fadd_rn(__fsub_rn(wv[u], S.hf), -S.hl);
       if (b0 + u < nblk && !(__fmul_rn(N, ivt[da]) < S.lo && __fmul_rn(N, ivt[db]) < S.lo)) cand |= 1u << u;
     }
     while (cand != 0) {
@@ -276,7 +360,12 @@ __device__ int exact_pov(const float* row, const float* wm, const float* ivt, in
 #ifdef SKS_EXP_BANDHIST
         if (S.first_band < 0) ++S.blk_before; else ++S.blk_after;
 #endif
+#if SKS_FIX_FULL16
+        const int d0 = sg > 0 ? 16 * w - x : x - (16 * w + 15);
+        if (!eval16(S, row, ivt, w, sg, d0, da, db)) eval_block(S, row, ivt, x, sg, da, db);
+#else
         eval_block(S, row, ivt, x, sg, da, db);
+#endif
       }
     }
   }
