@@ -322,20 +322,22 @@ __device__ int exact_pov(const float* row, const float* wm, const float* ivt, in
 #define SKS_FIX_WM 8
 #endif
   constexpr int kWm = SKS_FIX_WM;
+  // block b (scan order) is w = w0 + sg*b and its first target has
+  // dd = c0 + 16b (partial at the ends: da = max(1, .), db = min(D, .))
+  const int c0 = sg > 0 ? 16 * w0 - x : x - 16 * w0 - 15;
   for (int b0 = 0; b0 < nblk; b0 += kWm) {
+    const int df = c0 + 16 * b0;
     float wv[kWm];
 #pragma unroll
     for (int u = 0; u < kWm; ++u) wv[u] = b0 + u < nblk ? __ldg(wm + w0 + sg * (b0 + u)) : -INFINITY;
 #if SKS_FIX_COARSE
     {
-      // the kWm windows at once: the same bound over their whole dd span
+      // the kWm blocks at once: the same bound over their whole dd span
       // with the maximum of their maxima (monotone rounding, both signs of N)
       float m = wv[0];
 #pragma unroll
       for (int u = 1; u < kWm; ++u) m = fmaxf(m, wv[u]);
-      const int wf = w0 + sg * b0, wl = w0 + sg * min(b0 + kWm - 1, nblk - 1);
-      const int da = max(1, sg > 0 ? 16 * wf - x : x - (16 * wf + 15));
-      const int db = min(D, sg > 0 ? 16 * wl + 15 - x : x - 16 * wl);
+      const int da = max(1, df), db = min(D, df + 16 * kWm - 1);
       const float N = __fadd_rn(__fsub_rn(m, S.hf), -S.hl);
       if (__fmul_rn(N, ivt[da]) < S.lo && __fmul_rn(N, ivt[db]) < S.lo) continue;
     }
@@ -343,25 +345,23 @@ __device__ int exact_pov(const float* row, const float* wm, const float* ivt, in
     unsigned cand = 0;
 #pragma unroll
     for (int u = 0; u < kWm; ++u) {
-      const int w = w0 + sg * (b0 + u);
-      const int da = max(1, sg > 0 ? 16 * w - x : x - (16 * w + 15));
-      const int db = min(D, sg > 0 ? 16 * w + 15 - x : x - 16 * w);
+      const int d0 = df + 16 * u;
+      const int da = max(1, d0), db = min(D, d0 + 15);
       const float N = __fadd_rn(__fsub_rn(wv[u], S.hf), -S.hl);
-      if (b0 + u < nblk && !(__fmul_rn(N, ivt[da]) < S.lo && __fmul_rn(N, ivt[db]) < S.lo)) cand |= 1u << u;
+      if (d0 <= D && !(__fmul_rn(N, ivt[da]) < S.lo && __fmul_rn(N, ivt[db]) < S.lo)) cand |= 1u << u;
     }
     while (cand != 0) {
       const int u = __ffs(cand) - 1;
       cand &= cand - 1;
       const int w = w0 + sg * (b0 + u);
-      const int da = max(1, sg > 0 ? 16 * w - x : x - (16 * w + 15));
-      const int db = min(D, sg > 0 ? 16 * w + 15 - x : x - 16 * w);
+      const int d0 = df + 16 * u;
+      const int da = max(1, d0), db = min(D, d0 + 15);
       const float N = __fadd_rn(__fsub_rn(__ldg(wm + w), S.hf), -S.hl);  // L1 hit
       if (!(__fmul_rn(N, ivt[da]) < S.lo && __fmul_rn(N, ivt[db]) < S.lo)) {
 #ifdef SKS_EXP_BANDHIST
         if (S.first_band < 0) ++S.blk_before; else ++S.blk_after;
 #endif
 #if SKS_FIX_FULL16
-        const int d0 = sg > 0 ? 16 * w - x : x - (16 * w + 15);
         if (!eval16(S, row, ivt, w, sg, d0, da, db)) eval_block(S, row, ivt, x, sg, da, db);
 #else
         eval_block(S, row, ivt, x, sg, da, db);
