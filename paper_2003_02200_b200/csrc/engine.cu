@@ -129,6 +129,11 @@ struct Batch {
   // (indices relative to n_long)
   std::vector<int4> pairs, quads;
   DevBuf d_sectors, d_dest, d_fracf, d_fracd, d_ranges, d_items, d_fix_off, d_pairs, d_quads;
+  // unskew TMA tensor maps (one per sector over its cv rows), encoded for the
+  // cv pool at umap_cv; re-encoded when the pool moves
+  mutable DevBuf d_umaps;
+  mutable const int* umap_cv = nullptr;
+  mutable bool umap_ok = false;
 };
 
 struct Plans {
@@ -409,7 +414,34 @@ struct sks_context {
     for (const SectorDev& sd : b.sdev) {
       if (sd.q_lo > 0 || sd.q_hi < sd.skw_rows) d.row_blocks = 1;
     }
+    d.umaps = unskew_maps(b, d);
     return d;
+  }
+
+  // Tensor maps of the TMA-staged unskew (unskew_tma_kernel), or nullptr for
+  // the register-staged kernel: row-block runs, the fused loader, DEM sides
+  // that are not a multiple of 4 (a box's first column must be 16-byte
+  // aligned: tile column starts are then multiples of 4 in every pre-op
+  // orientation), SKS_UNSKEW_TMA=0.
+  const void* unskew_maps(const Batch& b, const BatchDev& d) {
+    const char* env = std::getenv("SKS_UNSKEW_TMA");
+    if ((env != nullptr && env[0] == '0') || d.row_blocks || b.fused || b.sdev.empty() || d.cv == nullptr) return nullptr;
+    if (b.umap_cv == d.cv) return b.umap_ok ? b.d_umaps.p : nullptr;
+    b.umap_cv = d.cv;
+    b.umap_ok = false;
+    std::vector<unsigned char> h(128 * b.sdev.size());
+    for (size_t s = 0; s < b.sdev.size(); ++s) {
+      const SectorDev& sd = b.sdev[s];
+      if (sd.src_rows % 4 != 0 || sd.src_cols % 4 != 0 || sd.sdem_off % 4 != 0) return nullptr;
+      if (!unskew_make_map(h.data() + 128 * s, d.cv + sd.sdem_off, sd.pitch, sd.skw_rows,
+                           unskew_box_rows(sd.shear_tan))) {
+        return nullptr;
+      }
+    }
+    b.d_umaps.ensure(h.size(), device);
+    cuda_check(cudaMemcpy(b.d_umaps.p, h.data(), h.size(), cudaMemcpyHostToDevice), "upload tensor maps");
+    b.umap_ok = true;
+    return b.d_umaps.p;
   }
 
   void ensure_pools(const Batch& b, bool split_bwd) {

@@ -55,7 +55,21 @@ struct BatchDev {
   // rows come from sdem written by relocate_kernel, which zeroes cv.
   const float* dem;
   int row_blocks;  // some sector owns only a block of its rows (multi-GPU run_rows)
+  // Unskew TMA staging (unskew_tma_kernel): one 2-D tensor map per sector
+  // over its cv rows (dims {pitch, skw_rows}, box {32, unskew_box_rows(tan)}),
+  // CUtensorMap objects (128 B each) in global memory; nullptr: the register-
+  // staged unskew_pipe_kernel (row blocks, the fused loader, DEM sides not a
+  // multiple of 4 — the box's column start must be 16-byte aligned).
+  const void* umaps;
 };
+
+// Rows of the unskew TMA box of a sector: a 32x32 DEM tile reads skewed rows
+// [p_min, p_min + 33 + d_hi - d_lo), d_hi - d_lo <= floor(31 tan) + 1; one
+// more for the rounding of fl(j tan). Host and device evaluate the same IEEE
+// product.
+__host__ __device__ inline int unskew_box_rows(double shear_tan) {
+  return 35 + static_cast<int>(31.0 * shear_tan);
+}
 
 struct ScanArgs {
   BatchDev b;
@@ -132,6 +146,10 @@ int prepare_scan3(int lmax, int rows, int any_capped);
 int launch_unskew(const BatchDev& b, const float* unused, double* map,
                   int dimy, int dimx, void* stream, int tile_row0 = 0, int tile_rows = -1);
 int unskew_tile_rows();
+// Encode the unskew tensor map of one sector into tm (128 bytes, host
+// memory): cv rows [0, rows) of `pitch` int32 starting at base. false: the
+// driver rejected it (the caller keeps the register-staged kernel).
+bool unskew_make_map(void* tm, const int* base, int pitch, int rows, int box_rows);
 int launch_unskew_from_vs(const BatchDev& b, const double* skw_vs,
                           double* map, int dimy, int dimx, void* stream);
 int launch_scale(double* map, long long n, double factor, void* stream);

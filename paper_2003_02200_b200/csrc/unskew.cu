@@ -15,7 +15,12 @@
 
 #include <cstdlib>
 
+#include <cuda.h>
+
+#include <mutex>
+
 #include "sks_device.cuh"
+#include "sks_ptx.cuh"
 
 namespace sks {
 
@@ -366,6 +371,232 @@ __global__ void __launch_bounds__(32 * kNW, SKS_UNSKEW_MINB) unskew_pipe_kernel(
   }
 }
 
+// TMA-staged unskew (same per-cell arithmetic and ascending-k order as the
+// kernels above, bit-identical maps). The copy engine brings each sector's cv
+// parallelogram in as ONE 2-D box — 32 skewed-row columns [j_lo, j_lo + 32)
+// x unskew_box_rows(tan) rows from p_min = base + i_lo - 1 - d(j_hi) — into a
+// ring of kStages shared-memory stages (full/empty mbarriers), so the four
+// consumer warps issue no staging loads, stores or CTA barriers. A fifth
+// (producer) warp publishes each stage as soon as the consumers release it:
+// the sector descriptor (prefetched a sector ahead, one word per lane), the
+// tile's column table (r, 1 - r, box offsets, recomputed with the
+// reference's double ops) and constants, then the TMA. Measured at config 2
+// (0.80 ms register-staged): producer in warp 0 0.50 ms, rotating over the
+// consumer warps 0.49, dedicated warp 0.45 (4 stages, 5 CTAs per SM).
+// Box rows are 128 bytes, so the bank of a read is its box column: a warp's
+// 32 lanes must read 32 different pre-op columns j. Plain sectors map DEM
+// columns to j and transposed ones DEM rows, so each thread owns a diagonal
+// of the tile — lane l, warp w: DEM column l, rows (l + 8w + u) mod 32,
+// u < 8 — whose 32 lanes hold distinct DEM rows AND columns at every u:
+// conflict-free in both orientations (the register-staged kernel stages by
+// source row to get the same, at a load + store + barrier per value).
+#ifndef SKS_UNSKEW_STAGES
+#define SKS_UNSKEW_STAGES 4  // config 2: 2 stages 0.518 ms, 3 0.499, 4 0.453 (with the producer warp), 5 0.523
+#endif
+#ifndef SKS_UNSKEW_DPF
+#define SKS_UNSKEW_DPF 1  // sector descriptors prefetched one issue ahead (a word per lane of warp 0)
+#endif
+#ifndef SKS_UNSKEW_ROLE
+#define SKS_UNSKEW_ROLE 2  // who publishes stages: 0 warp 0 (0.499 ms), 1 warp t % 4 (0.487), 2 a fifth (producer) warp (0.453)
+#endif
+constexpr int kStages = SKS_UNSKEW_STAGES;
+constexpr int kRole = SKS_UNSKEW_ROLE;
+constexpr int kUThreads = kRole == 2 ? 160 : 128;
+#ifndef SKS_UNSKEW_TMA_MINB
+#define SKS_UNSKEW_TMA_MINB (kRole == 2 ? 5 : 7)  // 5 CTAs/SM: 4 stages of 9.4 KB each
+#endif
+constexpr int kUMinBlocks = SKS_UNSKEW_TMA_MINB;
+constexpr int kBoxRowsMax = 66;  // unskew_box_rows(1.0)
+static_assert(sizeof(SectorDev) == 128, "a sector descriptor is one word per lane");
+
+struct __align__(128) UStage {
+  int cv[kBoxRowsMax * kUT];  // box rows p_min .., 32 columns each
+  double2 ro[kUT];            // (r, 1 - r) of box column jl (shear_params, skew.cpp:97-101)
+  int offb[kUT];              // byte offset of (box row d_hi - d_j, column jl): row p of pre-op row i
+                              // (il = i - i_lo + 1) at (il << 7) + offb[jl]
+  int iv[6];
+  int i_lo, j_lo, rows, fast;
+  double corr;
+  SectorDev sd;  // the descriptor, staged by warp 0 from its prefetched words
+};
+
+__global__ void __launch_bounds__(kUThreads, kUMinBlocks) unskew_tma_kernel(BatchDev b, double* __restrict__ map, int dimy, int dimx,
+                                                         int tile_row0) {
+  __shared__ UStage st[kStages];
+  __shared__ uint64_t full[kStages], empty[kStages];
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  const int y0 = (tile_row0 + blockIdx.y) * kUT, x0 = blockIdx.x * kUT;
+  const int ye = min(dimy, y0 + kUT) - 1, xe = min(dimx, x0 + kUT) - 1;
+  const bool full_tile = ye == y0 + kUT - 1 && xe == x0 + kUT - 1;
+  const int nsec = b.n_sectors;
+  if (threadIdx.x == 0) {
+    for (int k = 0; k < kStages; ++k) {
+      mbar_init(&full[k], 1);
+      mbar_init(&empty[k], 4);
+    }
+  }
+  __syncthreads();
+#if SKS_UNSKEW_DPF
+  // the first sector this warp publishes
+  const int t_first = kRole == 1 ? w : 0;
+  int dw = ((kRole == 0 ? w == 0 : kRole == 2 ? w == 4 : true) && t_first < nsec)
+               ? __ldg(reinterpret_cast<const int*>(b.sectors + t_first) + lane)
+               : 0;
+#endif
+  // warp 0: publish sector t in stage t % kStages
+  auto issue = [&](int t) {
+    const int slot = t % kStages;
+    if (t >= kStages) mbar_wait(&empty[slot], ((t / kStages) - 1) & 1);
+    UStage& S = st[slot];
+#if SKS_UNSKEW_DPF
+    // sector t's descriptor words arrived while sector t - 1 was published
+    reinterpret_cast<int*>(&S.sd)[lane] = dw;
+    __syncwarp();
+    {
+      const int tn = t + (kRole == 1 ? 4 : 1);  // the next sector this warp publishes
+      if (tn < nsec) dw = __ldg(reinterpret_cast<const int*>(b.sectors + tn) + lane);
+    }
+    const SectorDev& sd = S.sd;
+#define SKS_UDESC(x) (x)
+#else
+    const SectorDev& sd = b.sectors[t];
+#define SKS_UDESC(x) __ldg(&(x))
+#endif
+    int iv[6];
+#pragma unroll
+    for (int k = 0; k < 6; ++k) iv[k] = SKS_UDESC(sd.inv[k]);
+    const int ia = iv[0] * y0 + iv[1] * x0 + iv[2], ib = iv[0] * ye + iv[1] * xe + iv[2];
+    const int ja = iv[3] * y0 + iv[4] * x0 + iv[5], jb = iv[3] * ye + iv[4] * xe + iv[5];
+    const int i_lo = min(ia, ib), j_lo = min(ja, jb), i_hi = max(ia, ib), j_hi = max(ja, jb);
+    const double tan = SKS_UDESC(sd.shear_tan);
+    const int rows = SKS_UDESC(sd.rows);
+    const int d_hi = __double2int_rz(__dmul_rn(tan, static_cast<double>(j_hi)));
+    {
+      const int j = j_lo + lane;  // box column lane (columns past j_hi are never read)
+      const double y = __dmul_rn(tan, static_cast<double>(j));
+      const int d = __double2int_rz(y);
+      const double r = __dsub_rn(y, static_cast<double>(d));
+      S.ro[lane] = make_double2(r, __dsub_rn(1.0, r));
+      S.offb[lane] = ((d_hi - d) << 7) + (lane << 2);
+    }
+    if (lane == 0) {
+#pragma unroll
+      for (int k = 0; k < 6; ++k) S.iv[k] = iv[k];
+      S.i_lo = i_lo;
+      S.j_lo = j_lo;
+      S.rows = rows;
+      S.fast = full_tile && i_lo >= 1 && i_hi <= rows - 2;
+      S.corr = SKS_UDESC(sd.correction);
+    }
+    __syncwarp();
+    if (lane == 0) {
+      const int p_min = SKS_UDESC(sd.base) + i_lo - 1 - d_hi;
+      const int box = unskew_box_rows(tan);
+      mbar_expect_tx(&full[slot], static_cast<unsigned>(box * kUT * 4));
+      tma_tile_2d(S.cv, static_cast<const char*>(b.umaps) + 128 * static_cast<size_t>(t), j_lo, p_min, &full[slot]);
+    }
+#undef SKS_UDESC
+  };
+  if (kRole == 2 && w == 4) {
+    for (int t = 0; t < nsec; ++t) issue(t);
+    return;
+  }
+  const int sj = x0 + lane;
+  const int rb = lane + 8 * w;  // this thread's rows: (rb + u) & 31
+  double acc[8];
+#pragma unroll
+  for (int u = 0; u < 8; ++u) {
+    const int si = y0 + ((rb + u) & 31);
+    acc[u] = (si < dimy && sj < dimx) ? map[static_cast<long long>(si) * dimx + sj] : 0.0;
+  }
+  for (int s = 0; s < nsec; ++s) {
+    if (kRole != 2 && (kRole == 1 || w == 0)) {
+      // first turn: sectors 0 .. kStages - 1; then one per turn (one call site)
+      const int t_end = min(s + kStages, nsec);
+      for (int t = s == 0 ? 0 : s + kStages - 1; t < t_end; ++t) {
+        if (kRole == 0 || (t & 3) == w) issue(t);
+      }
+    }
+    const int slot = s % kStages;
+    mbar_wait(&full[slot], (s / kStages) & 1);
+    const UStage& S = st[slot];
+    const char* cvb = reinterpret_cast<const char*>(S.cv);
+    const int iv0 = S.iv[0], iv1 = S.iv[1], iv2 = S.iv[2], iv3 = S.iv[3], iv4 = S.iv[4], iv5 = S.iv[5];
+    const int i_lo = S.i_lo, j_lo = S.j_lo;
+    const double corr = S.corr;
+    if (S.fast) {
+      // Interior tile: both covered() weights are fl(fl(1-r)+r), within
+      // 2^-52 of 1, so both flags hold (skew.cpp:233-240) and every cell
+      // interpolates v = fl(fl(omr*fl(cv_p*corr)) + fl(r*fl(cv_{p-1}*corr))).
+      if (iv0 != 0) {
+        // plain: the thread's column j is fixed, row i = iv0 * si + iv2
+        const int jl = iv4 * sj + iv5 - j_lo;
+        const double2 ro = S.ro[jl];
+        const char* a0 = cvb + (S.offb[jl] + (iv0 * y0 + iv2 - i_lo + 1) * 128);
+#pragma unroll
+        for (int u = 0; u < 8; ++u) {
+          const char* a = a0 + (iv0 * ((rb + u) & 31) * 128);
+          const double va = __dmul_rn(static_cast<double>(*reinterpret_cast<const int*>(a)), corr);
+          const double vb = __dmul_rn(static_cast<double>(*reinterpret_cast<const int*>(a - 128)), corr);
+          acc[u] = __dadd_rn(acc[u], __dadd_rn(__dmul_rn(ro.y, va), __dmul_rn(ro.x, vb)));
+        }
+      } else {
+        // transposed: the thread's row i is fixed, column j = iv3 * si + iv5
+        const char* a0 = cvb + ((iv1 * sj + iv2 - i_lo + 1) * 128);
+        const int jb = iv3 * y0 + iv5 - j_lo;
+#pragma unroll
+        for (int u = 0; u < 8; ++u) {
+          const int jl = jb + iv3 * ((rb + u) & 31);
+          const double2 ro = S.ro[jl];
+          const char* a = a0 + (S.offb[jl]);
+          const double va = __dmul_rn(static_cast<double>(*reinterpret_cast<const int*>(a)), corr);
+          const double vb = __dmul_rn(static_cast<double>(*reinterpret_cast<const int*>(a - 128)), corr);
+          acc[u] = __dadd_rn(acc[u], __dadd_rn(__dmul_rn(ro.y, va), __dmul_rn(ro.x, vb)));
+        }
+      }
+    } else {
+      const int rows = S.rows;
+#pragma unroll
+      for (int u = 0; u < 8; ++u) {
+        const int si = y0 + ((rb + u) & 31);
+        if (si >= dimy || sj >= dimx) continue;
+        const int i = iv0 * si + iv1 * sj + iv2;
+        const int jl = iv3 * si + iv4 * sj + iv5 - j_lo;
+        const double2 ro = S.ro[jl];
+        const double r = ro.x, omr = ro.y;
+        const char* a = cvb + ((i - i_lo + 1) * 128 + S.offb[jl]);
+        const double w_p = (i + 1 < rows) ? __dadd_rn(omr, r) : omr;
+        const double w_m = (i >= 1) ? __dadd_rn(omr, r) : r;
+        const bool fa = full_d(w_p);
+        const bool fc = full_d(w_m);
+        double va = 0.0, vb = 0.0;
+        if (fa) va = __dmul_rn(static_cast<double>(*reinterpret_cast<const int*>(a)), corr);
+        if (!fa || fc) vb = __dmul_rn(static_cast<double>(*reinterpret_cast<const int*>(a - 128)), corr);
+        double v;
+        if (fa && fc) {
+          v = __dadd_rn(__dmul_rn(omr, va), __dmul_rn(r, vb));
+        } else if (fa) {
+          v = va;
+        } else {
+          v = vb;
+        }
+        acc[u] = __dadd_rn(acc[u], v);
+      }
+    }
+    __syncwarp();
+    if (lane == 0) mbar_arrive(&empty[slot]);
+  }
+  // recompute the store addresses (an opaque copy of rb): holding the eight
+  // load addresses across the sector loop costs 16 registers
+  int rb2 = rb;
+  asm volatile("" : "+r"(rb2));
+#pragma unroll
+  for (int u = 0; u < 8; ++u) {
+    const int si = y0 + ((rb2 + u) & 31);
+    if (si < dimy && sj < dimx) map[static_cast<long long>(si) * dimx + sj] = acc[u];
+  }
+}
+
 // Input scan of the DEM on device (total_host): res[0] = first non-finite
 // cell index (row-major, as validate(Dem) reports it, dem.cpp:36-60), res[1]
 // != 0 if a nonzero |e| lies outside the FP32 filter's proven range
@@ -406,7 +637,9 @@ int launch_unskew(const BatchDev& b, const float*, double* map, int dimy, int di
   if (tile_rows < 0) tile_rows = all_rows - tile_row0;
   if (tile_rows <= 0) return 0;
   dim3 grid((dimx + kUT - 1) / kUT, tile_rows);
-  if (b.row_blocks) {
+  if (b.umaps != nullptr && !b.row_blocks && b.dem == nullptr) {
+    unskew_tma_kernel<<<grid, kUThreads, 0, static_cast<cudaStream_t>(stream)>>>(b, map, dimy, dimx, tile_row0);
+  } else if (b.row_blocks) {
     unskew_pipe_kernel<true><<<grid, 32 * kNW, 0, static_cast<cudaStream_t>(stream)>>>(b, map, dimy, dimx, tile_row0);
   } else {
     unskew_pipe_kernel<false><<<grid, 32 * kNW, 0, static_cast<cudaStream_t>(stream)>>>(b, map, dimy, dimx, tile_row0);
@@ -415,6 +648,41 @@ int launch_unskew(const BatchDev& b, const float*, double* map, int dimy, int di
 }
 
 int unskew_tile_rows() { return kUT; }
+
+namespace {
+using EncodeTiledU = CUresult (*)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
+                                  const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
+                                  CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+EncodeTiledU encode_fn_u() {
+  static EncodeTiledU fn = nullptr;
+  static std::once_flag once;
+  std::call_once(once, [] {
+    void* p = nullptr;
+    cudaDriverEntryPointQueryResult q{};
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) == cudaSuccess &&
+        q == cudaDriverEntryPointSuccess) {
+      fn = reinterpret_cast<EncodeTiledU>(p);
+    }
+  });
+  return fn;
+}
+}  // namespace
+
+bool unskew_make_map(void* tm, const int* base, int pitch, int rows, int box_rows) {
+  static_assert(sizeof(CUtensorMap) == 128, "tensor maps are 128 bytes");
+  EncodeTiledU fn = encode_fn_u();
+  if (fn == nullptr || rows < 1 || box_rows > kBoxRowsMax || pitch % 32 != 0 ||
+      (reinterpret_cast<uintptr_t>(base) & 15u) != 0) {
+    return false;
+  }
+  const cuuint64_t dims[2] = {static_cast<cuuint64_t>(pitch), static_cast<cuuint64_t>(rows)};
+  const cuuint64_t strides[1] = {static_cast<cuuint64_t>(pitch) * sizeof(int)};
+  const cuuint32_t box[2] = {static_cast<cuuint32_t>(kUT), static_cast<cuuint32_t>(box_rows)};
+  const cuuint32_t estr[2] = {1, 1};
+  return fn(static_cast<CUtensorMap*>(tm), CU_TENSOR_MAP_DATA_TYPE_INT32, 2, const_cast<int*>(base), dims, strides,
+            box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_128B,
+            CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
 
 int launch_unskew_from_vs(const BatchDev& b, const double* skw_vs, double* map, int dimy,
                           int dimx, void* stream) {

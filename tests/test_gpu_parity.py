@@ -340,6 +340,29 @@ def test_total_viewshed_raw_bitexact(ora, shape, kind, ns, maxd):
     assert np.array_equal(b64(ours), b64(ref))
 
 
+@pytest.mark.parametrize("shape,kind,ns,maxd", [
+    ((64, 48), sk.SyntheticKind.Fractal, 90, None),
+    ((100, 60), sk.SyntheticKind.SmoothedNoise, 36, 300.0),
+    ((36, 132), sk.SyntheticKind.Cone, 180, None),
+    ((68, 36), sk.SyntheticKind.Fractal, 360, None),  # partial tiles on both axes
+])
+def test_unskew_tma_and_register_staged_bitexact(ora, shape, kind, ns, maxd, monkeypatch):
+    """The TMA-staged unskew (DEM sides multiples of 4: one 2-D box per
+    sector and tile, diagonal cell ownership) and the register-staged kernel
+    (SKS_UNSKEW_TMA=0, also what odd sides take) both give the reference's
+    map bit for bit."""
+    dem = sk.make_synthetic(kind, *shape, 10.0, 21)
+    cfg = sk.RunConfig(ns=ns, h0=1.5, max_distance=maxd, units=sk.Units.SquareMeters)
+    ref = ora.total_viewshed(dem.values, 10.0, ns, 1.5, max_distance=maxd or 0.0, raw=True)
+    ours = sk.total_viewshed_raw(dem, cfg)
+    assert np.array_equal(b64(ours), b64(ref))
+    monkeypatch.setenv("SKS_UNSKEW_TMA", "0")
+    ctx = sk.Context(0)
+    staged = ctx.total_viewshed(dem.values, 10.0, cfg, raw=True)
+    ctx.close()
+    assert np.array_equal(b64(staged), b64(ref))
+
+
 @pytest.mark.parametrize("scale", [3.0e12, 2.0e-13])
 def test_exact_path_outside_filter_range(ora, scale):
     """Elevations outside the FP32 filter's proven range [2^-40, 2^40]
