@@ -60,15 +60,58 @@ def load_peaks():
 
 
 class ClockSampler:
-    """nvidia-smi clocks + throttle reasons sampled during the timed region."""
+    """SM clocks + throttle reasons sampled during the timed region: NVML
+    every 20 ms from a thread (nvidia_ml_py; one sample is also taken when
+    the thread starts, so even a ~1 s region has samples), else nvidia-smi
+    -lms 100 (whose own start-up can outlast a short region)."""
+
+    # NVML clocks-event reason bits (nvml.h)
+    _BITS = {"hw_slowdown": 0x8, "hw_thermal_slowdown": 0x40, "sw_thermal_slowdown": 0x20, "sw_power_cap": 0x4}
 
     def __init__(self, index: int):
         self.index = index
         self.samples = []
         self._stop = threading.Event()
         self._proc = None
+        self._nvml = None
+        try:
+            import pynvml
+
+            pynvml.nvmlInit()
+            self._h = pynvml.nvmlDeviceGetHandleByIndex(index)
+            self._max = pynvml.nvmlDeviceGetMaxClockInfo(self._h, pynvml.NVML_CLOCK_SM)
+            self._nvml = pynvml
+        except Exception:
+            self._nvml = None
+
+    def _nvml_sample(self):
+        nv = self._nvml
+        sm = nv.nvmlDeviceGetClockInfo(self._h, nv.NVML_CLOCK_SM)
+        try:
+            bits = nv.nvmlDeviceGetCurrentClocksEventReasons(self._h)
+        except AttributeError:
+            bits = nv.nvmlDeviceGetCurrentClocksThrottleReasons(self._h)
+        try:
+            pw = nv.nvmlDeviceGetPowerUsage(self._h) / 1000.0
+        except Exception:
+            pw = float("nan")
+        flags = ["Active" if bits & b else "Not Active" for b in self._BITS.values()]
+        self.samples.append([str(sm), str(self._max), str(pw), hex(bits), *flags])
+
+    def _nvml_loop(self):
+        while True:
+            try:
+                self._nvml_sample()
+            except Exception:
+                return
+            if self._stop.wait(0.02):
+                return
 
     def start(self):
+        if self._nvml is not None:
+            self._t = threading.Thread(target=self._nvml_loop, daemon=True)
+            self._t.start()
+            return
         q = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
              "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
@@ -89,6 +132,9 @@ class ClockSampler:
                 self.samples.append(parts)
 
     def stop(self):
+        self._stop.set()
+        if self._nvml is not None:
+            self._t.join(timeout=2)
         if self._proc is not None:
             self._proc.terminate()
             try:
@@ -496,7 +542,9 @@ def run_ours(args, world, rank, local):
                                 "peak_kind": peak_kind, "traffic": reloc_traffic,
                                 "note": ("algorithmic 8N bytes per sector (read N, write N covered cells); the "
                                          "kernel also zeroes the N cv cells it covers (4N more written)")},
-        "roofline_unskew": {"kernel": "unskew_pipe_kernel", "bound": "hbm",
+        # the TMA-staged kernel when both DEM sides are multiples of 4 (engine.cu unskew_maps)
+        "roofline_unskew": {"kernel": ("unskew_tma_kernel" if n % 4 == 0 and os.environ.get("SKS_UNSKEW_TMA", "1")[:1] != "0"
+                                       else "unskew_pipe_kernel"), "bound": "hbm",
                             "achieved": unskew_bytes / max(unskew_s, 1e-12) / 1e9,
                             "peak": float(peaks.get("hbm_gbs", 6650.0)), "unit": "GB/s",
                             "frac": unskew_bytes / max(unskew_s, 1e-12) / 1e9

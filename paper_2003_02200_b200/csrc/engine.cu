@@ -419,13 +419,13 @@ struct sks_context {
   }
 
   // Tensor maps of the TMA-staged unskew (unskew_tma_kernel), or nullptr for
-  // the register-staged kernel: row-block runs, the fused loader, DEM sides
+  // the register-staged kernel: the fused loader, DEM sides
   // that are not a multiple of 4 (a box's first column must be 16-byte
   // aligned: tile column starts are then multiples of 4 in every pre-op
   // orientation), SKS_UNSKEW_TMA=0.
   const void* unskew_maps(const Batch& b, const BatchDev& d) {
     const char* env = std::getenv("SKS_UNSKEW_TMA");
-    if ((env != nullptr && env[0] == '0') || d.row_blocks || b.fused || b.sdev.empty() || d.cv == nullptr) return nullptr;
+    if ((env != nullptr && env[0] == '0') || b.fused || b.sdev.empty() || d.cv == nullptr) return nullptr;
     if (b.umap_cv == d.cv) return b.umap_ok ? b.d_umaps.p : nullptr;
     b.umap_cv = d.cv;
     b.umap_ok = false;
@@ -433,8 +433,11 @@ struct sks_context {
     for (size_t s = 0; s < b.sdev.size(); ++s) {
       const SectorDev& sd = b.sdev[s];
       if (sd.src_rows % 4 != 0 || sd.src_cols % 4 != 0 || sd.sdem_off % 4 != 0) return nullptr;
-      if (!unskew_make_map(h.data() + 128 * s, d.cv + sd.sdem_off, sd.pitch, sd.skw_rows,
-                           unskew_box_rows(sd.shear_tan))) {
+      // row blocks: the map covers the owned rows only (the TMA zero-fills
+      // the others); a sector owning none is never published
+      if (sd.q_hi <= sd.q_lo) continue;
+      if (!unskew_make_map(h.data() + 128 * s, d.cv + sd.sdem_off + static_cast<long long>(sd.q_lo) * sd.pitch,
+                           sd.pitch, sd.q_hi - sd.q_lo, unskew_box_rows(sd.shear_tan))) {
         return nullptr;
       }
     }

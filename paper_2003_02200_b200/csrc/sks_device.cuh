@@ -56,10 +56,11 @@ struct BatchDev {
   const float* dem;
   int row_blocks;  // some sector owns only a block of its rows (multi-GPU run_rows)
   // Unskew TMA staging (unskew_tma_kernel): one 2-D tensor map per sector
-  // over its cv rows (dims {pitch, skw_rows}, box {32, unskew_box_rows(tan)}),
-  // CUtensorMap objects (128 B each) in global memory; nullptr: the register-
-  // staged unskew_pipe_kernel (row blocks, the fused loader, DEM sides not a
-  // multiple of 4 — the box's column start must be 16-byte aligned).
+  // over its owned cv rows (dims {pitch, q_hi - q_lo}, box {32,
+  // unskew_box_rows(tan)}), CUtensorMap objects (128 B each) in global
+  // memory; nullptr: the register-staged unskew_pipe_kernel (the fused
+  // loader, DEM sides not a multiple of 4 — a box's column start must be
+  // 16-byte aligned).
   const void* umaps;
 };
 

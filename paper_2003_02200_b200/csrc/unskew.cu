@@ -13,6 +13,7 @@
 // needs, staged by unskew_pipe_kernel) + 16 B of map RMW per cell per batch.
 #include <cuda_runtime.h>
 
+#include <cstddef>
 #include <cstdlib>
 
 #include <cuda.h>
@@ -391,21 +392,13 @@ __global__ void __launch_bounds__(32 * kNW, SKS_UNSKEW_MINB) unskew_pipe_kernel(
 // conflict-free in both orientations (the register-staged kernel stages by
 // source row to get the same, at a load + store + barrier per value).
 #ifndef SKS_UNSKEW_STAGES
-#define SKS_UNSKEW_STAGES 4  // config 2: 2 stages 0.518 ms, 3 0.499, 4 0.453 (with the producer warp), 5 0.523
+#define SKS_UNSKEW_STAGES 4  // config 2: 2 stages 0.518 ms, 3 0.499 (producer in warp 0), 4 0.453 (producer warp), 5 0.523
 #endif
-#ifndef SKS_UNSKEW_DPF
-#define SKS_UNSKEW_DPF 1  // sector descriptors prefetched one issue ahead (a word per lane of warp 0)
-#endif
-#ifndef SKS_UNSKEW_ROLE
-#define SKS_UNSKEW_ROLE 2  // who publishes stages: 0 warp 0 (0.499 ms), 1 warp t % 4 (0.487), 2 a fifth (producer) warp (0.453)
+#ifndef SKS_UNSKEW_TMA_MINB
+#define SKS_UNSKEW_TMA_MINB 5  // CTAs per SM: 4 stages of 9.4 KB each
 #endif
 constexpr int kStages = SKS_UNSKEW_STAGES;
-constexpr int kRole = SKS_UNSKEW_ROLE;
-constexpr int kUThreads = kRole == 2 ? 160 : 128;
-#ifndef SKS_UNSKEW_TMA_MINB
-#define SKS_UNSKEW_TMA_MINB (kRole == 2 ? 5 : 7)  // 5 CTAs/SM: 4 stages of 9.4 KB each
-#endif
-constexpr int kUMinBlocks = SKS_UNSKEW_TMA_MINB;
+constexpr int kUThreads = 160;  // 4 consumer warps + the producer warp
 constexpr int kBoxRowsMax = 66;  // unskew_box_rows(1.0)
 static_assert(sizeof(SectorDev) == 128, "a sector descriptor is one word per lane");
 
@@ -413,15 +406,20 @@ struct __align__(128) UStage {
   int cv[kBoxRowsMax * kUT];  // box rows p_min .., 32 columns each
   double2 ro[kUT];            // (r, 1 - r) of box column jl (shear_params, skew.cpp:97-101)
   int offb[kUT];              // byte offset of (box row d_hi - d_j, column jl): row p of pre-op row i
-                              // (il = i - i_lo + 1) at (il << 7) + offb[jl]
+                              // (il = i - i_lo + 1) at il * 128 + offb[jl]
   int iv[6];
   int i_lo, j_lo, rows, fast;
+  int end;                    // no more sectors: the consumers leave
   double corr;
-  SectorDev sd;  // the descriptor, staged by warp 0 from its prefetched words
 };
 
-__global__ void __launch_bounds__(kUThreads, kUMinBlocks) unskew_tma_kernel(BatchDev b, double* __restrict__ map, int dimy, int dimx,
-                                                         int tile_row0) {
+// Row-block runs (b.row_blocks): a sector's map covers only its owned rows
+// [q_lo, q_hi) (the TMA zero-fills the rest, as the reference reads no cv
+// there), and the producer publishes only the sectors with an owned skewed
+// row in the tile's box (8 ranks: ~1/8 of them), in ascending k, then an
+// end marker.
+__global__ void __launch_bounds__(kUThreads, SKS_UNSKEW_TMA_MINB) unskew_tma_kernel(BatchDev b, double* __restrict__ map,
+                                                                                   int dimy, int dimx, int tile_row0) {
   __shared__ UStage st[kStages];
   __shared__ uint64_t full[kStages], empty[kStages];
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
@@ -436,69 +434,73 @@ __global__ void __launch_bounds__(kUThreads, kUMinBlocks) unskew_tma_kernel(Batc
     }
   }
   __syncthreads();
-#if SKS_UNSKEW_DPF
-  // the first sector this warp publishes
-  const int t_first = kRole == 1 ? w : 0;
-  int dw = ((kRole == 0 ? w == 0 : kRole == 2 ? w == 4 : true) && t_first < nsec)
-               ? __ldg(reinterpret_cast<const int*>(b.sectors + t_first) + lane)
-               : 0;
-#endif
-  // warp 0: publish sector t in stage t % kStages
-  auto issue = [&](int t) {
-    const int slot = t % kStages;
-    if (t >= kStages) mbar_wait(&empty[slot], ((t / kStages) - 1) & 1);
-    UStage& S = st[slot];
-#if SKS_UNSKEW_DPF
-    // sector t's descriptor words arrived while sector t - 1 was published
-    reinterpret_cast<int*>(&S.sd)[lane] = dw;
-    __syncwarp();
-    {
-      const int tn = t + (kRole == 1 ? 4 : 1);  // the next sector this warp publishes
-      if (tn < nsec) dw = __ldg(reinterpret_cast<const int*>(b.sectors + tn) + lane);
-    }
-    const SectorDev& sd = S.sd;
-#define SKS_UDESC(x) (x)
-#else
-    const SectorDev& sd = b.sectors[t];
-#define SKS_UDESC(x) __ldg(&(x))
-#endif
-    int iv[6];
+  if (w == 4) {
+    // producer: stage n (the n-th published sector) in slot n % kStages
+    int n = 0;
+    auto acquire = [&](int slot) -> UStage& {
+      if (n >= kStages) mbar_wait(&empty[slot], ((n / kStages) - 1) & 1);
+      return st[slot];
+    };
+    int dw = nsec > 0 ? __ldg(reinterpret_cast<const int*>(b.sectors) + lane) : 0;
+    for (int t = 0; t < nsec; ++t) {
+      // sector t's descriptor words arrived while sector t - 1 was handled
+      const int cur = dw;
+      if (t + 1 < nsec) dw = __ldg(reinterpret_cast<const int*>(b.sectors + t + 1) + lane);
+      int iv[6];
 #pragma unroll
-    for (int k = 0; k < 6; ++k) iv[k] = SKS_UDESC(sd.inv[k]);
-    const int ia = iv[0] * y0 + iv[1] * x0 + iv[2], ib = iv[0] * ye + iv[1] * xe + iv[2];
-    const int ja = iv[3] * y0 + iv[4] * x0 + iv[5], jb = iv[3] * ye + iv[4] * xe + iv[5];
-    const int i_lo = min(ia, ib), j_lo = min(ja, jb), i_hi = max(ia, ib), j_hi = max(ja, jb);
-    const double tan = SKS_UDESC(sd.shear_tan);
-    const int rows = SKS_UDESC(sd.rows);
-    const int d_hi = __double2int_rz(__dmul_rn(tan, static_cast<double>(j_hi)));
-    {
-      const int j = j_lo + lane;  // box column lane (columns past j_hi are never read)
-      const double y = __dmul_rn(tan, static_cast<double>(j));
-      const int d = __double2int_rz(y);
-      const double r = __dsub_rn(y, static_cast<double>(d));
-      S.ro[lane] = make_double2(r, __dsub_rn(1.0, r));
-      S.offb[lane] = ((d_hi - d) << 7) + (lane << 2);
-    }
-    if (lane == 0) {
+      for (int k = 0; k < 6; ++k) iv[k] = __shfl_sync(0xffffffffu, cur, offsetof(SectorDev, inv) / 4 + k);
+      const int ia = iv[0] * y0 + iv[1] * x0 + iv[2], ib = iv[0] * ye + iv[1] * xe + iv[2];
+      const int ja = iv[3] * y0 + iv[4] * x0 + iv[5], jb = iv[3] * ye + iv[4] * xe + iv[5];
+      const int i_lo = min(ia, ib), j_lo = min(ja, jb), i_hi = max(ia, ib), j_hi = max(ja, jb);
+      auto word = [&](size_t off) { return __shfl_sync(0xffffffffu, cur, static_cast<int>(off / 4)); };
+      const double tan = __hiloint2double(word(offsetof(SectorDev, shear_tan) + 4), word(offsetof(SectorDev, shear_tan)));
+      const int base = word(offsetof(SectorDev, base));
+      const int q_lo = word(offsetof(SectorDev, q_lo)), q_hi = word(offsetof(SectorDev, q_hi));
+      const int rows = word(offsetof(SectorDev, rows));
+      const double corr =
+          __hiloint2double(word(offsetof(SectorDev, correction) + 4), word(offsetof(SectorDev, correction)));
+      const int d_hi = __double2int_rz(__dmul_rn(tan, static_cast<double>(j_hi)));
+      const int p_min = base + i_lo - 1 - d_hi;
+      if (b.row_blocks) {
+        // none of the skewed rows the tile reads may belong to this run
+        const int d_lo = __double2int_rz(__dmul_rn(tan, static_cast<double>(j_lo)));
+        const int p_max = base + i_hi - d_lo;
+        if (max(p_min, q_lo) > min(p_max, q_hi - 1)) continue;
+      }
+      const int slot = n % kStages;
+      UStage& S = acquire(slot);
+      {
+        const int j = j_lo + lane;  // box column lane (columns past j_hi are never read)
+        const double y = __dmul_rn(tan, static_cast<double>(j));
+        const int d = __double2int_rz(y);
+        const double r = __dsub_rn(y, static_cast<double>(d));
+        S.ro[lane] = make_double2(r, __dsub_rn(1.0, r));
+        S.offb[lane] = (d_hi - d) * 128 + lane * 4;
+      }
+      if (lane == 0) {
 #pragma unroll
-      for (int k = 0; k < 6; ++k) S.iv[k] = iv[k];
-      S.i_lo = i_lo;
-      S.j_lo = j_lo;
-      S.rows = rows;
-      S.fast = full_tile && i_lo >= 1 && i_hi <= rows - 2;
-      S.corr = SKS_UDESC(sd.correction);
+        for (int k = 0; k < 6; ++k) S.iv[k] = iv[k];
+        S.i_lo = i_lo;
+        S.j_lo = j_lo;
+        S.rows = rows;
+        S.fast = full_tile && i_lo >= 1 && i_hi <= rows - 2;
+        S.end = 0;
+        S.corr = corr;
+      }
+      __syncwarp();
+      if (lane == 0) {
+        mbar_expect_tx(&full[slot], static_cast<unsigned>(unskew_box_rows(tan) * kUT * 4));
+        tma_tile_2d(S.cv, static_cast<const char*>(b.umaps) + 128 * static_cast<size_t>(t), j_lo, p_min - q_lo,
+                    &full[slot]);
+      }
+      ++n;
     }
-    __syncwarp();
+    const int slot = n % kStages;
+    UStage& S = acquire(slot);
     if (lane == 0) {
-      const int p_min = SKS_UDESC(sd.base) + i_lo - 1 - d_hi;
-      const int box = unskew_box_rows(tan);
-      mbar_expect_tx(&full[slot], static_cast<unsigned>(box * kUT * 4));
-      tma_tile_2d(S.cv, static_cast<const char*>(b.umaps) + 128 * static_cast<size_t>(t), j_lo, p_min, &full[slot]);
+      S.end = 1;
+      mbar_arrive(&full[slot]);
     }
-#undef SKS_UDESC
-  };
-  if (kRole == 2 && w == 4) {
-    for (int t = 0; t < nsec; ++t) issue(t);
     return;
   }
   const int sj = x0 + lane;
@@ -509,17 +511,11 @@ __global__ void __launch_bounds__(kUThreads, kUMinBlocks) unskew_tma_kernel(Batc
     const int si = y0 + ((rb + u) & 31);
     acc[u] = (si < dimy && sj < dimx) ? map[static_cast<long long>(si) * dimx + sj] : 0.0;
   }
-  for (int s = 0; s < nsec; ++s) {
-    if (kRole != 2 && (kRole == 1 || w == 0)) {
-      // first turn: sectors 0 .. kStages - 1; then one per turn (one call site)
-      const int t_end = min(s + kStages, nsec);
-      for (int t = s == 0 ? 0 : s + kStages - 1; t < t_end; ++t) {
-        if (kRole == 0 || (t & 3) == w) issue(t);
-      }
-    }
-    const int slot = s % kStages;
-    mbar_wait(&full[slot], (s / kStages) & 1);
+  for (int n = 0;; ++n) {
+    const int slot = n % kStages;
+    mbar_wait(&full[slot], (n / kStages) & 1);
     const UStage& S = st[slot];
+    if (S.end) break;
     const char* cvb = reinterpret_cast<const char*>(S.cv);
     const int iv0 = S.iv[0], iv1 = S.iv[1], iv2 = S.iv[2], iv3 = S.iv[3], iv4 = S.iv[4], iv5 = S.iv[5];
     const int i_lo = S.i_lo, j_lo = S.j_lo;
@@ -535,20 +531,20 @@ __global__ void __launch_bounds__(kUThreads, kUMinBlocks) unskew_tma_kernel(Batc
         const char* a0 = cvb + (S.offb[jl] + (iv0 * y0 + iv2 - i_lo + 1) * 128);
 #pragma unroll
         for (int u = 0; u < 8; ++u) {
-          const char* a = a0 + (iv0 * ((rb + u) & 31) * 128);
+          const char* a = a0 + iv0 * ((rb + u) & 31) * 128;
           const double va = __dmul_rn(static_cast<double>(*reinterpret_cast<const int*>(a)), corr);
           const double vb = __dmul_rn(static_cast<double>(*reinterpret_cast<const int*>(a - 128)), corr);
           acc[u] = __dadd_rn(acc[u], __dadd_rn(__dmul_rn(ro.y, va), __dmul_rn(ro.x, vb)));
         }
       } else {
         // transposed: the thread's row i is fixed, column j = iv3 * si + iv5
-        const char* a0 = cvb + ((iv1 * sj + iv2 - i_lo + 1) * 128);
+        const char* a0 = cvb + (iv1 * sj + iv2 - i_lo + 1) * 128;
         const int jb = iv3 * y0 + iv5 - j_lo;
 #pragma unroll
         for (int u = 0; u < 8; ++u) {
           const int jl = jb + iv3 * ((rb + u) & 31);
           const double2 ro = S.ro[jl];
-          const char* a = a0 + (S.offb[jl]);
+          const char* a = a0 + S.offb[jl];
           const double va = __dmul_rn(static_cast<double>(*reinterpret_cast<const int*>(a)), corr);
           const double vb = __dmul_rn(static_cast<double>(*reinterpret_cast<const int*>(a - 128)), corr);
           acc[u] = __dadd_rn(acc[u], __dadd_rn(__dmul_rn(ro.y, va), __dmul_rn(ro.x, vb)));
@@ -637,7 +633,7 @@ int launch_unskew(const BatchDev& b, const float*, double* map, int dimy, int di
   if (tile_rows < 0) tile_rows = all_rows - tile_row0;
   if (tile_rows <= 0) return 0;
   dim3 grid((dimx + kUT - 1) / kUT, tile_rows);
-  if (b.umaps != nullptr && !b.row_blocks && b.dem == nullptr) {
+  if (b.umaps != nullptr && b.dem == nullptr) {
     unskew_tma_kernel<<<grid, kUThreads, 0, static_cast<cudaStream_t>(stream)>>>(b, map, dimy, dimx, tile_row0);
   } else if (b.row_blocks) {
     unskew_pipe_kernel<true><<<grid, 32 * kNW, 0, static_cast<cudaStream_t>(stream)>>>(b, map, dimy, dimx, tile_row0);

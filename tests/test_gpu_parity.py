@@ -400,14 +400,15 @@ def test_device_entry_rejects_non_finite():
                         stream=torch.cuda.current_stream().cuda_stream)
 
 
+@pytest.mark.parametrize("shape", [(72, 60), (70, 61)])  # TMA-staged unskew / register-staged (odd side)
 @pytest.mark.parametrize("nparts", [1, 2, 3, 8])
-def test_row_block_parts_sum_to_total(ora, nparts):
+def test_row_block_parts_sum_to_total(ora, nparts, shape):
     """Row-block sharding (the multi-GPU split): the nparts partial maps of
     Context.run_rows sum to the reference's total_viewshed_raw (per-cell sum
     order differs, so within 1e-12 relative; one part is bit-exact)."""
     import torch
 
-    vals = sk.make_synthetic(sk.SyntheticKind.Fractal, 72, 60, 10.0, 9).values
+    vals = sk.make_synthetic(sk.SyntheticKind.Fractal, *shape, 10.0, 9).values
     cfg = sk.RunConfig(ns=24, h0=1.5, units=sk.Units.SquareMeters)
     ref = ora.total_viewshed(vals, 10.0, 24, 1.5, raw=True)
     ctx = sk.Context(0)

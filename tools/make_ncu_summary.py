@@ -27,7 +27,7 @@ def val(d, k):
 
 
 names = {"scan2_kernel": "scan_kernel", "scan3_kernel": "scan_kernel", "relocate_kernel": "relocate_kernel",
-         "unskew_pipe_kernel": "unskew_kernel",
+         "unskew_pipe_kernel": "unskew_kernel", "unskew_tma_kernel": "unskew_kernel",
          "fixup_kernel": "fixup_kernel"}
 out = {"source": note}
 for d in data:
