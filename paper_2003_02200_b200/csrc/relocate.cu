@@ -63,6 +63,26 @@ constexpr int kMaxBoxes = 4;                // n_src <= kTQ + kTJ + 1 = 97 (+3 o
 #endif
 constexpr int kStages = SKS_RELOC_STAGES;   // tiles in flight per CTA (kStages - 1 prefetched)
 constexpr int kOutLd = kTJ + 1;             // padded output tile (transposed sectors)
+#ifndef SKS_RELOC_VZERO
+#define SKS_RELOC_VZERO 1  // cv zeroing (and transposed-tile rows) as 16-byte stores: a quarter of the store instructions
+#endif
+
+// cv zeroing of warp w's 8 tile rows (q0 + 8w ..): 8 lanes x 16 B per
+// 128-byte row, two rows per lane; rows past the sector's skewed rows are
+// left alone (the last sector's rows end the pool). j0 + 32 <= pitch always
+// (j0 is a multiple of 32 below cols <= pitch, a multiple of 32).
+template <bool kInterior>
+__device__ __forceinline__ void zero_cv_rows(int* cv, size_t row0_off, int pitch, int q_first, int skw_rows,
+                                             int lane) {
+#pragma unroll
+  for (int k = 0; k < 2; ++k) {
+    const int rr = 4 * k + (lane >> 3);
+    if (kInterior || q_first + rr < skw_rows) {
+      __stcs(reinterpret_cast<int4*>(cv + row0_off + static_cast<size_t>(rr) * pitch + 4 * (lane & 7)),
+             make_int4(0, 0, 0, 0));
+    }
+  }
+}
 
 // Geometry of one output tile (t = sector * tiles_total + tile); s < 0: end.
 struct Tile {
@@ -173,11 +193,18 @@ __device__ __forceinline__ void plain_tile(const Tile& g, const SectorDev& sd, c
     }
     if (kInterior || (store_col && g.q0 + r0 + u < skw_rows)) {
       __stcs(po, acc);
+#if !SKS_RELOC_VZERO
       __stcs(pc, 0);
+#endif
     }
     po += pitch;
     pc += pitch;
   }
+#if SKS_RELOC_VZERO
+  (void)pc;
+  zero_cv_rows<kInterior>(b.cv + sd.sdem_off, static_cast<size_t>(g.q0 + r0) * pitch + g.j0, pitch, g.q0 + r0,
+                          skw_rows, lane);
+#endif
 }
 
 // Transposed sector: lane = output row r = 32*(warp&1) + lane, columns
@@ -187,12 +214,12 @@ __device__ __forceinline__ void plain_tile(const Tile& g, const SectorDev& sd, c
 template <bool kInterior>
 __device__ __forceinline__ void transposed_tile(const Tile& g, const SectorDev& sd, const BatchDev& b,
                                                 const float* box, float* outs, int lane, int warp) {
+  const int* dest = b.dest + sd.col_off + g.j0;
+  const float* fracf = b.fracf + sd.col_off + g.j0;
   const int base = sd.base, rows = sd.rows;
   const int m1 = sd.map[1], m2 = sd.map[2], m3 = sd.map[3], m5 = sd.map[5];
   const int r = 32 * (warp & 1) + lane;
   const int c0 = 8 * (warp >> 1);
-  const int* dest = b.dest + sd.col_off + g.j0;
-  const float* fracf = b.fracf + sd.col_off + g.j0;
 #pragma unroll 4
   for (int cc = 0; cc < 8; ++cc) {
     const int c = c0 + cc;
@@ -222,7 +249,7 @@ __device__ __forceinline__ void transposed_tile(const Tile& g, const SectorDev& 
 // wait on full[st], compute and store the tile, and release the stage
 // (empty[st]), so the producer's geometry walk and the copies overlap the
 // consumers' work.
-__global__ void __launch_bounds__(kConsumers + 32) relocate_kernel(const __grid_constant__ CUtensorMap tm,
+__global__ void __launch_bounds__(kConsumers + 32, 5) relocate_kernel(const __grid_constant__ CUtensorMap tm,
                                                                    BatchDev b, int tiles_x, int tiles_total) {
   extern __shared__ __align__(128) unsigned char smem_raw[];
   RelocSmem& sm = *reinterpret_cast<RelocSmem*>(smem_raw);
@@ -295,6 +322,21 @@ __global__ void __launch_bounds__(kConsumers + 32) relocate_kernel(const __grid_
       const int pitch = sd.pitch, skw_rows = sd.skw_rows;
       float* out = b.sdem + sd.sdem_off;
       int* cvz = b.cv + sd.sdem_off;
+#if SKS_RELOC_VZERO
+      // rows as 16-byte stores: lane -> row 8w + 4k + lane/8, columns 4*(lane%8) ..
+      const size_t o0 = static_cast<size_t>(g.q0 + 8 * warp) * pitch + g.j0;
+#pragma unroll
+      for (int k = 0; k < 2; ++k) {
+        const int rr = 4 * k + (lane >> 3), c4 = 4 * (lane & 7);
+        const int rt = 8 * warp + rr;
+        if (g.interior || g.q0 + rt < skw_rows) {
+          const float* src = sm.out + rt * kOutLd + c4;
+          __stcs(reinterpret_cast<float4*>(out + o0 + static_cast<size_t>(rr) * pitch + c4),
+                 make_float4(src[0], src[1], src[2], src[3]));
+        }
+      }
+      zero_cv_rows<false>(cvz, o0, pitch, g.q0 + 8 * warp, skw_rows, lane);
+#else
       const size_t o0 = static_cast<size_t>(g.q0 + 8 * warp) * pitch + g.j0 + lane;
 #pragma unroll
       for (int rr = 0; rr < 8; ++rr) {
@@ -305,6 +347,7 @@ __global__ void __launch_bounds__(kConsumers + 32) relocate_kernel(const __grid_
           __stcs(cvz + o, 0);
         }
       }
+#endif
       consumer_sync();  // output tile free
     }
   }
