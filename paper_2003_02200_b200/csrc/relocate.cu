@@ -267,19 +267,23 @@ __global__ void __launch_bounds__(kConsumers + 32, 5) relocate_kernel(const __gr
     if (lane != 0) return;
     const int n_all = b.n_sectors * tiles_total;
     int t = blockIdx.x;
+    // the next tile's geometry (its descriptor and dest loads) is found
+    // before waiting for a free stage, so that latency overlaps the wait
+    Tile g;
+    auto next_tile = [&]() {
+      for (; t < n_all; t += gridDim.x) {
+        if (tile_geom(b, tiles_x, tiles_total, t, g)) return;
+      }
+    };
+    next_tile();
     for (int n = 0;; ++n) {
       const int st = n % kStages;
       mbar_wait(&sm.empty[st], (static_cast<unsigned>(n / kStages) & 1u) ^ 1u);
-      Tile g;
-      for (; t < n_all; t += gridDim.x) {
-        if (tile_geom(b, tiles_x, tiles_total, t, g)) break;
-      }
       if (t >= n_all) {
         sm.tile[st].s = -1;
         mbar_arrive(&sm.full[st]);
         return;
       }
-      t += gridDim.x;
       sm.tile[st] = g;
       // the stage was last read through the generic proxy
       fence_proxy_async();
@@ -292,6 +296,8 @@ __global__ void __launch_bounds__(kConsumers + 32, 5) relocate_kernel(const __gr
           tma_load_2d(dst, &tm, g.J0 + k * kBoxLong, g.S0, &sm.full[st]);
         }
       }
+      t += gridDim.x;
+      next_tile();
     }
   }
   for (int n = 0;; ++n) {
