@@ -467,6 +467,13 @@ __global__ void __launch_bounds__(kUThreads, SKS_UNSKEW_TMA_MINB) unskew_tma_ker
         const int p_max = base + i_hi - d_lo;
         if (max(p_min, q_lo) > min(p_max, q_hi - 1)) continue;
       }
+      // the box must hold every row the tile reads: rows p - 1 .. p of pre-op
+      // rows i_lo .. i_hi over columns j_lo .. j_hi (unskew_box_rows' bound);
+      // a violation would read a neighbour's rows, so it stops the kernel
+      if (i_hi - i_lo + 2 + d_hi - __double2int_rz(__dmul_rn(tan, static_cast<double>(j_lo))) >
+          unskew_box_rows(tan)) {
+        __trap();
+      }
       const int slot = n % kStages;
       UStage& S = acquire(slot);
       {
