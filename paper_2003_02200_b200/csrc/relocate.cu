@@ -44,7 +44,12 @@ namespace sks {
 
 namespace {
 
-constexpr int kTQ = 64;  // output rows per tile
+#ifndef SKS_RELOC_TQ
+#define SKS_RELOC_TQ 64  // measured (config 2 / 4): 32 rows 0.98 / 4.40 ms (3 stages 1.01 / 4.90), 64 rows 0.77 / 3.76, 128 rows 0.78 / 3.67
+#endif
+constexpr int kTQ = SKS_RELOC_TQ;  // output rows per tile (64 or 32)
+static_assert(kTQ == 32 || kTQ == 64 || kTQ == 128, "8 consumer warps: 4, 8 or 16 rows each");
+constexpr int kRW = kTQ / 8;       // rows per consumer warp (plain tiles, stores)
 constexpr int kTJ = 32;  // output columns per tile (narrow: the parallelogram overhang grows with the width)
 constexpr int kConsumers = 256;  // 8 consumer warps (+ 1 producer warp)
 constexpr int kBoxLong = 32;  // source cells per box along the parallelogram's long side
@@ -57,7 +62,7 @@ constexpr int kBoxLong = 32;  // source cells per box along the parallelogram's 
 // serves source columns 32k .. 32k + 31 of the aligned start).
 constexpr int kBW = kBoxLong + 4;           // box columns
 constexpr int kBoxFloats = kBW * kBoxLong;  // 4.5 KB (a multiple of 128 B)
-constexpr int kMaxBoxes = 4;                // n_src <= kTQ + kTJ + 1 = 97 (+3 of alignment) -> 4
+constexpr int kMaxBoxes = (kTQ + kTJ + 4 + kBoxLong - 1) / kBoxLong;  // n_src <= kTQ + kTJ + 1 (+3 of alignment)
 #ifndef SKS_RELOC_STAGES
 #define SKS_RELOC_STAGES 2  // measured (config 2): 2 stages 0.95 ms, 3 1.01, 4 1.18, 6 1.92 (CTAs per SM matter more than depth)
 #endif
@@ -75,7 +80,7 @@ template <bool kInterior>
 __device__ __forceinline__ void zero_cv_rows(int* cv, size_t row0_off, int pitch, int q_first, int skw_rows,
                                              int lane) {
 #pragma unroll
-  for (int k = 0; k < 2; ++k) {
+  for (int k = 0; k < kRW / 4; ++k) {
     const int rr = 4 * k + (lane >> 3);
     if (kInterior || q_first + rr < skw_rows) {
       __stcs(reinterpret_cast<int4*>(cv + row0_off + static_cast<size_t>(rr) * pitch + 4 * (lane & 7)),
@@ -163,7 +168,7 @@ __device__ __forceinline__ void plain_tile(const Tile& g, const SectorDev& sd, c
   const int base = sd.base, rows = sd.rows, pitch = sd.pitch, skw_rows = sd.skw_rows;
   const int m0 = sd.map[0], m2 = sd.map[2], m4 = sd.map[4], m5 = sd.map[5];
   const int c = lane;
-  const int r0 = 8 * warp;
+  const int r0 = kRW * warp;
   const bool colok = kInterior || c < g.jn;
   const float f = colok ? __ldg(b.fracf + sd.col_off + g.j0 + c) : 0.f;
   const float a = __fsub_rn(1.0f, f);
@@ -171,9 +176,9 @@ __device__ __forceinline__ void plain_tile(const Tile& g, const SectorDev& sd, c
   const int col = m4 * (g.j0 + c) + m5 - g.J0;
   const int rstep = kBW * m0;
   int idx = (m0 * im0 + m2 - g.S0) * kBW + col;
-  float sv[9];
+  float sv[kRW + 1];
 #pragma unroll
-  for (int u = 0; u < 9; ++u) {
+  for (int u = 0; u < kRW + 1; ++u) {
     const int im = im0 + u;
     sv[u] = (kInterior || (colok && im >= 0 && im < rows)) ? box[idx] : 0.f;
     idx += rstep;
@@ -182,7 +187,7 @@ __device__ __forceinline__ void plain_tile(const Tile& g, const SectorDev& sd, c
   int* pc = b.cv + sd.sdem_off + static_cast<size_t>(g.q0 + r0) * pitch + g.j0 + c;
   const bool store_col = kInterior || g.j0 + c < pitch;
 #pragma unroll
-  for (int u = 0; u < 8; ++u) {
+  for (int u = 0; u < kRW; ++u) {
     const int im = im0 + u;
     float acc = 0.0f;
     if (kInterior) {
@@ -218,10 +223,13 @@ __device__ __forceinline__ void transposed_tile(const Tile& g, const SectorDev& 
   const float* fracf = b.fracf + sd.col_off + g.j0;
   const int base = sd.base, rows = sd.rows;
   const int m1 = sd.map[1], m2 = sd.map[2], m3 = sd.map[3], m5 = sd.map[5];
-  const int r = 32 * (warp & 1) + lane;
-  const int c0 = 8 * (warp >> 1);
+  // lane = one of 32 output rows of a row group (kTQ / 32 groups), the
+  // group's 8 / groups warps split the 32 columns (64-row tiles: 8 each)
+  constexpr int kGroups = kTQ / 32, kCW = 4 * kGroups;
+  const int r = 32 * (warp % kGroups) + lane;
+  const int c0 = kCW * (warp / kGroups);
 #pragma unroll 4
-  for (int cc = 0; cc < 8; ++cc) {
+  for (int cc = 0; cc < kCW; ++cc) {
     const int c = c0 + cc;
     float acc = 0.0f;
     if (kInterior || c < g.jn) {
@@ -249,7 +257,10 @@ __device__ __forceinline__ void transposed_tile(const Tile& g, const SectorDev& 
 // wait on full[st], compute and store the tile, and release the stage
 // (empty[st]), so the producer's geometry walk and the copies overlap the
 // consumers' work.
-__global__ void __launch_bounds__(kConsumers + 32, 5) relocate_kernel(const __grid_constant__ CUtensorMap tm,
+#ifndef SKS_RELOC_MINB
+#define SKS_RELOC_MINB 5
+#endif
+__global__ void __launch_bounds__(kConsumers + 32, SKS_RELOC_MINB) relocate_kernel(const __grid_constant__ CUtensorMap tm,
                                                                    BatchDev b, int tiles_x, int tiles_total) {
   extern __shared__ __align__(128) unsigned char smem_raw[];
   RelocSmem& sm = *reinterpret_cast<RelocSmem*>(smem_raw);
@@ -330,23 +341,23 @@ __global__ void __launch_bounds__(kConsumers + 32, 5) relocate_kernel(const __gr
       int* cvz = b.cv + sd.sdem_off;
 #if SKS_RELOC_VZERO
       // rows as 16-byte stores: lane -> row 8w + 4k + lane/8, columns 4*(lane%8) ..
-      const size_t o0 = static_cast<size_t>(g.q0 + 8 * warp) * pitch + g.j0;
+      const size_t o0 = static_cast<size_t>(g.q0 + kRW * warp) * pitch + g.j0;
 #pragma unroll
-      for (int k = 0; k < 2; ++k) {
+      for (int k = 0; k < kRW / 4; ++k) {
         const int rr = 4 * k + (lane >> 3), c4 = 4 * (lane & 7);
-        const int rt = 8 * warp + rr;
+        const int rt = kRW * warp + rr;
         if (g.interior || g.q0 + rt < skw_rows) {
           const float* src = sm.out + rt * kOutLd + c4;
           __stcs(reinterpret_cast<float4*>(out + o0 + static_cast<size_t>(rr) * pitch + c4),
                  make_float4(src[0], src[1], src[2], src[3]));
         }
       }
-      zero_cv_rows<false>(cvz, o0, pitch, g.q0 + 8 * warp, skw_rows, lane);
+      zero_cv_rows<false>(cvz, o0, pitch, g.q0 + kRW * warp, skw_rows, lane);
 #else
-      const size_t o0 = static_cast<size_t>(g.q0 + 8 * warp) * pitch + g.j0 + lane;
+      const size_t o0 = static_cast<size_t>(g.q0 + kRW * warp) * pitch + g.j0 + lane;
 #pragma unroll
-      for (int rr = 0; rr < 8; ++rr) {
-        const int rt = 8 * warp + rr;
+      for (int rr = 0; rr < kRW; ++rr) {
+        const int rt = kRW * warp + rr;
         if (g.interior || (g.q0 + rt < skw_rows && g.j0 + lane < pitch)) {
           const size_t o = o0 + static_cast<size_t>(rr) * pitch;
           __stcs(out + o, sm.out[rt * kOutLd + lane]);
